@@ -1,0 +1,166 @@
+/*
+ * pbsm.h — C ABI of the B200-native PBSM filter step (arXiv 1908.11740).
+ *
+ * This is the drop-in boundary for the reference's kernel plugin protocol
+ * (`backends.get_kernels(name)` → module of six kernels,
+ * /root/reference/pkg/src/sweepjoin/backends.py:41-50, kernels in
+ * /root/reference/pkg/src/sweepjoin/_kernels.pyx).  The reference calls its
+ * kernels once per input slice or per tile (10^4–10^7 calls); a GPU cannot
+ * amortise launches at that granularity, so this ABI is *join-granular*: each
+ * entry point below replaces one reference kernel for ALL tiles at once.
+ *
+ *   reference kernel (file:line)                      → entry point here
+ *   count_tiles      _kernels.pyx:34-58               → pbsm_count
+ *   compute_segment_offsets partition.py:151-164      → pbsm_plan
+ *   (+ build_task_queue engine.py:84-100)
+ *   write_tiles      _kernels.pyx:61-98               → pbsm_scatter
+ *   (+ overflow guard partition.py:229-233)
+ *   sort_segment     _kernels.pyx:188-228  ┐
+ *   sweep_count      _kernels.pyx:304-315  ├─fused──→ pbsm_join_count
+ *   sweep_collect    _kernels.pyx:318-341  ┘          pbsm_join_emit
+ *   (+ aggregation   engine.py:293-309)
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer owned by the caller (PyTorch in the
+ *     shipped host code); the library never allocates device memory and keeps
+ *     no global mutable state, so it is safe on any device/stream.
+ *   - `stream` is a cudaStream_t passed as void*; every entry point only
+ *     enqueues work on it (no implicit synchronisation) except
+ *     pbsm_read_header, which is the one documented host sync point.
+ *   - Return value: 0 = OK, >0 = cudaError_t of a failed launch, <0 = PBSM_E_*.
+ *   - Coordinates are float64 in [0,1] (the reference's normalised domain,
+ *     geometry.py:1-6); inputs are the reference's SoA columns
+ *     (ids int64, xl, xu, yl, yu float64 — geometry.py:109-130).
+ *   - Grid: kx columns × ky rows; flat tile = row*kx + col
+ *     (partition.py:53-69).  2D grid: kx = ky = K.  1D stripes along x:
+ *     kx = K, ky = 1; along y: kx = 1, ky = K.  A strip (multi-GPU shard)
+ *     is the tile-row range [row_lo, row_hi); single GPU: [0, ky).
+ */
+#ifndef PBSM_H_
+#define PBSM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBSM_ABI_VERSION 1
+
+/* library error codes (negative) */
+#define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
+#define PBSM_E_OVERFLOW   (-2)  /* partition write overflow (partition.py:229-233)  */
+#define PBSM_E_TOO_LARGE  (-3)  /* a total exceeds the 32-bit offset range           */
+#define PBSM_E_PAIRS      (-4)  /* pair buffer smaller than the counted result       */
+
+/* device-side error bits, reported in pbsm_header.error */
+#define PBSM_ERR_SCATTER_OVERFLOW  1u  /* a scatter cursor left its tile range       */
+#define PBSM_ERR_OFFSET_MISMATCH   2u  /* count and write passes disagree            */
+#define PBSM_ERR_TOTAL_RANGE       4u  /* A_R / A_S / W exceed 2^32-1                 */
+#define PBSM_ERR_PAIR_OVERFLOW     8u  /* emit past the pair capacity                 */
+
+/* one tile-list entry: the rectangle's MBR.  The two top bits of `xl`
+ * (always zero for a float64 in [0,1]) carry the class label of the entry in
+ * its tile: bit 63 = x-out (starts left of the tile), bit 62 = y-out (starts
+ * below the tile).  A = neither, B = y-out, C = x-out, D = both — the class
+ * scheme of PAPER.md:651-733. */
+typedef struct pbsm_entry {
+  uint64_t xl_key;
+  double xu, yl, yu;
+} pbsm_entry;
+
+/* plan/result totals, device-resident at the start of the workspace */
+typedef struct pbsm_header {
+  int64_t a_r;            /* Σ per-tile R counts = PartitionedDataset.total_assigned */
+  int64_t a_s;            /* same for S                                             */
+  int64_t n_join;         /* tiles with both inputs non-empty, chunk path           */
+  int64_t w_join;         /* entries (R+S) in those tiles                           */
+  int64_t n_chunks;       /* CTA work units of the chunk path                       */
+  int64_t n_large;        /* join tiles too large for one CTA's shared memory       */
+  int64_t n_items;        /* work items of the large-tile path                      */
+  int64_t pairs;          /* result_count, valid after pbsm_join_count              */
+  int64_t max_tile;       /* largest |R_T|+|S_T| over join tiles                   */
+  int64_t join_tiles_all; /* n_join + n_large                                       */
+  uint32_t error;         /* PBSM_ERR_* bits                                        */
+  uint32_t pad;
+  int64_t reserved[5];
+} pbsm_header;
+
+/* Bytes of the grid workspace for a kx × (row_hi-row_lo) strip. */
+int64_t pbsm_workspace_bytes(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi);
+
+/* Zero counters and build the exact tile-boundary tables i/k
+ * (geometry.py:82-84).  Must precede pbsm_count for each join. */
+int pbsm_init(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+              void* stream);
+
+/* count_tiles (_kernels.pyx:34-58) for ALL n rectangles of one input
+ * (side 0 = R, 1 = S): per-tile assignment counts in the workspace. */
+int pbsm_count(const double* xl, const double* xu, const double* yl,
+               const double* yu, int64_t n, int32_t side, void* ws,
+               int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+               void* stream);
+
+/* compute_segment_offsets (partition.py:151-164) for both inputs plus the
+ * join-task plan (build_task_queue, engine.py:84-100): CSR offsets, the list
+ * of join tiles, their CTA chunks and the large-tile work items. */
+int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+              void* stream);
+
+/* Copy the device header to *out and synchronise the stream. */
+int pbsm_read_header(void* ws, pbsm_header* out, void* stream);
+
+/* write_tiles (_kernels.pyx:61-98) for ALL n rectangles of one input:
+ * scatter each rectangle into the list of every tile it overlaps, labelled
+ * with its class there.  `out` / `out_ids` hold `capacity` entries
+ * (= header.a_r or a_s). */
+int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu,
+                 const double* yl, const double* yu, int64_t n, int32_t side,
+                 void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                 pbsm_entry* out, int64_t* out_ids, int64_t capacity,
+                 void* stream);
+
+/* Scratch bytes for the join passes (per-unit pair counts + scan). */
+int64_t pbsm_join_scratch_bytes(int64_t n_chunks, int64_t n_items);
+
+/* sort_segment + sweep_count (_kernels.pyx:188-228, 231-315) for every join
+ * tile: per-tile segmented sort by x-lower and forward-scan mini-joins over
+ * the class combinations; writes per-unit counts, their exclusive scan and
+ * header.pairs (= JoinReport.result_count). */
+int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                    const pbsm_entry* r_list, const pbsm_entry* s_list,
+                    int64_t n_chunks, int64_t n_items, void* scratch,
+                    void* stream);
+
+/* sweep_collect (_kernels.pyx:318-341): re-runs the sort + sweep and writes
+ * each pair (r_id, s_id) as two int64 at pairs[2*(base+i)] for
+ * i < header.pairs, base = pair_base.  Requires pbsm_join_count's scratch. */
+int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                   const pbsm_entry* r_list, const int64_t* r_ids,
+                   const pbsm_entry* s_list, const int64_t* s_ids,
+                   int64_t n_chunks, int64_t n_items, const void* scratch,
+                   int64_t* pairs, int64_t pair_base, int64_t capacity,
+                   void* stream);
+
+/* ε-distance refinement (engine.py:201-206, 298-300) of candidate pairs given
+ * as ROW indices (cand[2i], cand[2i+1]) into the point arrays p / q: keeps the
+ * pairs with dx*dx + dy*dy <= eps_sq (no FMA contraction, numpy rounding) and
+ * writes their (p_ids, q_ids) compacted, in candidate order, to out (capacity
+ * n_cand pairs).  The kept count is the int64 at byte offset
+ * pbsm_refine_result_offset(n_cand) of scratch. */
+int64_t pbsm_refine_scratch_bytes(int64_t n_cand);
+int64_t pbsm_refine_result_offset(int64_t n_cand);
+int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const double* py,
+                const double* qx, const double* qy, const int64_t* p_ids, const int64_t* q_ids,
+                double eps_sq, void* scratch, int64_t* out, void* stream);
+
+/* ABI version / build identification */
+int32_t pbsm_abi_version(void);
+const char* pbsm_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBSM_H_ */

@@ -1,0 +1,114 @@
+"""ctypes binding of the C ABI in ``include/pbsm.h`` (``_lib/libpbsm.so``).
+
+There is deliberately no fallback: if the library is missing or fails to
+load, every join raises ``KernelError``.  Pointers are passed as raw device
+addresses (``tensor.data_ptr()``) and the stream as the raw ``cudaStream_t``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+from ._build import LIB_PATH
+from .errors import KernelError
+
+ABI_VERSION = 1
+
+# error bits of pbsm_header.error (include/pbsm.h)
+ERR_SCATTER_OVERFLOW = 1
+ERR_OFFSET_MISMATCH = 2
+ERR_TOTAL_RANGE = 4
+ERR_PAIR_OVERFLOW = 8
+
+EXPORTED = (
+    "pbsm_abi_version", "pbsm_build_info", "pbsm_workspace_bytes", "pbsm_init",
+    "pbsm_count", "pbsm_plan", "pbsm_read_header", "pbsm_scatter",
+    "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit",
+    "pbsm_refine_scratch_bytes", "pbsm_refine_result_offset", "pbsm_refine",
+)
+
+
+class Header(C.Structure):
+    """Mirror of ``pbsm_header``."""
+
+    _fields_ = [
+        ("a_r", C.c_int64), ("a_s", C.c_int64), ("n_join", C.c_int64),
+        ("w_join", C.c_int64), ("n_chunks", C.c_int64), ("n_large", C.c_int64),
+        ("n_items", C.c_int64), ("pairs", C.c_int64), ("max_tile", C.c_int64),
+        ("join_tiles_all", C.c_int64), ("error", C.c_uint32), ("pad", C.c_uint32),
+        ("reserved", C.c_int64 * 5),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_
+                if name not in ("pad", "reserved")}
+
+
+_lock = threading.Lock()
+_lib = None
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+
+_SIGNATURES = {
+    "pbsm_abi_version": (_I32, []),
+    "pbsm_build_info": (C.c_char_p, []),
+    "pbsm_workspace_bytes": (_I64, [_I32, _I32, _I32, _I32]),
+    "pbsm_init": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
+    "pbsm_count": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P]),
+    "pbsm_plan": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
+    "pbsm_read_header": (C.c_int, [_P, C.POINTER(Header), _P]),
+    "pbsm_scatter": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32,
+                               _P, _P, _I64, _P]),
+    "pbsm_join_scratch_bytes": (_I64, [_I64, _I64]),
+    "pbsm_join_count": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I64, _I64, _P, _P]),
+    "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _I64, _I64, _P,
+                                 _P, _I64, _I64, _P]),
+    "pbsm_refine_scratch_bytes": (_I64, [_I64]),
+    "pbsm_refine_result_offset": (_I64, [_I64]),
+    "pbsm_refine": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),
+}
+
+
+def load(path=None):
+    """Load (once) and return the CDLL; raises KernelError if unavailable."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = str(path or LIB_PATH)
+        try:
+            lib = C.CDLL(p)
+        except OSError as exc:
+            raise KernelError(
+                f"CUDA library {p} is not loadable ({exc}); run __graft_entry__.build() "
+                "— there is no CPU fallback") from exc
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.pbsm_abi_version() != ABI_VERSION:
+            raise KernelError("libpbsm ABI version mismatch; rebuild the library")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise KernelError(f"{what} failed with code {rc}")
+
+
+def describe_error(bits: int) -> str:
+    names = []
+    if bits & ERR_SCATTER_OVERFLOW:
+        names.append("scatter overflow")
+    if bits & ERR_OFFSET_MISMATCH:
+        names.append("count/write offset mismatch")
+    if bits & ERR_TOTAL_RANGE:
+        names.append("total exceeds 32-bit offsets")
+    if bits & ERR_PAIR_OVERFLOW:
+        names.append("pair buffer overflow")
+    return ", ".join(names) or f"bits {bits:#x}"

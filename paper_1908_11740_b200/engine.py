@@ -1,0 +1,199 @@
+"""Drop-in join API: ``join`` / ``epsilon_distance_join`` on the B200.
+
+Same entry points, configuration object, report object and error behaviour
+as the reference engine (/root/reference/pkg/src/sweepjoin/engine.py:35-70,
+103-120, 312-353); the whole filter step runs in the sm_100a library
+(``device.run_join``).  ``axis_policy``, ``threads``, ``phi``, ``k_buckets``
+and ``backend`` are validated exactly like the reference and otherwise
+ignored: the sweep axis and thread count never change the result set
+(sweep.py:131-132), and there is one backend.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Literal, Sequence
+
+import numpy as np
+import torch
+
+from . import device as dev
+from .errors import ConfigError, KernelError
+from .geometry import Rect, RectBatch, as_batch
+from .partition import MAX_DEVICE_K, PartitionLayout
+
+AxisPolicyName = Literal["x", "y", "adaptive", "auto"]
+
+__all__ = ["JoinConfig", "JoinReport", "epsilon_distance_join", "join", "join_device",
+           "squares"]
+
+
+@dataclass
+class JoinConfig:
+    """Parameters of one join (engine.py:35-52 in the reference).
+
+    ``devices`` is new: the number of GPUs of a strip-sharded join (see
+    ``parallel.py``); the single-process ``join`` uses the current device.
+    """
+
+    layout: PartitionLayout
+    axis_policy: AxisPolicyName | None = None
+    threads: int = 1
+    sink_mode: Literal["count-only", "collect-pairs"] = "count-only"
+    phi: int | None = None
+    k_buckets: int | None = None
+    backend: str | None = None
+    devices: int = 1
+
+
+@dataclass
+class JoinReport:
+    """Result size, optional ``(n, 2)`` int64 (r_id, s_id) pairs and phase times.
+
+    Field meanings follow engine.py:55-70.  ``sort_time`` is 0.0: the
+    per-tile sort is fused into the join kernels and accounted in
+    ``join_time``.  ``task_sizes`` (|R_T|+|S_T| of every join tile, largest
+    first) is materialised from the device on first access.
+    """
+
+    result_count: int
+    pairs: np.ndarray | None
+    partition_time: float
+    sort_time: float
+    join_time: float
+    total_time: float
+    _task_sizes: object = field(default=None, repr=False)
+
+    @property
+    def task_sizes(self) -> np.ndarray | None:
+        ts = self._task_sizes
+        if callable(ts):
+            ts = self._task_sizes = ts()
+        return ts
+
+
+def _resolve_policy(cfg: JoinConfig) -> str:
+    """Config validation with the reference's messages (engine.py:103-120)."""
+    if cfg.threads < 1:
+        raise ConfigError("threads must be >= 1")
+    if cfg.sink_mode not in ("count-only", "collect-pairs"):
+        raise ConfigError(f"unknown sink mode {cfg.sink_mode!r}")
+    if cfg.phi is not None and cfg.phi < 1:
+        raise ConfigError("phi must be >= 1")
+    if cfg.k_buckets is not None and cfg.k_buckets < 1:
+        raise ConfigError("k_buckets must be >= 1")
+    policy = cfg.axis_policy
+    if policy is None:
+        policy = "auto" if cfg.layout.kind == "1d" else "adaptive"
+    if policy not in ("x", "y", "adaptive", "auto"):
+        raise ConfigError(f"unknown axis policy {policy!r}")
+    if policy == "auto" and cfg.layout.kind != "1d":
+        raise ConfigError("axis policy 'auto' applies to 1D stripes only; "
+                          "use 'adaptive' for grids")
+    if cfg.backend not in (None, "cuda", "b200"):
+        raise ValueError(f"unknown backend {cfg.backend!r}; available: ('cuda',)")
+    if cfg.layout.k > MAX_DEVICE_K:
+        raise ConfigError(f"k={cfg.layout.k} exceeds the device limit {MAX_DEVICE_K}")
+    if cfg.devices < 1:
+        raise ConfigError("devices must be >= 1")
+    return policy
+
+
+def _require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise KernelError("no CUDA device: the B200 join has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _task_sizes_fn(r: dev.DeviceRects, s: dev.DeviceRects, kx: int, ky: int):
+    def compute():
+        # recount per tile (cheap) so the report does not pin the workspace
+        res = dev.run_join(r, s, kx, ky, collect=False, keep_counts=True)
+        cr, cs = (c.to(torch.int64) for c in res.tile_counts)
+        both = (cr > 0) & (cs > 0)
+        sizes = (cr + cs)[both]
+        return torch.sort(sizes, descending=True).values.cpu().numpy()
+    return compute
+
+
+def join_device(r: dev.DeviceRects, s: dev.DeviceRects, cfg: JoinConfig,
+                timing: bool = False) -> dev.DeviceJoinResult:
+    """Device-resident join: inputs and the pair tensor stay in HBM."""
+    _resolve_policy(cfg)
+    kx, ky = cfg.layout.grid
+    return dev.run_join(r, s, kx, ky, collect=cfg.sink_mode == "collect-pairs", timing=timing)
+
+
+def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) -> JoinReport:
+    collect_user = cfg.sink_mode == "collect-pairs"
+    if len(r) == 0 or len(s) == 0:
+        return JoinReport(0, np.empty((0, 2), dtype=np.int64) if collect_user else None,
+                          0.0, 0.0, 0.0, time.perf_counter() - t0,
+                          np.empty(0, dtype=np.int64))
+    device = _require_cuda()
+    rd = dev.to_device(r, device)
+    sd = rd if s is r else dev.to_device(s, device)
+    kx, ky = cfg.layout.grid
+    res = dev.run_join(rd, sd, kx, ky, collect=collect_user or refine is not None, timing=True)
+    count, pairs = res.count, res.pairs
+    if refine is not None:
+        count, pairs = refine(res.pairs)
+    out = None
+    if collect_user:
+        out = pairs.cpu().numpy() if count else np.empty((0, 2), dtype=np.int64)
+    t = res.times
+    return JoinReport(
+        result_count=int(count), pairs=out,
+        partition_time=t.get("partition", 0.0), sort_time=0.0,
+        join_time=t.get("join_count", 0.0) + t.get("emit", 0.0),
+        total_time=time.perf_counter() - t0,
+        _task_sizes=_task_sizes_fn(rd, sd, kx, ky))
+
+
+def join(r: RectBatch | Sequence[Rect], s: RectBatch | Sequence[Rect],
+         cfg: JoinConfig) -> JoinReport:
+    """Every intersecting (r, s) pair of R × S exactly once (engine.py:312-323)."""
+    r, s = as_batch(r), as_batch(s)
+    _resolve_policy(cfg)
+    r.validate()
+    s.validate()
+    return _run(r, s, cfg, time.perf_counter())
+
+
+def squares(batch: RectBatch, eps: float, ids: np.ndarray | None = None) -> RectBatch:
+    """Side-``eps`` squares around the lower corners, clipped to [0, 1].
+
+    Exactly the numpy arithmetic of engine.py:342-350 (half = eps / 2.0).
+    ``ids`` defaults to row indices, as the reference uses for refinement.
+    """
+    half = eps / 2.0
+    return RectBatch(
+        np.arange(len(batch), dtype=np.int64) if ids is None else ids,
+        np.clip(batch.xl - half, 0.0, 1.0), np.clip(batch.xl + half, 0.0, 1.0),
+        np.clip(batch.yl - half, 0.0, 1.0), np.clip(batch.yl + half, 0.0, 1.0))
+
+
+def epsilon_distance_join(p: RectBatch | Sequence[Rect], q: RectBatch | Sequence[Rect],
+                          eps: float, cfg: JoinConfig) -> JoinReport:
+    """Point pairs within distance ``eps`` exactly once (engine.py:326-353).
+
+    Candidates come from the square join; the distance test
+    ``dx*dx + dy*dy <= eps*eps`` runs on the device without FMA contraction
+    (numpy rounds every operation, engine.py:201-206).
+    """
+    if not eps > 0.0:
+        raise ConfigError(f"epsilon must be positive, got {eps!r}")
+    p, q = as_batch(p), as_batch(q)
+    _resolve_policy(cfg)
+    p.validate()
+    q.validate()
+    t0 = time.perf_counter()
+    sp = squares(p, eps)
+    sq = sp if q is p else squares(q, eps)
+
+    def refine(cand: torch.Tensor):
+        from .refine import refine_distance
+        return refine_distance(cand, p, q, eps * eps)
+
+    return _run(sp, sq, cfg, t0, refine=refine)

@@ -1,0 +1,191 @@
+"""GPU parity: the sm_100a path through the C ABI vs the oracle and the reference.
+
+Bit-exact bar: identical result_count and identical lexicographically sorted
+(r_id, s_id) lists.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1908_11740_b200 as pb
+from paper_1908_11740_b200 import device as dev
+from paper_1908_11740_b200.synth import CONFIGS, make_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _case_list(golden):
+    for row in golden["instances"]["cases"]:
+        tag, kind, k, axis, self_join, count = str(row).split(",")
+        yield tag, kind, int(k), int(axis), bool(int(self_join)), int(count)
+
+
+def _side(g, tag, side):
+    return pb.RectBatch(*(g[f"{tag}_{side}_{c}"] for c in ("ids", "xl", "xu", "yl", "yu")))
+
+
+def _collect(kind, k, axis=0):
+    return pb.JoinConfig(pb.PartitionLayout(kind, k, pb.Axis(axis)), sink_mode="collect-pairs")
+
+
+def test_reference_instances_bit_exact(golden):
+    g = golden["instances"]
+    for tag, kind, k, axis, self_join, count in _case_list(golden):
+        r = _side(g, tag, "r")
+        s = r if self_join else _side(g, tag, "s")
+        rep = pb.join(r, s, _collect(kind, k, axis))
+        assert rep.result_count == count, tag
+        assert np.array_equal(oracle.sorted_pairs(rep.pairs), g[f"{tag}_pairs"]), tag
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_reference_configs_bit_exact(golden, cfg):
+    g = golden["configs"]
+    r, s, k = make_config(cfg, float(g[f"cfg{cfg}_scale"]))
+    R = pb.RectBatch(*r)
+    S = R if s is r else pb.RectBatch(*s)
+    rep = pb.join(R, S, _collect("2d", k))
+    assert rep.result_count == int(g[f"cfg{cfg}_count"])
+    assert np.array_equal(oracle.sorted_pairs(rep.pairs), g[f"cfg{cfg}_pairs"])
+
+
+def test_count_only_matches_collect():
+    r, s, k = make_config(1)
+    R, S = pb.RectBatch(*r), pb.RectBatch(*s)
+    c = pb.join(R, S, pb.JoinConfig(pb.PartitionLayout("2d", k)))
+    assert c.pairs is None and c.result_count == 10_101
+
+
+def test_tile_counts_match_reference(golden):
+    g = golden["configs"]
+    r, s, k = make_config(1)
+    res = dev.run_join(dev.to_device(r), dev.to_device(s), k, k, collect=False,
+                       keep_counts=True)
+    cr, cs = (c.cpu().numpy() for c in res.tile_counts)
+    assert np.array_equal(cr, g["cfg1_counts_r"])
+    assert np.array_equal(cs, g["cfg1_counts_s"])
+    assert res.header["a_r"] == CONFIGS[1].a_r and res.header["a_s"] == CONFIGS[1].a_s
+
+
+def _dense_tile_instance(n_dense=900, n_other=700, seed=3):
+    """One tile holding > kLmax entries (large-tile path) next to normal tiles."""
+    rng = np.random.default_rng(seed)
+    k = 16
+    def side(n, base):
+        cx = 0.5 + rng.random(n) * (1 / k) * 0.9 + 1e-9  # inside tile (8, 8)
+        cy = 0.5 + rng.random(n) * (1 / k) * 0.9 + 1e-9
+        w = rng.random(n) * 0.01
+        h = rng.random(n) * 0.01
+        xl, yl = np.clip(cx - w, 0, 1), np.clip(cy - h, 0, 1)
+        xu, yu = np.clip(cx + w, 0, 1), np.clip(cy + h, 0, 1)
+        # plus a sprinkle of ordinary rectangles elsewhere
+        m = 200
+        ox, oy = rng.random(m), rng.random(m)
+        ow, oh = rng.random(m) * 0.05, rng.random(m) * 0.05
+        return (np.arange(base, base + n + m, dtype=np.int64),
+                np.concatenate([xl, ox]), np.concatenate([xu, np.minimum(ox + ow, 1)]),
+                np.concatenate([yl, oy]), np.concatenate([yu, np.minimum(oy + oh, 1)]))
+    return side(n_dense, 0), side(n_other, 10**6), k
+
+
+@pytest.mark.parametrize("sizes", [(900, 700), (3000, 20), (20, 3000), (600, 1)])
+def test_large_tile_path_bit_exact(sizes):
+    r, s, k = _dense_tile_instance(*sizes)
+    rep = pb.join(pb.RectBatch(*r), pb.RectBatch(*s), _collect("2d", k))
+    ref = oracle.join(r, s, "2d", k)
+    assert rep.result_count == ref["count"]
+    assert np.array_equal(oracle.sorted_pairs(rep.pairs), oracle.sorted_pairs(ref["pairs"]))
+
+
+def test_degenerate_identical_rectangles():
+    # every rectangle identical and on tile boundaries: one huge owner tile
+    n = 700
+    one = np.full(n, 0.25)
+    r = (np.arange(n, dtype=np.int64), one, one + 0.25, one, one + 0.25)
+    rep = pb.join(pb.RectBatch(*r), pb.RectBatch(*r), _collect("2d", 8))
+    assert rep.result_count == n * n
+    got = oracle.sorted_pairs(rep.pairs)
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    assert np.array_equal(got, np.stack([ii.ravel(), jj.ravel()], 1))
+
+
+def test_epsilon_join_matches_reference(golden):
+    g = golden["epsilon"]
+    for i in range(3):
+        x, y = g[f"e{i}_p"]
+        x2, y2 = g[f"e{i}_q"]
+        n = len(x)
+        P = pb.RectBatch(np.arange(n, dtype=np.int64), x, x, y, y)
+        Q = pb.RectBatch(np.arange(n, dtype=np.int64) + 5000, x2, x2, y2, y2)
+        rep = pb.epsilon_distance_join(P, Q, float(g[f"e{i}_eps"]), _collect("2d", int(g[f"e{i}_k"])))
+        assert np.array_equal(oracle.sorted_pairs(rep.pairs), g[f"e{i}_pairs"])
+
+
+def test_self_join_identity_pairs():
+    r, _, k = make_config(5, 0.01)
+    R = pb.RectBatch(*r)
+    rep = pb.join(R, R, _collect("2d", k))
+    ref = oracle.join(r, r, "2d", k)
+    assert rep.result_count == ref["count"]
+    got = oracle.sorted_pairs(rep.pairs)
+    assert np.array_equal(got, oracle.sorted_pairs(ref["pairs"]))
+    diag = got[got[:, 0] == got[:, 1]]
+    assert len(diag) == len(r[0])  # every rectangle intersects itself
+
+
+def test_repeat_runs_identical_sets():
+    r, s, k = make_config(4, 0.005)
+    R, S = pb.RectBatch(*r), pb.RectBatch(*s)
+    a = oracle.sorted_pairs(pb.join(R, S, _collect("2d", k)).pairs)
+    for _ in range(3):
+        assert np.array_equal(oracle.sorted_pairs(pb.join(R, S, _collect("2d", k)).pairs), a)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [2, 5])
+def test_full_size_bit_exact_vs_oracle(cfg):
+    spec = CONFIGS[cfg]
+    r, s, k = make_config(cfg)
+    rd = dev.to_device(r)
+    sd = rd if s is r else dev.to_device(s)
+    res = dev.run_join(rd, sd, k, k, collect=True)
+    assert res.count == spec.pairs
+    assert res.header["a_r"] == spec.a_r and res.header["a_s"] == spec.a_s
+    ref = oracle.join(r, s, "2d", k, threads=8)
+    assert ref["count"] == spec.pairs
+    got = oracle.sorted_pairs(res.pairs.cpu().numpy())
+    assert np.array_equal(got, oracle.sorted_pairs(ref["pairs"]))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_counts_and_properties(cfg):
+    """cfg3/cfg4 at full size: exact P, A_R, A_S (survey, measured with the
+    reference) and size-independent properties of the pair list."""
+    spec = CONFIGS[cfg]
+    r, s, k = make_config(cfg)
+    rd, sd = dev.to_device(r), dev.to_device(s)
+    res = dev.run_join(rd, sd, k, k, collect=True)
+    assert res.header["a_r"] == spec.a_r and res.header["a_s"] == spec.a_s
+    assert res.count == spec.pairs
+    p = res.pairs
+    # no duplicates: sort the packed (r, s) keys on the device
+    key = p[:, 0] * (len(s[0]) + 1) + p[:, 1]
+    ks = torch.sort(key).values
+    assert bool((ks[1:] != ks[:-1]).all())
+    # every emitted pair intersects (closed intervals)
+    rx = [torch.as_tensor(a, device=p.device) for a in r[1:]]
+    sx = [torch.as_tensor(a, device=p.device) for a in s[1:]]
+    i, j = p[:, 0], p[:, 1]
+    ok = ((rx[0][i] <= sx[1][j]) & (sx[0][j] <= rx[1][i]) &
+          (rx[2][i] <= sx[3][j]) & (sx[2][j] <= rx[3][i]))
+    assert bool(ok.all())
