@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 1
+#define PBSM_ABI_VERSION 2
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -58,33 +58,42 @@ extern "C" {
 #define PBSM_ERR_SCATTER_OVERFLOW  1u  /* a scatter cursor left its tile range       */
 #define PBSM_ERR_OFFSET_MISMATCH   2u  /* count and write passes disagree            */
 #define PBSM_ERR_TOTAL_RANGE       4u  /* A_R / A_S / W exceed 2^32-1                 */
-#define PBSM_ERR_PAIR_OVERFLOW     8u  /* emit past the pair capacity                 */
+#define PBSM_ERR_PAIR_OVERFLOW     8u  /* pair buffer too small: re-run with >= pairs   */
+#define PBSM_ERR_INVERTED         16u  /* R has xl > xu or yl > yu (or NaN); S: << 2    */
+#define PBSM_ERR_RANGE            32u  /* R has a coordinate outside [0, 1];  S: << 2   */
+#define PBSM_ERR_INTERNAL        256u  /* a work unit violated a plan invariant          */
 
-/* one tile-list entry: the rectangle's MBR.  The two top bits of `xl`
- * (always zero for a float64 in [0,1]) carry the class label of the entry in
- * its tile: bit 63 = x-out (starts left of the tile), bit 62 = y-out (starts
- * below the tile).  A = neither, B = y-out, C = x-out, D = both — the class
- * scheme of PAPER.md:651-733. */
+/* one tile-list entry: a 64-byte, 64-byte-aligned record, so the random
+ * scatter writes whole 32-byte sectors and a chunk of tiles is one contiguous
+ * range for the TMA bulk copy.  The two top bits of `xl` (always zero for a
+ * float64 in [0,1]) carry the class label of the entry in its tile: bit 63 =
+ * x-out (starts left of the tile), bit 62 = y-out (starts below the tile).
+ * A = neither, B = y-out, C = x-out, D = both — the class scheme of
+ * PAPER.md:651-733. */
 typedef struct pbsm_entry {
   uint64_t xl_key;
   double xu, yl, yu;
+  int64_t id;
+  uint64_t pad[3];
 } pbsm_entry;
 
 /* plan/result totals, device-resident at the start of the workspace */
 typedef struct pbsm_header {
   int64_t a_r;            /* Σ per-tile R counts = PartitionedDataset.total_assigned */
   int64_t a_s;            /* same for S                                             */
-  int64_t n_join;         /* tiles with both inputs non-empty, chunk path           */
+  int64_t list_r;         /* R entries written to tile lists (join tiles only)     */
+  int64_t list_s;         /* same for S                                             */
+  int64_t n_join;         /* join tiles (both inputs non-empty) on the chunk path  */
   int64_t w_join;         /* entries (R+S) in those tiles                           */
   int64_t n_chunks;       /* CTA work units of the chunk path                       */
   int64_t n_large;        /* join tiles too large for one CTA's shared memory       */
-  int64_t n_items;        /* work items of the large-tile path                      */
-  int64_t pairs;          /* result_count, valid after pbsm_join_count              */
+  int64_t n_items;        /* work units of the large-tile path                      */
+  int64_t pairs;          /* result_count, valid after pbsm_join_count/emit         */
+  int64_t pair_bound;     /* Σ |R_T|·|S_T| over join tiles (>= pairs)               */
   int64_t max_tile;       /* largest |R_T|+|S_T| over join tiles                   */
-  int64_t join_tiles_all; /* n_join + n_large                                       */
   uint32_t error;         /* PBSM_ERR_* bits                                        */
   uint32_t pad;
-  int64_t reserved[5];
+  int64_t reserved[3];
 } pbsm_header;
 
 /* Bytes of the grid workspace for a kx × (row_hi-row_lo) strip. */
@@ -112,36 +121,38 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
 int pbsm_read_header(void* ws, pbsm_header* out, void* stream);
 
 /* write_tiles (_kernels.pyx:61-98) for ALL n rectangles of one input:
- * scatter each rectangle into the list of every tile it overlaps, labelled
- * with its class there.  `out` / `out_ids` hold `capacity` entries
- * (= header.a_r or a_s). */
+ * scatter each rectangle into the list of every JOIN tile it overlaps (tiles
+ * where the other input is empty can produce no pair and get no list),
+ * labelled with its class there.  `out` holds `capacity` entries
+ * (= header.list_r or list_s). */
 int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu,
                  const double* yl, const double* yu, int64_t n, int32_t side,
                  void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-                 pbsm_entry* out, int64_t* out_ids, int64_t capacity,
-                 void* stream);
+                 pbsm_entry* out, int64_t capacity, void* stream);
 
-/* Scratch bytes for the join passes (per-unit pair counts + scan). */
+/* Scratch bytes for one join launch (work ticket + look-back words). */
 int64_t pbsm_join_scratch_bytes(int64_t n_chunks, int64_t n_items);
 
 /* sort_segment + sweep_count (_kernels.pyx:188-228, 231-315) for every join
- * tile: per-tile segmented sort by x-lower and forward-scan mini-joins over
- * the class combinations; writes per-unit counts, their exclusive scan and
- * header.pairs (= JoinReport.result_count). */
+ * tile: the write guard (partition.py:229-233), then per-tile segmented sort
+ * by x-lower and forward-scan mini-joins over the class combinations; the
+ * total lands in header.pairs (= JoinReport.result_count). */
 int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                     const pbsm_entry* r_list, const pbsm_entry* s_list,
                     int64_t n_chunks, int64_t n_items, void* scratch,
                     void* stream);
 
-/* sweep_collect (_kernels.pyx:318-341): re-runs the sort + sweep and writes
- * each pair (r_id, s_id) as two int64 at pairs[2*(base+i)] for
- * i < header.pairs, base = pair_base.  Requires pbsm_join_count's scratch. */
+/* sweep_collect (_kernels.pyx:318-341) + aggregation (engine.py:293-309):
+ * the same sort + sweep; each work unit counts its pairs, takes its output
+ * offset from a decoupled look-back over the preceding units, and writes
+ * (r_id, s_id) int64 pairs at pairs[2*i], i < header.pairs.  If header.pairs
+ * exceeds `capacity` nothing past it is written and PBSM_ERR_PAIR_OVERFLOW is
+ * set: re-run with capacity >= header.pairs (header.pair_bound always
+ * suffices). */
 int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-                   const pbsm_entry* r_list, const int64_t* r_ids,
-                   const pbsm_entry* s_list, const int64_t* s_ids,
-                   int64_t n_chunks, int64_t n_items, const void* scratch,
-                   int64_t* pairs, int64_t pair_base, int64_t capacity,
-                   void* stream);
+                   const pbsm_entry* r_list, const pbsm_entry* s_list,
+                   int64_t n_chunks, int64_t n_items, void* scratch,
+                   int64_t* pairs, int64_t capacity, void* stream);
 
 /* ε-distance refinement (engine.py:201-206, 298-300) of candidate pairs given
  * as ROW indices (cand[2i], cand[2i+1]) into the point arrays p / q: keeps the

@@ -364,12 +364,12 @@ typedef struct {
   pairbuf pairs;
 } worker_t;
 
+/* the reference's workers popleft() from a shared deque (engine.py:241-249,
+ * 261-265); here an atomic cursor hands out the task list in order */
 static i64 claim(eng_t* e, i64* cursor, i64 n) {
-  i64 v;
-  pthread_mutex_lock(&e->mu);
-  v = *cursor < n ? (*cursor)++ : -1;
-  pthread_mutex_unlock(&e->mu);
-  return v;
+  (void)e;
+  i64 v = __atomic_fetch_add(cursor, 1, __ATOMIC_RELAXED);
+  return v < n ? v : -1;
 }
 
 static void* sort_worker(void* p) {

@@ -13,13 +13,16 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
 ERR_OFFSET_MISMATCH = 2
 ERR_TOTAL_RANGE = 4
 ERR_PAIR_OVERFLOW = 8
+ERR_INVERTED = 16
+ERR_RANGE = 32
+ERR_INTERNAL = 256
 
 EXPORTED = (
     "pbsm_abi_version", "pbsm_build_info", "pbsm_workspace_bytes", "pbsm_init",
@@ -33,11 +36,11 @@ class Header(C.Structure):
     """Mirror of ``pbsm_header``."""
 
     _fields_ = [
-        ("a_r", C.c_int64), ("a_s", C.c_int64), ("n_join", C.c_int64),
-        ("w_join", C.c_int64), ("n_chunks", C.c_int64), ("n_large", C.c_int64),
-        ("n_items", C.c_int64), ("pairs", C.c_int64), ("max_tile", C.c_int64),
-        ("join_tiles_all", C.c_int64), ("error", C.c_uint32), ("pad", C.c_uint32),
-        ("reserved", C.c_int64 * 5),
+        ("a_r", C.c_int64), ("a_s", C.c_int64), ("list_r", C.c_int64), ("list_s", C.c_int64),
+        ("n_join", C.c_int64), ("w_join", C.c_int64), ("n_chunks", C.c_int64),
+        ("n_large", C.c_int64), ("n_items", C.c_int64), ("pairs", C.c_int64),
+        ("pair_bound", C.c_int64), ("max_tile", C.c_int64), ("error", C.c_uint32),
+        ("pad", C.c_uint32), ("reserved", C.c_int64 * 3),
     ]
 
     def as_dict(self) -> dict:
@@ -61,11 +64,11 @@ _SIGNATURES = {
     "pbsm_plan": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
     "pbsm_read_header": (C.c_int, [_P, C.POINTER(Header), _P]),
     "pbsm_scatter": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32,
-                               _P, _P, _I64, _P]),
+                               _P, _I64, _P]),
     "pbsm_join_scratch_bytes": (_I64, [_I64, _I64]),
     "pbsm_join_count": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I64, _I64, _P, _P]),
-    "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _I64, _I64, _P,
-                                 _P, _I64, _I64, _P]),
+    "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I64, _I64, _P, _P,
+                                 _I64, _P]),
     "pbsm_refine_scratch_bytes": (_I64, [_I64]),
     "pbsm_refine_result_offset": (_I64, [_I64]),
     "pbsm_refine": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),
@@ -111,4 +114,10 @@ def describe_error(bits: int) -> str:
         names.append("total exceeds 32-bit offsets")
     if bits & ERR_PAIR_OVERFLOW:
         names.append("pair buffer overflow")
+    if bits & (ERR_INVERTED | ERR_INVERTED << 2):
+        names.append("inverted rectangle")
+    if bits & (ERR_RANGE | ERR_RANGE << 2):
+        names.append("coordinates outside [0, 1]")
+    if bits & ERR_INTERNAL:
+        names.append("internal plan invariant violated")
     return ", ".join(names) or f"bits {bits:#x}"

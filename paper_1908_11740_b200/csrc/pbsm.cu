@@ -4,19 +4,23 @@
 // (/root/reference/pkg/src/sweepjoin/_kernels.pyx) for ALL tiles at once:
 //
 //  1. grid partitioning with class A/B/C/D labels
-//       k_count    ← count_tiles   (_kernels.pyx:34-58)
+//       k_count    ← count_tiles   (_kernels.pyx:34-58) + RectBatch.validate
+//                    (geometry.py:166-177) folded into the same pass
 //       k_plan_*   ← compute_segment_offsets (partition.py:151-164) and
 //                    build_task_queue (engine.py:84-100)
 //       k_scatter  ← write_tiles   (_kernels.pyx:61-98)
+//       k_guard    ← the write-overflow guard (partition.py:229-233)
 //  2. per-tile segmented sort by x-lower        ← sort_segment (_kernels.pyx:188-228)
 //  3. forward-scan mini-joins over the class combinations
 //                                               ← do_sweep (_kernels.pyx:231-293)
-//  4. two-pass count → emit pair writer         ← sweep_count / sweep_collect
+//  4. count → emit pair writer                  ← sweep_count / sweep_collect
 //                                                 (_kernels.pyx:304-341) and the
 //                                                 aggregation (engine.py:293-309)
-//  (2)-(4) are fused in k_join_chunk: a CTA stages a chunk of small tiles in
-//  shared memory, sorts every (tile, side) segment there and sweeps it.
-//  Tiles too large for one CTA's shared memory go to k_join_large.
+//  (2)-(4) are one kernel, k_join: a CTA stages a chunk of join tiles in shared
+//  memory with TMA bulk copies, sorts every (tile, side) segment there, counts
+//  its pairs, learns its output offset by a decoupled look-back over the
+//  preceding chunks, and emits.  Tiles too large for one CTA's shared memory
+//  are split into work items handled by the same kernel (nested loop).
 //
 // Duplicate avoidance.  The reference keeps a pair in tile T iff
 // max(r.xl,s.xl) >= T.xl and max(r.yl,s.yl) >= T.yl (Eq. 1,
@@ -31,7 +35,13 @@
 // All coordinate arithmetic is IEEE float64 with correctly rounded mul/div
 // (no fast-math; tile boundaries are the exact doubles i/k), so the result
 // set is bit-identical to the reference's.
+//
+// Memory layout in HBM: inputs are the reference's SoA
+// columns; a tile-list entry is one 64-byte record {xl|label, xu, yl, yu, id}
+// so the random scatter writes whole 32-byte sectors (no read-modify-write)
+// and a chunk's entries are one contiguous byte range for the TMA bulk copy.
 
+#include <cuda/atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -43,6 +53,7 @@
 typedef unsigned long long u64;
 typedef long long i64;
 typedef unsigned int u32;
+typedef unsigned short u16;
 
 namespace {
 
@@ -50,32 +61,51 @@ namespace {
 constexpr int kPlanThreads = 256;
 constexpr int kPlanPer = 16;                         // tiles per thread
 constexpr int kPlanTile = kPlanThreads * kPlanPer;   // 4096 tiles per CTA
-constexpr int kNV = 6;                               // plan scan lanes
+constexpr int kNV = 11;                              // plan scan lanes
 
 constexpr int kJoinThreads = 256;
-constexpr int kChunkB = 1024;       // chunk bucket width in entries
-constexpr int kLmax = 512;          // largest tile (|R_T|+|S_T|) on the chunk path
+constexpr int kChunkB = 640;        // chunk bucket width in entries
+constexpr int kLmax = 384;          // largest tile (|R_T|+|S_T|) on the chunk path
 constexpr int kCap = kChunkB + kLmax;   // max entries staged per chunk CTA
-constexpr int kEPT = kCap / kJoinThreads;  // entries per thread in the load
-constexpr int kMaxTilesPerChunk = kCap / 2 + 1;
-constexpr int kLargeLead = 256;     // lead-side entries per large-tile work item
-constexpr int kLargeStage = 1024;   // other-side entries staged per round
+constexpr int kMaxTiles = kCap / 2;     // a join tile holds >= 2 entries
+constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
 
 constexpr int kScanThreads = 256;
 constexpr int kScanPer = 16;
 constexpr int kScanTile = kScanThreads * kScanPer;
 
+constexpr int kRectsPerThread = 4;  // ILP in the count / scatter passes
+
 constexpr u64 kXOut = 1ull << 63;
 constexpr u64 kYOut = 1ull << 62;
 constexpr u64 kLabelMask = kXOut | kYOut;
 
-static_assert(kCap % kJoinThreads == 0, "kCap must be a multiple of the CTA size");
+constexpr u32 kSkip = 0x80000000u;  // cursor base of tiles whose list is not needed
+
+constexpr u64 kFlagAgg = 1ull << 62;   // look-back: aggregate published
+constexpr u64 kFlagPre = 2ull << 62;   // look-back: inclusive prefix published
+constexpr u64 kValMask = (1ull << 62) - 1;
+
 static_assert(kLmax <= kChunkB, "a small tile may cross at most one bucket boundary");
+
+// ---------------------------------------------------------------- records
+struct __align__(64) Rec {
+  u64 xl_key;   // xl bits | class label (bit 63 x-out, bit 62 y-out)
+  double xu, yl, yu;
+  i64 id;
+  u64 pad[3];
+};
+static_assert(sizeof(Rec) == 64, "record size");
+static_assert(sizeof(Rec) == sizeof(pbsm_entry), "entry layout");
+
+struct __align__(32) Half {  // the MBR half of a record: one sector
+  u64 xl_key;
+  double xu, yl, yu;
+};
 
 // ---------------------------------------------------------------- workspace
 struct WsLayout {
-  size_t hdr, bx, by, cnt_r, cnt_s, off_r, off_s, jlist, je, cstart, llist, lpre,
-      partials, total;
+  size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec, je, cstart, lrec, lpre, partials, total;
   u64 tiles;
   u64 nblocks;
 };
@@ -84,7 +114,7 @@ __host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a -
 
 inline WsLayout ws_layout(int kx, int ky, int row_lo, int row_hi) {
   WsLayout L;
-  u64 T = (u64)kx * (u64)(row_hi - row_lo);
+  const u64 T = (u64)kx * (u64)(row_hi - row_lo);
   L.tiles = T;
   L.nblocks = (T + kPlanTile - 1) / kPlanTile;
   size_t o = 0;
@@ -93,12 +123,12 @@ inline WsLayout ws_layout(int kx, int ky, int row_lo, int row_hi) {
   L.by = o; o = align_up(o + sizeof(double) * (ky + 1), 256);
   L.cnt_r = o; o = align_up(o + 4 * T, 256);
   L.cnt_s = o; o = align_up(o + 4 * T, 256);
-  L.off_r = o; o = align_up(o + 4 * T, 256);
-  L.off_s = o; o = align_up(o + 4 * T, 256);
-  L.jlist = o; o = align_up(o + 4 * T, 256);
+  L.cur_r = o; o = align_up(o + 4 * T, 256);
+  L.cur_s = o; o = align_up(o + 4 * T, 256);
+  L.jrec = o; o = align_up(o + 16 * T, 256);
   L.je = o; o = align_up(o + 4 * (T + 1), 256);
   L.cstart = o; o = align_up(o + 4 * (T + 2), 256);
-  L.llist = o; o = align_up(o + 4 * T, 256);
+  L.lrec = o; o = align_up(o + 16 * T, 256);
   L.lpre = o; o = align_up(o + 4 * (T + 1), 256);
   L.partials = o; o = align_up(o + sizeof(u64) * kNV * (L.nblocks + 1), 256);
   L.total = o;
@@ -109,7 +139,8 @@ struct Ws {
   pbsm_header* hdr;
   double* bx;
   double* by;
-  u32 *cnt_r, *cnt_s, *off_r, *off_s, *jlist, *je, *cstart, *llist, *lpre;
+  u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *je, *cstart, *lpre;
+  uint4 *jrec, *lrec;   // {r_start, s_start, nR, nS}
   u64* partials;
   u64 tiles, nblocks;
 };
@@ -122,28 +153,18 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
   w.by = (double*)(b + L.by);
   w.cnt_r = (u32*)(b + L.cnt_r);
   w.cnt_s = (u32*)(b + L.cnt_s);
-  w.off_r = (u32*)(b + L.off_r);
-  w.off_s = (u32*)(b + L.off_s);
-  w.jlist = (u32*)(b + L.jlist);
+  w.cur_r = (u32*)(b + L.cur_r);
+  w.cur_s = (u32*)(b + L.cur_s);
+  w.jrec = (uint4*)(b + L.jrec);
   w.je = (u32*)(b + L.je);
   w.cstart = (u32*)(b + L.cstart);
-  w.llist = (u32*)(b + L.llist);
+  w.lrec = (uint4*)(b + L.lrec);
   w.lpre = (u32*)(b + L.lpre);
   w.partials = (u64*)(b + L.partials);
   w.tiles = L.tiles;
   w.nblocks = L.nblocks;
   return w;
 }
-
-struct __align__(32) Entry {
-  u64 xl_key;
-  double xu, yl, yu;
-};
-static_assert(sizeof(Entry) == sizeof(pbsm_entry), "entry layout");
-
-struct __align__(32) Box {
-  double xl, xu, yl, yu;
-};
 
 // ---------------------------------------------------------------- helpers
 
@@ -152,8 +173,8 @@ struct __align__(32) Box {
 // boundaries b[i] = i/k so it agrees with boundary comparisons exactly.
 __device__ __forceinline__ int tile_of(double p, int k, const double* __restrict__ b) {
   long long i = (long long)__dmul_rn(p, (double)k);
-  if (i < 0) i = 0;
-  else if (i > k - 1) i = k - 1;
+  if (!(i >= 0)) i = 0;
+  if (i > k - 1) i = k - 1;
   while (i > 0 && p < __ldg(b + i)) --i;
   while (i < k - 1 && p >= __ldg(b + i + 1)) ++i;
   return (int)i;
@@ -201,13 +222,36 @@ __device__ __forceinline__ u64 block_excl_scan(u64 v, u64* total, u64* sh /* >= 
   return r;
 }
 
-__device__ __forceinline__ int upper_bound_u32(const u32* a, int n, u32 v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] <= v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
+// ---- TMA bulk copy (cp.async.bulk) + mbarrier, one elected thread issues
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
 }
 
 // ---------------------------------------------------------------- init
@@ -219,7 +263,10 @@ __global__ void k_bounds(double* bx, int kx, double* by, int ky) {
 }
 
 // ---------------------------------------------------------------- 1a count
-// count_tiles (_kernels.pyx:34-58), all rectangles, one thread per rectangle.
+// count_tiles (_kernels.pyx:34-58) for all rectangles; each thread keeps
+// kRectsPerThread rectangles in flight.  The same pass applies
+// RectBatch.validate (geometry.py:166-177): inverted or out-of-[0,1]
+// rectangles raise error bits the host turns into the reference's ValueError.
 __global__ void __launch_bounds__(256) k_count(const double* __restrict__ xl,
                                                const double* __restrict__ xu,
                                                const double* __restrict__ yl,
@@ -227,28 +274,48 @@ __global__ void __launch_bounds__(256) k_count(const double* __restrict__ xl,
                                                int kx, int ky, int row_lo, int row_hi,
                                                const double* __restrict__ bx,
                                                const double* __restrict__ by,
-                                               u32* __restrict__ cnt) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
-       i += (i64)gridDim.x * blockDim.x) {
-    const int c0 = tile_of(__ldg(xl + i), kx, bx);
-    const int c1 = tile_of(__ldg(xu + i), kx, bx);
-    int r0 = tile_of(__ldg(yl + i), ky, by);
-    int r1 = tile_of(__ldg(yu + i), ky, by);
-    r0 = max(r0, row_lo);
-    r1 = min(r1, row_hi - 1);
-    for (int row = r0; row <= r1; ++row) {
-      u32* base = cnt + (size_t)(row - row_lo) * kx;
-      for (int col = c0; col <= c1; ++col) atomicAdd(base + col, 1u);
+                                               u32* __restrict__ cnt, int side,
+                                               pbsm_header* hdr) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  u32 bad = 0;
+  for (i64 base = blockIdx.x * (i64)blockDim.x + threadIdx.x; base < n;
+       base += stride * kRectsPerThread) {
+    double a[kRectsPerThread], b[kRectsPerThread], c[kRectsPerThread], d[kRectsPerThread];
+#pragma unroll
+    for (int u = 0; u < kRectsPerThread; ++u) {
+      const i64 i = base + u * stride;
+      if (i < n) {
+        a[u] = __ldg(xl + i);
+        b[u] = __ldg(xu + i);
+        c[u] = __ldg(yl + i);
+        d[u] = __ldg(yu + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRectsPerThread; ++u) {
+      const i64 i = base + u * stride;
+      if (i >= n) continue;
+      if (!(a[u] <= b[u]) || !(c[u] <= d[u])) bad |= PBSM_ERR_INVERTED;
+      if (a[u] < 0.0 || c[u] < 0.0 || b[u] > 1.0 || d[u] > 1.0) bad |= PBSM_ERR_RANGE;
+      const int c0 = tile_of(a[u], kx, bx);
+      const int c1 = tile_of(b[u], kx, bx);
+      const int r0 = max(tile_of(c[u], ky, by), row_lo);
+      const int r1 = min(tile_of(d[u], ky, by), row_hi - 1);
+      for (int row = r0; row <= r1; ++row) {
+        u32* rowp = cnt + (size_t)(row - row_lo) * kx;
+        for (int col = c0; col <= c1; ++col) atomicAdd(rowp + col, 1u);
+      }
     }
   }
+  if (bad) atomicOr(&hdr->error, bad << (2 * side));
 }
 
 // ---------------------------------------------------------------- 1c scatter
 // write_tiles (_kernels.pyx:61-98): copy each rectangle into every tile it
-// overlaps, at a cursor that starts at the tile's exclusive offset.  After the
-// pass off[t] is the END of tile t; the join kernels check
-// end[t] - cnt[t] == end[t-1], the device form of the write guard
-// (partition.py:229-233).
+// overlaps, labelled with its class there.  Only tiles where both inputs are
+// non-empty get a list (the others cannot produce a pair: build_task_queue
+// joins only those, engine.py:97); their cursors start at kSkip and the write
+// is skipped, but the cursor still advances so k_guard can check every tile.
 __global__ void __launch_bounds__(256) k_scatter(const i64* __restrict__ ids,
                                                  const double* __restrict__ xl,
                                                  const double* __restrict__ xu,
@@ -257,47 +324,89 @@ __global__ void __launch_bounds__(256) k_scatter(const i64* __restrict__ ids,
                                                  int kx, int ky, int row_lo, int row_hi,
                                                  const double* __restrict__ bx,
                                                  const double* __restrict__ by,
-                                                 u32* __restrict__ cursor,
-                                                 Entry* __restrict__ out,
-                                                 i64* __restrict__ out_ids, i64 capacity,
-                                                 pbsm_header* hdr) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
-       i += (i64)gridDim.x * blockDim.x) {
-    const double a = __ldg(xl + i), b = __ldg(xu + i), c = __ldg(yl + i), d = __ldg(yu + i);
-    const i64 id = __ldg(ids + i);
-    const int c0 = tile_of(a, kx, bx);
-    const int c1 = tile_of(b, kx, bx);
-    const int rr0 = tile_of(c, ky, by);
-    const int r1 = min(tile_of(d, ky, by), row_hi - 1);
-    const int r0 = max(rr0, row_lo);
-    const u64 xk = xl_bits(a);
-    for (int row = r0; row <= r1; ++row) {
-      u32* base = cursor + (size_t)(row - row_lo) * kx;
-      const u64 ylab = (row != rr0) ? kYOut : 0ull;
-      for (int col = c0; col <= c1; ++col) {
-        const u32 pos = atomicAdd(base + col, 1u);
-        if ((i64)pos >= capacity) {
-          atomicOr(&hdr->error, PBSM_ERR_SCATTER_OVERFLOW);
-          continue;
+                                                 u32* __restrict__ cursor, Rec* __restrict__ out,
+                                                 i64 capacity, pbsm_header* hdr) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  u32 bad = 0;
+  for (i64 base = blockIdx.x * (i64)blockDim.x + threadIdx.x; base < n;
+       base += stride * kRectsPerThread) {
+    double a[kRectsPerThread], b[kRectsPerThread], c[kRectsPerThread], d[kRectsPerThread];
+    i64 id[kRectsPerThread];
+#pragma unroll
+    for (int u = 0; u < kRectsPerThread; ++u) {
+      const i64 i = base + u * stride;
+      if (i < n) {
+        a[u] = __ldg(xl + i);
+        b[u] = __ldg(xu + i);
+        c[u] = __ldg(yl + i);
+        d[u] = __ldg(yu + i);
+        id[u] = __ldg(ids + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRectsPerThread; ++u) {
+      const i64 i = base + u * stride;
+      if (i >= n) continue;
+      const int c0 = tile_of(a[u], kx, bx);
+      const int c1 = tile_of(b[u], kx, bx);
+      const int rr0 = tile_of(c[u], ky, by);
+      const int r0 = max(rr0, row_lo);
+      const int r1 = min(tile_of(d[u], ky, by), row_hi - 1);
+      const u64 xk = xl_bits(a[u]);
+      for (int row = r0; row <= r1; ++row) {
+        u32* rowp = cursor + (size_t)(row - row_lo) * kx;
+        const u64 ylab = (row != rr0) ? kYOut : 0ull;
+        for (int col = c0; col <= c1; ++col) {
+          const u32 pos = atomicAdd(rowp + col, 1u);
+          if (pos >= kSkip) continue;  // not a join tile
+          if ((i64)pos >= capacity) {
+            bad |= PBSM_ERR_SCATTER_OVERFLOW;
+            continue;
+          }
+          Half h;
+          h.xl_key = xk | ylab | ((col != c0) ? kXOut : 0ull);
+          h.xu = b[u];
+          h.yl = c[u];
+          h.yu = d[u];
+          Rec* r = out + pos;
+          *reinterpret_cast<Half*>(r) = h;
+          Half t;
+          t.xl_key = (u64)id[u];
+          t.xu = 0.0;
+          t.yl = 0.0;
+          t.yu = 0.0;
+          *reinterpret_cast<Half*>(&r->id) = t;
         }
-        Entry e;
-        e.xl_key = xk | ylab | ((col != c0) ? kXOut : 0ull);
-        e.xu = b;
-        e.yl = c;
-        e.yu = d;
-        out[pos] = e;
-        out_ids[pos] = id;
       }
     }
   }
+  if (bad) atomicOr(&hdr->error, bad);
+}
+
+// write guard (partition.py:229-233): every cursor must end exactly where the
+// count pass said (the plan stored the expected end in cnt[]).
+__global__ void k_guard(const u32* __restrict__ cur_r, const u32* __restrict__ end_r,
+                        const u32* __restrict__ cur_s, const u32* __restrict__ end_s, u64 T,
+                        pbsm_header* hdr) {
+  bool bad = false;
+  for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < T;
+       t += (u64)gridDim.x * blockDim.x)
+    bad |= (cur_r[t] != end_r[t]) || (cur_s[t] != end_s[t]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&hdr->error, PBSM_ERR_OFFSET_MISMATCH);
 }
 
 // ---------------------------------------------------------------- 1b plan
-// Per tile t the plan scans six lanes at once:
-//   0 |R_T|  1 |S_T|  (→ CSR offsets, compute_segment_offsets partition.py:151-164)
-//   2 small-join flag  3 small-join entries   (→ join tile list + chunk buckets)
-//   4 large-join flag  5 large-join work items (→ large tile list)
+// Per tile t the plan scans nine lanes at once:
+//   0 |R_T|  1 |S_T|                         (A_R, A_S: PartitionedDataset totals)
+//   2 small-join flag  3 small-join entries  (→ join tile list + CTA chunks)
+//   4 large-join flag  5 large-join items    (→ large tile list)
+//   6 |R_T| 7 |S_T| of small join tiles   ┐ tile-list offsets (compute_segment_
+//   9 |R_T| 10 |S_T| of large join tiles  ┘ offsets, partition.py:151-164)
+//   8 |R_T|·|S_T| of join tiles              (upper bound on the pair count)
 // A join tile has both inputs non-empty (build_task_queue, engine.py:97).
+// Small join tiles take the front of each tile list in tile order, so a
+// chunk of consecutive small tiles is one contiguous range per input; large
+// tiles follow in a second region.
 __device__ __forceinline__ void tile_vals(u32 a, u32 b, u64 v[kNV]) {
   const bool join = a != 0u && b != 0u;
   const u32 w = a + b;
@@ -310,6 +419,11 @@ __device__ __forceinline__ void tile_vals(u32 a, u32 b, u64 v[kNV]) {
   v[3] = small ? w : 0u;
   v[4] = large;
   v[5] = large ? (lead + kLargeLead - 1) / kLargeLead : 0u;
+  v[6] = small ? a : 0u;
+  v[7] = small ? b : 0u;
+  v[8] = join ? (u64)a * (u64)b : 0ull;
+  v[9] = large ? a : 0u;
+  v[10] = large ? b : 0u;
 }
 
 __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restrict__ cr,
@@ -318,7 +432,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
                                                               pbsm_header* hdr) {
   __shared__ u64 sh[kPlanThreads / 32][kNV];
   __shared__ u32 shmax[kPlanThreads / 32];
-  u64 acc[kNV] = {0, 0, 0, 0, 0, 0};
+  u64 acc[kNV];
+#pragma unroll
+  for (int q = 0; q < kNV; ++q) acc[q] = 0;
   u32 mx = 0;
   const u64 base = (u64)blockIdx.x * kPlanTile;
   for (int i = 0; i < kPlanPer; ++i) {
@@ -361,7 +477,9 @@ __global__ void __launch_bounds__(1024) k_plan_partials(u64* __restrict__ partia
                                                         pbsm_header* hdr, u32* je, u32* lpre,
                                                         u32* cstart) {
   __shared__ u64 sh[33];
-  u64 carry[kNV] = {0, 0, 0, 0, 0, 0};
+  u64 carry[kNV];
+#pragma unroll
+  for (int q = 0; q < kNV; ++q) carry[q] = 0;
   for (u64 base = 0; base < nb; base += 1024) {
     const u64 i = base + threadIdx.x;
 #pragma unroll
@@ -380,10 +498,15 @@ __global__ void __launch_bounds__(1024) k_plan_partials(u64* __restrict__ partia
     hdr->w_join = (i64)carry[3];
     hdr->n_large = (i64)carry[4];
     hdr->n_items = (i64)carry[5];
-    hdr->join_tiles_all = (i64)(carry[2] + carry[4]);
+    hdr->list_r = (i64)(carry[6] + carry[9]);
+    hdr->list_s = (i64)(carry[7] + carry[10]);
+    partials[nb * kNV + 0] = carry[6];   // small-region sizes, read by k_plan_apply
+    partials[nb * kNV + 1] = carry[7];
+    hdr->pair_bound = (i64)carry[8];
     hdr->n_chunks = 0;
-    if (carry[0] > 0xffffffffull || carry[1] > 0xffffffffull || carry[3] > 0xffffffffull ||
-        carry[5] > 0xffffffffull)
+    hdr->pairs = 0;
+    if (carry[0] >= kSkip || carry[1] >= kSkip || carry[3] >= kSkip || carry[5] >= kSkip ||
+        carry[6] + carry[9] >= kSkip || carry[7] + carry[10] >= kSkip)
       hdr->error |= PBSM_ERR_TOTAL_RANGE;
     je[carry[2]] = (u32)carry[3];      // sentinel: end of the last join tile
     lpre[carry[4]] = (u32)carry[5];    // sentinel: total large work items
@@ -392,10 +515,9 @@ __global__ void __launch_bounds__(1024) k_plan_partials(u64* __restrict__ partia
 }
 
 __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(
-    const u32* __restrict__ cr, const u32* __restrict__ cs, u64 T,
-    const u64* __restrict__ partials, u32* __restrict__ off_r, u32* __restrict__ off_s,
-    u32* __restrict__ jlist, u32* __restrict__ je, u32* __restrict__ llist,
-    u32* __restrict__ lpre) {
+    u32* __restrict__ cr, u32* __restrict__ cs, u64 T, u64 nb, const u64* __restrict__ partials,
+    u32* __restrict__ cur_r, u32* __restrict__ cur_s, uint4* __restrict__ jrec,
+    u32* __restrict__ je, uint4* __restrict__ lrec, u32* __restrict__ lpre) {
   __shared__ u32 sa[kPlanTile];
   __shared__ u32 sb[kPlanTile];
   __shared__ u64 shs[33];
@@ -407,7 +529,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(
   }
   __syncthreads();
   u32 a[kPlanPer], b[kPlanPer];
-  u64 acc[kNV] = {0, 0, 0, 0, 0, 0};
+  u64 acc[kNV];
+#pragma unroll
+  for (int q = 0; q < kNV; ++q) acc[q] = 0;
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     a[i] = sa[threadIdx.x * kPlanPer + i];
@@ -424,21 +548,26 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(
     pre[q] = block_excl_scan<kPlanThreads>(acc[q], &tot, shs) +
              partials[(u64)blockIdx.x * kNV + q];
   }
-  // (block_excl_scan ends with a barrier, so sa/sb may be overwritten now)
+  const u64 small_r = partials[nb * kNV + 0], small_s = partials[nb * kNV + 1];
+  // (block_excl_scan ends with a barrier, so sa/sb may be overwritten now:
+  // they receive the cursor starts; the expected cursor ends go back into
+  // cnt[] for k_guard.)
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     const u64 t = base + (u64)threadIdx.x * kPlanPer + i;
     u64 v[kNV];
     tile_vals(a[i], b[i], v);
-    sa[threadIdx.x * kPlanPer + i] = (u32)pre[0];
-    sb[threadIdx.x * kPlanPer + i] = (u32)pre[1];
+    const u32 r0 = v[2] ? (u32)pre[6] : v[4] ? (u32)(small_r + pre[9]) : kSkip;
+    const u32 s0 = v[2] ? (u32)pre[7] : v[4] ? (u32)(small_s + pre[10]) : kSkip;
+    sa[threadIdx.x * kPlanPer + i] = r0;
+    sb[threadIdx.x * kPlanPer + i] = s0;
     if (t < T) {
       if (v[2]) {
-        jlist[pre[2]] = (u32)t;
+        jrec[pre[2]] = make_uint4(r0, s0, a[i], b[i]);
         je[pre[2]] = (u32)pre[3];
       }
       if (v[4]) {
-        llist[pre[4]] = (u32)t;
+        lrec[pre[4]] = make_uint4(r0, s0, a[i], b[i]);
         lpre[pre[4]] = (u32)pre[5];
       }
     }
@@ -449,8 +578,11 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(
   for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
     const u64 t = base + i;
     if (t < T) {
-      off_r[t] = sa[i];
-      off_s[t] = sb[i];
+      const u32 r0 = sa[i], s0 = sb[i];
+      cr[t] = r0 + cr[t];   // expected end of tile t's R cursor
+      cs[t] = s0 + cs[t];
+      cur_r[t] = r0;
+      cur_s[t] = s0;
     }
   }
 }
@@ -472,7 +604,7 @@ __global__ void k_chunks(const u32* __restrict__ je, u32* __restrict__ cstart, p
 }
 
 // ---------------------------------------------------------------- generic scan
-// exclusive scan of u32 counts into u64 bases; base[n] = total → hdr->pairs
+// exclusive scan of u32 counts into u64 bases; base[n] = total (ε refinement)
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const u32* __restrict__ in, u64 n,
                                                               u64* __restrict__ partials) {
   __shared__ u64 sh[kScanThreads / 32];
@@ -494,8 +626,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const u32* __restr
 }
 
 __global__ void __launch_bounds__(1024) k_scan_partials(u64* __restrict__ partials, u64 nb,
-                                                        u64* __restrict__ out, u64 n,
-                                                        pbsm_header* hdr) {
+                                                        u64* __restrict__ out, u64 n) {
   __shared__ u64 sh[33];
   u64 carry = 0;
   for (u64 base = 0; base < nb; base += 1024) {
@@ -506,10 +637,7 @@ __global__ void __launch_bounds__(1024) k_scan_partials(u64* __restrict__ partia
     if (i < nb) partials[i] = carry + ex;
     carry += tot;
   }
-  if (threadIdx.x == 0) {
-    out[n] = carry;
-    if (hdr) hdr->pairs = (i64)carry;
-  }
+  if (threadIdx.x == 0) out[n] = carry;
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const u32* __restrict__ in, u64 n,
@@ -539,44 +667,85 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const u32* __restri
 
 // ---------------------------------------------------------------- 2-4 join
 struct JoinArgs {
-  const u32* jlist;
-  const u32* je;
+  const uint4* jrec;
   const u32* cstart;
-  const u32* llist;
+  const uint4* lrec;
   const u32* lpre;
-  const u32* cnt_r;
-  const u32* cnt_s;
-  const u32* off_r;   // tile END after the scatter
-  const u32* off_s;
-  const Entry* rl;
-  const Entry* sl;
-  const i64* rid;
-  const i64* sid;
-  u32* unit_cnt;       // [n_chunks + n_items]
-  const u64* unit_base;
-  i64* pairs;
-  i64 pair_base;
-  i64 capacity;
+  const Rec* rl;
+  const Rec* sl;
+  u32* ticket;
+  u64* status;     // [n_units] decoupled look-back words (emit mode)
+  i64* pairs;      // (r_id, s_id) int64 pairs
+  i64 capacity;    // pairs the buffer holds
   i64 n_chunks;
+  i64 n_units;
   pbsm_header* hdr;
 };
 
 struct ChunkSmem {
-  Box sorted[kCap];            // per tile: [R x-in sorted by xl | R x-out | S x-in sorted | S x-out]
-  u64 key[kCap];               // label|xl bits as loaded
-  i64 ids[kCap];               // ids in sorted order (emit only)
-  unsigned short seg[kCap];    // chunk-local tile of each loaded entry
-  unsigned char yin[kCap];     // y-in flag in sorted order
-  u32 tE[kMaxTilesPerChunk + 1];
-  u32 tR[kMaxTilesPerChunk];
-  u32 tS[kMaxTilesPerChunk];
-  u32 tRs[kMaxTilesPerChunk];
-  u32 tSs[kMaxTilesPerChunk];
-  unsigned short tNinR[kMaxTilesPerChunk];
-  unsigned short tNinS[kMaxTilesPerChunk];
-  u64 scan[33];
-  int nt, N;
+  Rec recs[kCap];      // TMA landing zone: the chunk's R range then its S range
+  u64 key[kCap];       // label|xl bits per loaded entry
+  double sxl[kCap];    // per segment: [x-in sorted by xl | x-out]
+  double syl[kCap];
+  double syu[kCap];
+  u16 sidx[kCap];      // sorted position → loaded entry
+  u16 seg[kCap];       // position → chunk-local tile
+  unsigned char syin[kCap];
+  u16 tR0[kMaxTiles], tS0[kMaxTiles], tNR[kMaxTiles], tNS[kMaxTiles];
+  u16 tNinR[kMaxTiles], tNinS[kMaxTiles];
+  u64 bar;
+  u64 scan[kJoinThreads / 32 + 1];
+  u64 base;
+  int unit, nt, NR, NS;
 };
+
+struct LargeSmem {
+  Rec other[kCap];
+  u64 bar;
+  u64 scan[kJoinThreads / 32 + 1];
+  u64 base;
+  int unit;
+};
+
+union JoinSmem {
+  ChunkSmem c;
+  LargeSmem l;
+};
+
+// Decoupled look-back (one thread): publish this unit's count, accumulate the
+// predecessors' published values until an inclusive prefix is found, publish
+// ours.  Units are handed out by an atomic ticket in launch order, so every
+// predecessor is resident or finished — the spin cannot deadlock.
+__device__ u64 lookback(u64* status, i64 unit, u64 count, pbsm_header* hdr) {
+  cuda::atomic_ref<u64, cuda::thread_scope_device> me(status[unit]);
+  if (unit == 0) {
+    me.store(kFlagPre | count, cuda::memory_order_release);
+    return 0;
+  }
+  me.store(kFlagAgg | count, cuda::memory_order_release);
+  u64 excl = 0;
+  i64 j = unit - 1;
+  u64 spins = 0;
+  while (true) {
+    cuda::atomic_ref<u64, cuda::thread_scope_device> st(status[j]);
+    const u64 v = st.load(cuda::memory_order_acquire);
+    const u64 flag = v & ~kValMask;
+    if (flag == 0) {
+      // a predecessor that never publishes is a bug; never hang the GPU on it
+      if (++spins > (1ull << 24)) {
+        atomicOr(&hdr->error, PBSM_ERR_INTERNAL);
+        break;
+      }
+      __nanosleep(64);
+      continue;
+    }
+    excl += v & kValMask;
+    if (flag == kFlagPre) break;
+    --j;
+  }
+  me.store(kFlagPre | (excl + count), cuda::memory_order_release);
+  return excl;
+}
 
 // One leader element of the forward scan (Alg. 1, _kernels.pyx:231-293,
 // reformulated per element).  In the reference, when r.xl < s.xl the R
@@ -590,50 +759,47 @@ struct ChunkSmem {
 // x rule above leaves exactly the nine class combinations AA AB AC AD BA BC CA
 // CB DA.
 template <bool EMIT>
-__device__ __forceinline__ u32 sweep_one(const ChunkSmem& S, int p, int lt, i64* out) {
-  const int base = (int)S.tE[lt];
-  const int nR = (int)S.tR[lt];
-  const int ninR = S.tNinR[lt], ninS = S.tNinS[lt];
-  const int q = p - base;
-  const Box me = S.sorted[p];
-  const bool yme = S.yin[p];
+__device__ __forceinline__ u32 sweep_one(const ChunkSmem& S, int p, i64* out) {
+  const int lt = S.seg[p];
+  const int rb = S.tR0[lt], sb = S.tS0[lt];
+  const bool lead_r = p < sb;
+  const double mxl = S.sxl[p], myl = S.syl[p], myu = S.syu[p];
+  const bool yme = S.syin[p];
+  const double mxu = S.recs[S.sidx[p]].xu;
   int k, hi;
-  bool lead_r;
-  if (q < nR) {
-    lead_r = true;
-    const int lo = base + nR;
-    hi = lo + ninS;
-    k = lo;
-    if (q < ninR) {
+  if (lead_r) {
+    k = sb;
+    hi = sb + S.tNinS[lt];
+    if (p - rb < S.tNinR[lt]) {
       // upper_bound(S x-in run, r.xl): first s with s.xl > r.xl
       int b = hi;
       while (k < b) {
         const int m = (k + b) >> 1;
-        if (S.sorted[m].xl <= me.xl) k = m + 1; else b = m;
+        if (S.sxl[m] <= mxl) k = m + 1; else b = m;
       }
     }
   } else {
-    lead_r = false;
-    const int lo = base;
-    hi = lo + ninR;
-    k = lo;
-    if (q - nR < ninS) {
+    k = rb;
+    hi = rb + S.tNinR[lt];
+    if (p - sb < S.tNinS[lt]) {
       // lower_bound(R x-in run, s.xl): first r with r.xl >= s.xl
       int b = hi;
       while (k < b) {
         const int m = (k + b) >> 1;
-        if (S.sorted[m].xl < me.xl) k = m + 1; else b = m;
+        if (S.sxl[m] < mxl) k = m + 1; else b = m;
       }
     }
   }
   u32 c = 0;
+  i64 my_id = 0;
+  if (EMIT) my_id = S.recs[S.sidx[p]].id;
   for (; k < hi; ++k) {
-    const Box o = S.sorted[k];
-    if (o.xl > me.xu) break;
-    if (me.yl <= o.yu && o.yl <= me.yu && (yme || S.yin[k])) {
+    if (S.sxl[k] > mxu) break;
+    if (myl <= S.syu[k] && S.syl[k] <= myu && (yme || S.syin[k])) {
       if (EMIT) {
-        out[2 * (i64)c] = lead_r ? S.ids[p] : S.ids[k];
-        out[2 * (i64)c + 1] = lead_r ? S.ids[k] : S.ids[p];
+        const i64 oid = S.recs[S.sidx[k]].id;
+        *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
+            lead_r ? make_longlong2(my_id, oid) : make_longlong2(oid, my_id);
       }
       ++c;
     }
@@ -642,167 +808,130 @@ __device__ __forceinline__ u32 sweep_one(const ChunkSmem& S, int p, int lt, i64*
 }
 
 template <bool EMIT>
-__global__ void __launch_bounds__(kJoinThreads, 2) k_join_chunk(JoinArgs A) {
-  extern __shared__ __align__(32) unsigned char smem_raw[];
-  ChunkSmem& S = *reinterpret_cast<ChunkSmem*>(smem_raw);
-  const int c = blockIdx.x;
+__device__ void join_chunk(ChunkSmem& S, const JoinArgs& A, int c) {
   const int tid = threadIdx.x;
   const u32 j0 = A.cstart[c], j1 = A.cstart[c + 1];
   const int nt = (int)(j1 - j0);
-  const u32 e0 = A.je[j0];
-
-  // ---- tile table of the chunk (task list: build_task_queue engine.py:84-100)
-  for (int lt = tid; lt < nt; lt += kJoinThreads) {
-    const u32 t = A.jlist[j0 + lt];
-    const u32 nR = A.cnt_r[t], nS = A.cnt_s[t];
-    const u32 endR = A.off_r[t], endS = A.off_s[t];
-    const u32 rs = endR - nR, ss = endS - nS;
-    const u32 prevR = t == 0 ? 0u : A.off_r[t - 1];
-    const u32 prevS = t == 0 ? 0u : A.off_s[t - 1];
-    if (rs != prevR || ss != prevS) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
-    S.tE[lt] = A.je[j0 + lt] - e0;
-    S.tR[lt] = nR;
-    S.tS[lt] = nS;
-    S.tRs[lt] = rs;
-    S.tSs[lt] = ss;
-    if (lt == nt - 1) {
-      S.tE[nt] = A.je[j0 + lt] - e0 + nR + nS;
-      S.N = (int)(A.je[j0 + lt] - e0 + nR + nS);
+  if (tid == 0) {
+    const uint4 first = A.jrec[j0], last = A.jrec[j1 - 1];
+    const int NR = (int)(last.x + last.z - first.x);
+    const int NS = (int)(last.y + last.w - first.y);
+    // a chunk never exceeds the staging buffer by construction (k_chunks);
+    // if it somehow did, flag it and contribute 0 pairs (the look-back chain
+    // must still be fed, so no early return)
+    const bool fits = NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles;
+    if (!fits) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
+    S.nt = fits ? nt : 0;
+    S.NR = fits ? NR : 0;
+    S.NS = fits ? NS : 0;
+    if (fits) {
+      // TMA: two bulk copies (the chunk's R and S ranges are contiguous
+      // because small join tiles get consecutive list offsets in tile order)
+      mbar_init(&S.bar, 1);
+      mbar_expect_tx(&S.bar, (u32)(NR + NS) * (u32)sizeof(Rec));
+      bulk_g2s(&S.recs[0], A.rl + first.x, (u32)NR * (u32)sizeof(Rec), &S.bar);
+      bulk_g2s(&S.recs[NR], A.sl + first.y, (u32)NS * (u32)sizeof(Rec), &S.bar);
     }
   }
   __syncthreads();
-  const int N = S.N;
-
-  // ---- stage the chunk: one 256-bit load per entry, kept in registers
-  Entry ent[kEPT];
-  i64 eid[kEPT];
-#pragma unroll
-  for (int i = 0; i < kEPT; ++i) {
-    const int e = tid + i * kJoinThreads;
-    if (e < N) {
-      const int lt = upper_bound_u32(S.tE, nt, (u32)e) - 1;
-      const int q = e - (int)S.tE[lt];
-      const int nR = (int)S.tR[lt];
-      if (q < nR) {
-        const u32 g = S.tRs[lt] + q;
-        ent[i] = A.rl[g];
-        if (EMIT) eid[i] = A.rid[g];
-      } else {
-        const u32 g = S.tSs[lt] + (q - nR);
-        ent[i] = A.sl[g];
-        if (EMIT) eid[i] = A.sid[g];
-      }
-      S.key[e] = ent[i].xl_key;
-      S.seg[e] = (unsigned short)lt;
+  const int NR = S.NR, N = S.NR + S.NS;
+  // tile table + position → tile map, while the copies are in flight
+  {
+    const uint4 first = A.jrec[j0];
+    for (int lt = tid; lt < S.nt; lt += kJoinThreads) {
+      const uint4 r = A.jrec[j0 + lt];
+      const int r0 = (int)(r.x - first.x), s0 = NR + (int)(r.y - first.y);
+      S.tR0[lt] = (u16)r0;
+      S.tS0[lt] = (u16)s0;
+      S.tNR[lt] = (u16)r.z;
+      S.tNS[lt] = (u16)r.w;
+      for (int e = 0; e < (int)r.z; ++e) S.seg[r0 + e] = (u16)lt;
+      for (int e = 0; e < (int)r.w; ++e) S.seg[s0 + e] = (u16)lt;
     }
   }
+  if (N > 0) mbar_wait(&S.bar, 0);
+  for (int e = tid; e < N; e += kJoinThreads) S.key[e] = S.recs[e].xl_key;
   __syncthreads();
 
   // ---- 2: segmented sort (sort_segment, _kernels.pyx:188-228) by rank
   // counting inside each (tile, side) segment.  x-in entries are ordered by
   // (xl, load position) — a strict total order, so ranks are a permutation;
   // x-out entries keep load order after the x-in run.
-#pragma unroll
-  for (int i = 0; i < kEPT; ++i) {
-    const int e = tid + i * kJoinThreads;
-    if (e < N) {
-      const int lt = S.seg[e];
-      const int base = (int)S.tE[lt];
-      const int nR = (int)S.tR[lt];
-      int a, b;
-      if (e < base + nR) { a = base; b = base + nR; }
-      else { a = base + nR; b = a + (int)S.tS[lt]; }
-      const u64 ke = S.key[e];
-      const bool in_e = !(ke & kXOut);
-      const u64 xe = ke & ~kLabelMask;
-      int n_in = 0, less = 0, out_before = 0;
-      for (int j = a; j < b; ++j) {
-        const u64 kj = S.key[j];
-        if (!(kj & kXOut)) {
-          ++n_in;
-          const u64 xj = kj & ~kLabelMask;
-          less += (xj < xe) || (xj == xe && j < e);
-        } else {
-          out_before += (j < e);
-        }
-      }
-      const int rank = in_e ? less : n_in + out_before;
-      const int p = a + rank;
-      Box bx;
-      bx.xl = __longlong_as_double((long long)xe);
-      bx.xu = ent[i].xu;
-      bx.yl = ent[i].yl;
-      bx.yu = ent[i].yu;
-      S.sorted[p] = bx;
-      S.yin[p] = (ke & kYOut) ? 0 : 1;
-      if (EMIT) S.ids[p] = eid[i];
-      if (e == a) {
-        if (a == base) S.tNinR[lt] = (unsigned short)n_in;
-        else S.tNinS[lt] = (unsigned short)n_in;
-      }
+  for (int e = tid; e < N; e += kJoinThreads) {
+    const int lt = S.seg[e];
+    const bool is_r = e < NR;
+    const int a = is_r ? S.tR0[lt] : S.tS0[lt];
+    const int b = a + (is_r ? S.tNR[lt] : S.tNS[lt]);
+    const u64 ke = S.key[e];
+    const bool in_e = !(ke & kXOut);
+    const u64 xe = ke & ~kLabelMask;
+    int n_in = 0, less = 0, out_before = 0;
+    for (int j = a; j < b; ++j) {
+      const u64 kj = S.key[j];
+      const bool in_j = !(kj & kXOut);
+      const u64 xj = kj & ~kLabelMask;
+      n_in += in_j;
+      less += in_j & ((xj < xe) | ((xj == xe) & (j < e)));
+      out_before += (!in_j) & (j < e);
+    }
+    const int p = a + (in_e ? less : n_in + out_before);
+    S.sxl[p] = __longlong_as_double((long long)xe);
+    S.syl[p] = S.recs[e].yl;
+    S.syu[p] = S.recs[e].yu;
+    S.syin[p] = (ke & kYOut) ? 0 : 1;
+    S.sidx[p] = (u16)e;
+    if (e == a) {
+      if (is_r) S.tNinR[lt] = (u16)n_in;
+      else S.tNinS[lt] = (u16)n_in;
     }
   }
   __syncthreads();
 
-  // ---- 3/4: forward-scan mini-joins, count (then emit)
-  const int per = (N + kJoinThreads - 1) / kJoinThreads;
-  const int p0 = min(N, tid * per), p1 = min(N, p0 + per);
-  int lt0 = 0;
-  if (p0 < p1) lt0 = upper_bound_u32(S.tE, nt, (u32)p0) - 1;
+  // ---- 3/4: forward-scan mini-joins: count, look-back, emit
   u32 cnt = 0;
-  {
-    int lt = lt0;
-    for (int p = p0; p < p1; ++p) {
-      while ((u32)p >= S.tE[lt + 1]) ++lt;
-      cnt += sweep_one<false>(S, p, lt, nullptr);
-    }
-  }
+  for (int p = tid; p < N; p += kJoinThreads) cnt += sweep_one<false>(S, p, nullptr);
   u64 total;
   const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
   if (!EMIT) {
-    if (tid == 0) A.unit_cnt[c] = (u32)total;
+    if (tid == 0 && total) atomicAdd((unsigned long long*)&A.hdr->pairs, total);
     return;
   }
-  const i64 start = (i64)A.unit_base[c] + (i64)excl;
+  if (tid == 0) {
+    const u64 b = lookback(A.status, c, total, A.hdr);
+    S.base = b;
+    if (c == A.n_units - 1) A.hdr->pairs = (i64)(b + total);
+  }
+  __syncthreads();
+  const i64 start = (i64)(S.base + excl);
   if (start + (i64)cnt > A.capacity) {
     if (cnt) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
     return;
   }
-  i64* out = A.pairs + 2 * (A.pair_base + start);
-  int lt = lt0;
-  for (int p = p0; p < p1; ++p) {
-    while ((u32)p >= S.tE[lt + 1]) ++lt;
-    out += 2 * (i64)sweep_one<true>(S, p, lt, out);
-  }
+  i64* out = A.pairs + 2 * start;
+  for (int p = tid; p < N; p += kJoinThreads) out += 2 * (i64)sweep_one<true>(S, p, out);
 }
 
-// Large join tiles (|R_T|+|S_T| > kLmax): the larger side is split into
-// work items of kLargeLead entries, one per thread; the other side streams
-// through shared memory.  Every (lead, other) pair is tested with the full
-// closed-interval predicate (intersects, geometry.py:59-61) and the class
-// rule (>=1 x-in and >=1 y-in ⇔ Eq. 1 owner tile).
-struct LargeSmem {
-  Entry other[kLargeStage];
-  i64 oid[kLargeStage];
-  u64 scan[33];
-};
-
+// Large join tiles (|R_T|+|S_T| > kLmax): the larger side is split into work
+// items of kLargeLead entries, one per thread; the other side streams through
+// shared memory.  Every (lead, other) pair is tested with the full
+// closed-interval predicate (intersects, geometry.py:59-61) and the class rule
+// (>= 1 x-in and >= 1 y-in ⇔ Eq. 1 owner tile).
 template <bool EMIT>
-__device__ __forceinline__ u32 large_pass(const LargeSmem& S, int n, bool have, const Entry& me,
+__device__ __forceinline__ u32 large_pass(const LargeSmem& S, int n, bool have, const Half& me,
                                           bool lead_r, i64 my_id, i64* out) {
   u32 c = 0;
   if (!have) return 0;
   const double mxl = key_x(me.xl_key);
   const bool mxin = !(me.xl_key & kXOut), myin = !(me.xl_key & kYOut);
   for (int k = 0; k < n; ++k) {
-    const Entry o = S.other[k];
-    const double oxl = key_x(o.xl_key);
-    const bool oxin = !(o.xl_key & kXOut), oyin = !(o.xl_key & kYOut);
-    if (mxl <= o.xu && oxl <= me.xu && me.yl <= o.yu && o.yl <= me.yu && (mxin || oxin) &&
-        (myin || oyin)) {
+    const Rec& o = S.other[k];
+    const u64 ok = o.xl_key;
+    const double oxl = key_x(ok);
+    if (mxl <= o.xu && oxl <= me.xu && me.yl <= o.yu && o.yl <= me.yu &&
+        (mxin || !(ok & kXOut)) && (myin || !(ok & kYOut))) {
       if (EMIT) {
-        out[2 * (i64)c] = lead_r ? my_id : S.oid[k];
-        out[2 * (i64)c + 1] = lead_r ? S.oid[k] : my_id;
+        *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
+            lead_r ? make_longlong2(my_id, o.id) : make_longlong2(o.id, my_id);
       }
       ++c;
     }
@@ -811,71 +940,85 @@ __device__ __forceinline__ u32 large_pass(const LargeSmem& S, int n, bool have, 
 }
 
 template <bool EMIT>
-__global__ void __launch_bounds__(kLargeLead) k_join_large(JoinArgs A) {
-  extern __shared__ __align__(32) unsigned char smem_raw[];
-  LargeSmem& S = *reinterpret_cast<LargeSmem*>(smem_raw);
-  const int item = blockIdx.x;
+__device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit) {
   const int tid = threadIdx.x;
+  const i64 item = unit - A.n_chunks;
   // item → large tile (binary search over the work-item prefix)
   int lo = 0, hi = (int)A.hdr->n_large;
   while (lo < hi) {
     const int m = (lo + hi) >> 1;
-    if (A.lpre[m] <= (u32)item) lo = m + 1; else hi = m;
+    if ((i64)A.lpre[m] <= item) lo = m + 1; else hi = m;
   }
   const int lj = lo - 1;
-  const u32 t = A.llist[lj];
-  const u32 nR = A.cnt_r[t], nS = A.cnt_s[t];
-  const u32 rs = A.off_r[t] - nR, ss = A.off_s[t] - nS;
-  if (tid == 0) {
-    const u32 prevR = t == 0 ? 0u : A.off_r[t - 1];
-    const u32 prevS = t == 0 ? 0u : A.off_s[t - 1];
-    if (rs != prevR || ss != prevS) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
-  }
+  const uint4 rec = A.lrec[lj];
+  const u32 nR = rec.z, nS = rec.w;
   const bool lead_r = nR >= nS;
-  const u32 nl = lead_r ? nR : nS, no = lead_r ? nS : nR;
-  const Entry* L = lead_r ? A.rl + rs : A.sl + ss;
-  const Entry* O = lead_r ? A.sl + ss : A.rl + rs;
-  const i64* Lid = lead_r ? A.rid + rs : A.sid + ss;
-  const i64* Oid = lead_r ? A.sid + ss : A.rid + rs;
-  const u32 a = (u32)(item - (int)A.lpre[lj]) * kLargeLead + tid;
+  const u32 no = lead_r ? nS : nR;
+  const Rec* L = lead_r ? A.rl + rec.x : A.sl + rec.y;
+  const Rec* O = lead_r ? A.sl + rec.y : A.rl + rec.x;
+  const u32 nl = lead_r ? nR : nS;
+  const u32 a = (u32)(item - (i64)A.lpre[lj]) * kLargeLead + tid;
   const bool have = a < nl;
-  Entry me;
+  Half me;
   i64 my_id = 0;
   if (have) {
-    me = L[a];
-    if (EMIT) my_id = Lid[a];
+    me = *reinterpret_cast<const Half*>(L + a);
+    my_id = L[a].id;
   }
+  if (tid == 0) mbar_init(&S.bar, 1);
+  __syncthreads();
+  u32 phase = 0;
   u32 cnt = 0;
-  for (u32 ob = 0; ob < no; ob += kLargeStage) {
-    const int n = (int)min((u32)kLargeStage, no - ob);
-    __syncthreads();
-    for (int k = tid; k < n; k += kLargeLead) {
-      S.other[k] = O[ob + k];
+  const int passes = EMIT ? 2 : 1;
+  i64* out = nullptr;
+  bool ok = true;
+  for (int pass = 0; pass < passes; ++pass) {
+    for (u32 ob = 0; ob < no; ob += kCap) {
+      const int n = (int)min((u32)kCap, no - ob);
+      __syncthreads();  // previous piece fully consumed
+      if (tid == 0) {
+        mbar_expect_tx(&S.bar, (u32)n * (u32)sizeof(Rec));
+        bulk_g2s(&S.other[0], O + ob, (u32)n * (u32)sizeof(Rec), &S.bar);
+      }
+      mbar_wait(&S.bar, phase);
+      phase ^= 1u;
+      if (pass == 0) {
+        cnt += large_pass<false>(S, n, have, me, lead_r, my_id, nullptr);
+      } else if (ok) {
+        out += 2 * (i64)large_pass<true>(S, n, have, me, lead_r, my_id, out);
+      }
     }
-    __syncthreads();
-    cnt += large_pass<false>(S, n, have, me, lead_r, my_id, nullptr);
-  }
-  u64 total;
-  const u64 excl = block_excl_scan<kLargeLead>((u64)cnt, &total, S.scan);
-  const i64 unit = A.n_chunks + item;
-  if (!EMIT) {
-    if (tid == 0) A.unit_cnt[unit] = (u32)total;
-    return;
-  }
-  const i64 start = (i64)A.unit_base[unit] + (i64)excl;
-  const bool ok = start + (i64)cnt <= A.capacity;
-  if (!ok && cnt) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
-  i64* out = A.pairs + 2 * (A.pair_base + start);
-  for (u32 ob = 0; ob < no; ob += kLargeStage) {
-    const int n = (int)min((u32)kLargeStage, no - ob);
-    __syncthreads();
-    for (int k = tid; k < n; k += kLargeLead) {
-      S.other[k] = O[ob + k];
-      S.oid[k] = Oid[ob + k];
+    if (pass == 0) {
+      u64 total;
+      const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
+      if (!EMIT) {
+        if (tid == 0 && total) atomicAdd((unsigned long long*)&A.hdr->pairs, total);
+        return;
+      }
+      if (tid == 0) {
+        const u64 b = lookback(A.status, unit, total, A.hdr);
+        S.base = b;
+        if (unit == A.n_units - 1) A.hdr->pairs = (i64)(b + total);
+      }
+      __syncthreads();
+      const i64 start = (i64)(S.base + excl);
+      ok = start + (i64)cnt <= A.capacity;
+      if (!ok && cnt) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
+      out = A.pairs + 2 * start;
     }
-    __syncthreads();
-    if (ok) out += 2 * (i64)large_pass<true>(S, n, have, me, lead_r, my_id, out);
   }
+}
+
+template <bool EMIT>
+__global__ void __launch_bounds__(kJoinThreads, 2) k_join(JoinArgs A) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  JoinSmem& U = *reinterpret_cast<JoinSmem*>(smem_raw);
+  __shared__ int s_unit;
+  if (threadIdx.x == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
+  __syncthreads();
+  const int unit = s_unit;
+  if (unit < A.n_chunks) join_chunk<EMIT>(U.c, A, unit);
+  else join_large<EMIT>(U.l, A, unit);
 }
 
 // ---------------------------------------------------------------- ε refinement
@@ -929,24 +1072,24 @@ inline bool grid_ok(int kx, int ky, int row_lo, int row_hi) {
          row_hi <= ky && (u64)kx * (u64)(row_hi - row_lo) < (1ull << 32) - 2;
 }
 
-int g_num_sms = 0;
-inline int num_sms() {
-  if (g_num_sms == 0) {
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
-  return g_num_sms;
+  return n;
 }
 
-struct ScratchLayout {
+struct ScanLayout {
   size_t cnt, base, partials, total;
   u64 n, nb;
 };
-inline ScratchLayout scratch_layout(i64 n_chunks, i64 n_items) {
-  ScratchLayout L;
-  L.n = (u64)(n_chunks + n_items);
+inline ScanLayout scan_layout(i64 n) {
+  ScanLayout L;
+  L.n = (u64)n;
   L.nb = (L.n + kScanTile - 1) / kScanTile;
   size_t o = 0;
   L.cnt = o; o = align_up(o + 4 * (L.n + 1), 256);
@@ -956,50 +1099,57 @@ inline ScratchLayout scratch_layout(i64 n_chunks, i64 n_items) {
   return L;
 }
 
-bool g_attr_set = false;
+// join scratch: [ticket | status[n_units]]
+inline size_t join_scratch(i64 n_units) { return 256 + align_up(8 * (size_t)(n_units + 1), 256); }
+
 int set_smem_attrs() {
-  if (g_attr_set) return 0;
+  static bool done = false;
+  if (done) return 0;
   cudaError_t e;
-  e = cudaFuncSetAttribute(k_join_chunk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(ChunkSmem));
+  e = cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(JoinSmem));
   if (e != cudaSuccess) return (int)e;
-  e = cudaFuncSetAttribute(k_join_chunk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(ChunkSmem));
+  e = cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(JoinSmem));
   if (e != cudaSuccess) return (int)e;
-  e = cudaFuncSetAttribute(k_join_large<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(LargeSmem));
-  if (e != cudaSuccess) return (int)e;
-  e = cudaFuncSetAttribute(k_join_large<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(LargeSmem));
-  if (e != cudaSuccess) return (int)e;
-  g_attr_set = true;
+  done = true;
   return 0;
 }
 
-JoinArgs make_args(const Ws& w, const pbsm_entry* r_list, const pbsm_entry* s_list,
-                   i64 n_chunks, const ScratchLayout& SL, void* scratch) {
+int launch_join(bool emit, void* ws, int kx, int ky, int row_lo, int row_hi,
+                const pbsm_entry* r_list, const pbsm_entry* s_list, i64 n_chunks, i64 n_items,
+                void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s) {
+  int rc = set_smem_attrs();
+  if (rc) return rc;
+  const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
+  Ws w = ws_bind(ws, L);
+  const i64 n_units = n_chunks + n_items;
+  // write guard first (reads the cursors the scatter left behind)
+  const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
+                                                                (i64)num_sms() * 8));
+  k_guard<<<gb, 256, 0, s>>>(w.cur_r, w.cnt_r, w.cur_s, w.cnt_s, L.tiles, w.hdr);
+  cudaMemsetAsync(&w.hdr->pairs, 0, sizeof(int64_t), s);
+  if (n_units == 0) return launch_status();
+  cudaMemsetAsync(scratch, 0, join_scratch(n_units), s);
   JoinArgs A;
-  A.jlist = w.jlist;
-  A.je = w.je;
+  A.jrec = w.jrec;
   A.cstart = w.cstart;
-  A.llist = w.llist;
+  A.lrec = w.lrec;
   A.lpre = w.lpre;
-  A.cnt_r = w.cnt_r;
-  A.cnt_s = w.cnt_s;
-  A.off_r = w.off_r;
-  A.off_s = w.off_s;
-  A.rl = reinterpret_cast<const Entry*>(r_list);
-  A.sl = reinterpret_cast<const Entry*>(s_list);
-  A.rid = nullptr;
-  A.sid = nullptr;
-  A.unit_cnt = (u32*)((char*)scratch + SL.cnt);
-  A.unit_base = (const u64*)((char*)scratch + SL.base);
-  A.pairs = nullptr;
-  A.pair_base = 0;
-  A.capacity = 0;
+  A.rl = reinterpret_cast<const Rec*>(r_list);
+  A.sl = reinterpret_cast<const Rec*>(s_list);
+  A.ticket = (u32*)scratch;
+  A.status = (u64*)((char*)scratch + 256);
+  A.pairs = (i64*)pairs;
+  A.capacity = capacity;
   A.n_chunks = n_chunks;
+  A.n_units = n_units;
   A.hdr = w.hdr;
-  return A;
+  if (emit)
+    k_join<true><<<(unsigned)n_units, kJoinThreads, sizeof(JoinSmem), s>>>(A);
+  else
+    k_join<false><<<(unsigned)n_units, kJoinThreads, sizeof(JoinSmem), s>>>(A);
+  return launch_status();
 }
 
 }  // namespace
@@ -1010,8 +1160,9 @@ extern "C" {
 int32_t pbsm_abi_version(void) { return PBSM_ABI_VERSION; }
 
 const char* pbsm_build_info(void) {
-  return "pbsm sm_100a: count/plan/scatter + chunk sort-sweep + large nested-loop; "
-         "kCap=1536 kLmax=512";
+  return "pbsm sm_100a v2: count+validate / plan / scatter(64B records, join tiles only) / "
+         "guard / fused TMA-staged sort+sweep join with decoupled look-back; "
+         "kCap=1024 kLmax=384";
 }
 
 int64_t pbsm_workspace_bytes(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi) {
@@ -1040,10 +1191,12 @@ int pbsm_count(const double* xl, const double* xu, const double* yl, const doubl
   if (n == 0) return 0;
   if (!xl || !xu || !yl || !yu) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * 16);
+  const i64 per_block = 256 * kRectsPerThread;
+  const i64 blocks = std::min<i64>((n + per_block - 1) / per_block, (i64)num_sms() * 8);
   k_count<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(xl, xu, yl, yu, n, kx, ky, row_lo,
                                                            row_hi, w.bx, w.by,
-                                                           side ? w.cnt_s : w.cnt_r);
+                                                           side ? w.cnt_s : w.cnt_r, side,
+                                                           w.hdr);
   return launch_status();
 }
 
@@ -1055,8 +1208,8 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi, 
                                                               w.partials, w.hdr);
   k_plan_partials<<<1, 1024, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je, w.lpre, w.cstart);
   k_plan_apply<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles,
-                                                             w.partials, w.off_r, w.off_s,
-                                                             w.jlist, w.je, w.llist, w.lpre);
+                                                             w.nblocks, w.partials, w.cur_r, w.cur_s,
+                                                             w.jrec, w.je, w.lrec, w.lpre);
   const i64 blocks = std::min<i64>((i64)((w.tiles + 255) / 256), (i64)num_sms() * 8);
   k_chunks<<<(unsigned)std::max<i64>(blocks, 1), 256, 0, s>>>(w.je, w.cstart, w.hdr);
   return launch_status();
@@ -1073,23 +1226,25 @@ int pbsm_read_header(void* ws, pbsm_header* out, void* stream) {
 
 int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu, const double* yl,
                  const double* yu, int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky,
-                 int32_t row_lo, int32_t row_hi, pbsm_entry* out, int64_t* out_ids,
-                 int64_t capacity, void* stream) {
-  if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1))
+                 int32_t row_lo, int32_t row_hi, pbsm_entry* out, int64_t capacity,
+                 void* stream) {
+  if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1) ||
+      capacity < 0)
     return PBSM_E_ARG;
   if (n == 0) return 0;
-  if (!ids || !xl || !xu || !yl || !yu || ((!out || !out_ids) && capacity > 0)) return PBSM_E_ARG;
+  if (!ids || !xl || !xu || !yl || !yu || (!out && capacity > 0)) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * 16);
+  const i64 per_block = 256 * kRectsPerThread;
+  const i64 blocks = std::min<i64>((n + per_block - 1) / per_block, (i64)num_sms() * 8);
   k_scatter<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       (const i64*)ids, xl, xu, yl, yu, n, kx, ky, row_lo, row_hi, w.bx, w.by,
-      side ? w.off_s : w.off_r, reinterpret_cast<Entry*>(out), (i64*)out_ids, capacity, w.hdr);
+      side ? w.cur_s : w.cur_r, reinterpret_cast<Rec*>(out), capacity, w.hdr);
   return launch_status();
 }
 
 int64_t pbsm_join_scratch_bytes(int64_t n_chunks, int64_t n_items) {
   if (n_chunks < 0 || n_items < 0) return PBSM_E_ARG;
-  return (int64_t)scratch_layout(n_chunks, n_items).total;
+  return (int64_t)join_scratch(n_chunks + n_items);
 }
 
 int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
@@ -1097,68 +1252,37 @@ int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t ro
                     int64_t n_items, void* scratch, void* stream) {
   if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || n_chunks < 0 || n_items < 0)
     return PBSM_E_ARG;
-  int rc = set_smem_attrs();
-  if (rc) return rc;
-  Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const ScratchLayout SL = scratch_layout(n_chunks, n_items);
-  cudaStream_t s = as_stream(stream);
-  JoinArgs A = make_args(w, r_list, s_list, n_chunks, SL, scratch);
-  if (n_chunks > 0)
-    k_join_chunk<false><<<(unsigned)n_chunks, kJoinThreads, sizeof(ChunkSmem), s>>>(A);
-  if (n_items > 0) {
-    k_join_large<false><<<(unsigned)n_items, kLargeLead, sizeof(LargeSmem), s>>>(A);
-  }
-  const u64 n = SL.n;
-  if (n > 0) {
-    u32* cnt = (u32*)((char*)scratch + SL.cnt);
-    u64* base = (u64*)((char*)scratch + SL.base);
-    u64* part = (u64*)((char*)scratch + SL.partials);
-    k_scan_reduce<<<(unsigned)SL.nb, kScanThreads, 0, s>>>(cnt, n, part);
-    k_scan_partials<<<1, 1024, 0, s>>>(part, SL.nb, base, n, w.hdr);
-    k_scan_apply<<<(unsigned)SL.nb, kScanThreads, 0, s>>>(cnt, n, part, base);
-  } else {
-    cudaMemsetAsync(&w.hdr->pairs, 0, sizeof(int64_t), s);
-  }
-  return launch_status();
+  return launch_join(false, ws, kx, ky, row_lo, row_hi, r_list, s_list, n_chunks, n_items,
+                     scratch, nullptr, 0, as_stream(stream));
 }
 
 int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-                   const pbsm_entry* r_list, const int64_t* r_ids, const pbsm_entry* s_list,
-                   const int64_t* s_ids, int64_t n_chunks, int64_t n_items, const void* scratch,
-                   int64_t* pairs, int64_t pair_base, int64_t capacity, void* stream) {
+                   const pbsm_entry* r_list, const pbsm_entry* s_list, int64_t n_chunks,
+                   int64_t n_items, void* scratch, int64_t* pairs, int64_t capacity,
+                   void* stream) {
   if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || n_chunks < 0 || n_items < 0 ||
-      pair_base < 0 || capacity < 0)
+      capacity < 0 || (capacity > 0 && !pairs))
     return PBSM_E_ARG;
-  if (capacity > 0 && !pairs) return PBSM_E_ARG;
-  int rc = set_smem_attrs();
-  if (rc) return rc;
-  Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const ScratchLayout SL = scratch_layout(n_chunks, n_items);
-  cudaStream_t s = as_stream(stream);
-  JoinArgs A = make_args(w, r_list, s_list, n_chunks, SL, const_cast<void*>(scratch));
-  A.rid = (const i64*)r_ids;
-  A.sid = (const i64*)s_ids;
-  A.pairs = (i64*)pairs;
-  A.pair_base = pair_base;
-  A.capacity = capacity;
-  if (n_chunks > 0)
-    k_join_chunk<true><<<(unsigned)n_chunks, kJoinThreads, sizeof(ChunkSmem), s>>>(A);
-  if (n_items > 0) {
-    k_join_large<true><<<(unsigned)n_items, kLargeLead, sizeof(LargeSmem), s>>>(A);
-  }
-  return launch_status();
+  return launch_join(true, ws, kx, ky, row_lo, row_hi, r_list, s_list, n_chunks, n_items,
+                     scratch, pairs, capacity, as_stream(stream));
 }
 
 int64_t pbsm_refine_scratch_bytes(int64_t n_cand) {
   if (n_cand < 0) return PBSM_E_ARG;
-  return (int64_t)scratch_layout(n_cand, 0).total;
+  return (int64_t)scan_layout(n_cand).total;
+}
+
+int64_t pbsm_refine_result_offset(int64_t n_cand) {
+  if (n_cand < 0) return PBSM_E_ARG;
+  const ScanLayout SL = scan_layout(n_cand);
+  return (int64_t)(SL.base + 8 * SL.n);
 }
 
 int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const double* py,
                 const double* qx, const double* qy, const int64_t* p_ids, const int64_t* q_ids,
                 double eps_sq, void* scratch, int64_t* out, void* stream) {
   if (n_cand < 0 || !scratch) return PBSM_E_ARG;
-  const ScratchLayout SL = scratch_layout(n_cand, 0);
+  const ScanLayout SL = scan_layout(n_cand);
   cudaStream_t s = as_stream(stream);
   u64* base = (u64*)((char*)scratch + SL.base);
   if (n_cand == 0) {
@@ -1171,17 +1295,11 @@ int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const dou
   const unsigned blocks = (unsigned)std::min<i64>((n_cand + 255) / 256, (i64)num_sms() * 16);
   k_refine_flag<<<blocks, 256, 0, s>>>((const i64*)cand, n_cand, px, py, qx, qy, eps_sq, flag);
   k_scan_reduce<<<(unsigned)SL.nb, kScanThreads, 0, s>>>(flag, SL.n, part);
-  k_scan_partials<<<1, 1024, 0, s>>>(part, SL.nb, base, SL.n, nullptr);
+  k_scan_partials<<<1, 1024, 0, s>>>(part, SL.nb, base, SL.n);
   k_scan_apply<<<(unsigned)SL.nb, kScanThreads, 0, s>>>(flag, SL.n, part, base);
   k_refine_compact<<<blocks, 256, 0, s>>>((const i64*)cand, n_cand, flag, base,
                                           (const i64*)p_ids, (const i64*)q_ids, (i64*)out);
   return launch_status();
-}
-
-int64_t pbsm_refine_result_offset(int64_t n_cand) {
-  if (n_cand < 0) return PBSM_E_ARG;
-  const ScratchLayout SL = scratch_layout(n_cand, 0);
-  return (int64_t)(SL.base + 8 * SL.n);
 }
 
 }  // extern "C"

@@ -23,7 +23,7 @@ import torch
 from . import _native
 from .errors import KernelError
 
-__all__ = ["DeviceRects", "DeviceJoinResult", "run_join", "to_device"]
+__all__ = ["DeviceRects", "DeviceJoinResult", "PhaseProbe", "run_join", "to_device"]
 
 
 @dataclass
@@ -91,19 +91,64 @@ def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None or t.numel() == 0 else t.data_ptr()
 
 
-def _read_header(lib, ws, stream) -> _native.Header:
+# messages of RectBatch.validate (geometry.py:166-177), raised in the same order:
+# R before S, inverted before out-of-range
+_VALIDATION = (
+    (_native.ERR_INVERTED, "inverted rectangle: lower bound exceeds upper bound"),
+    (_native.ERR_RANGE, "coordinates outside [0, 1]; normalize the datasets first"),
+    (_native.ERR_INVERTED << 2, "inverted rectangle: lower bound exceeds upper bound"),
+    (_native.ERR_RANGE << 2, "coordinates outside [0, 1]; normalize the datasets first"),
+)
+_VALIDATION_BITS = sum(b for b, _ in _VALIDATION)
+
+
+def _read_header(lib, ws, stream, allow=0) -> _native.Header:
     h = _native.Header()
     _native.check(lib.pbsm_read_header(ws.data_ptr(), C.byref(h), stream), "pbsm_read_header")
-    if h.error:
-        raise KernelError(f"device guard: {_native.describe_error(h.error)} "
+    for bit, msg in _VALIDATION:
+        if h.error & bit:
+            raise ValueError(msg)
+    bad = h.error & ~allow & ~_VALIDATION_BITS
+    if bad:
+        raise KernelError(f"device guard: {_native.describe_error(bad)} "
                           "(partition write overflow check, partition.py:229-233)")
     return h
 
 
+class PhaseProbe:
+    """Records a CUDA event after every library call (per-kernel timing in bench.py)."""
+
+    def __init__(self):
+        self.marks: list[tuple[str, torch.cuda.Event]] = []
+
+    def mark(self, name: str) -> None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((name, ev))
+
+    def durations(self) -> dict:
+        """Seconds per phase name, summed over repeats."""
+        out: dict = {}
+        for (_, a), (name, b) in zip(self.marks, self.marks[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b) / 1e3
+        return out
+
+
+def pair_capacity(h) -> int:
+    """Initial pair-buffer size: the exact bound when affordable, else a
+    generous estimate (the emit pass reports overflow and is re-run)."""
+    return int(min(h.pair_bound, 2 * (h.list_r + h.list_s) + (1 << 20)))
+
+
 def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool = True,
              row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
-             keep_counts: bool = False) -> DeviceJoinResult:
-    """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi))."""
+             keep_counts: bool = False, probe: PhaseProbe | None = None) -> DeviceJoinResult:
+    """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
+
+    ``probe`` (optional) gets an event after each library call, named after
+    the phase that call ran: init, count, plan, header, scatter, join, header2.
+    """
+    mark = probe.mark if probe is not None else (lambda name: None)
     lib = _native.load()
     if row_hi is None:
         row_hi = ky
@@ -115,62 +160,72 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     ws = _workspace(lib, device, kx, ky, row_lo, row_hi)
     wsp = ws.data_ptr()
     grid = (kx, ky, row_lo, row_hi)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timing else None
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
     if ev:
         ev[0].record()
-
+    mark("start")
     _native.check(lib.pbsm_init(wsp, *grid, stream), "pbsm_init")
+    mark("init")
     for side, b in ((0, r), (1, s)):
         _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
                                      side, wsp, *grid, stream), "pbsm_count")
+    mark("count")
+    counts = None
+    if keep_counts:  # per-tile counts, before the plan turns them into cursor ends
+        counts = tuple(v.clone() for v in _tile_count_views(ws, kx, ky, kx * (row_hi - row_lo)))
     _native.check(lib.pbsm_plan(wsp, *grid, stream), "pbsm_plan")
+    mark("plan")
     h = _read_header(lib, ws, stream)
+    mark("header")
 
     lists = []
-    for side, b, total in ((0, r, h.a_r), (1, s, h.a_s)):
-        ent = torch.empty((max(total, 1), 4), dtype=torch.float64, device=device)
-        eid = torch.empty(max(total, 1), dtype=torch.int64, device=device)
+    for side, b, total in ((0, r, h.list_r), (1, s, h.list_s)):
+        ent = torch.empty((max(total, 1), 8), dtype=torch.int64, device=device)  # 64 B records
         _native.check(lib.pbsm_scatter(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
                                        _ptr(b.yu), len(b), side, wsp, *grid, ent.data_ptr(),
-                                       eid.data_ptr(), total, stream), "pbsm_scatter")
-        lists.append((ent, eid))
+                                       total, stream), "pbsm_scatter")
+        lists.append(ent)
+    mark("scatter")
     if ev:
         ev[1].record()
 
     n_chunks, n_items = h.n_chunks, h.n_items
     scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(n_chunks, n_items)),
                           dtype=torch.uint8, device=device)
-    (rl, rid), (sl, sid) = lists
-    _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), n_chunks,
-                                      n_items, scratch.data_ptr(), stream), "pbsm_join_count")
-    h2 = _read_header(lib, ws, stream)
-    if ev:
-        ev[2].record()
-    count = int(h2.pairs)
+    rl, sl = lists
     pairs = None
-    if collect:
-        pairs = torch.empty((max(count, 1), 2), dtype=torch.int64, device=device)
-        _native.check(lib.pbsm_join_emit(wsp, *grid, rl.data_ptr(), rid.data_ptr(),
-                                         sl.data_ptr(), sid.data_ptr(), n_chunks, n_items,
-                                         scratch.data_ptr(), pairs.data_ptr(), 0, count,
-                                         stream), "pbsm_join_emit")
+    if not collect:
+        _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), n_chunks,
+                                          n_items, scratch.data_ptr(), stream),
+                      "pbsm_join_count")
+        mark("join")
         h2 = _read_header(lib, ws, stream)
+        mark("header2")
+        count = int(h2.pairs)
+    else:
+        cap = pair_capacity(h)
+        while True:
+            pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
+            _native.check(lib.pbsm_join_emit(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
+                                             n_chunks, n_items, scratch.data_ptr(),
+                                             pairs.data_ptr(), cap, stream), "pbsm_join_emit")
+            mark("join")
+            h2 = _read_header(lib, ws, stream, allow=_native.ERR_PAIR_OVERFLOW)
+            mark("header2")
+            count = int(h2.pairs)
+            if count <= cap:
+                break
+            cap = count  # rare: the estimate was short, emit again into an exact buffer
         pairs = pairs[:count]
     if ev:
-        ev[3].record()
-        ev[3].synchronize()
+        ev[2].record()
+        ev[2].synchronize()
     res = DeviceJoinResult(count, pairs, header=h2.as_dict())
     if ev:
-        res.times = {
-            "partition": ev[0].elapsed_time(ev[1]) / 1e3,
-            "join_count": ev[1].elapsed_time(ev[2]) / 1e3,
-            "emit": ev[2].elapsed_time(ev[3]) / 1e3,
-            "total": ev[0].elapsed_time(ev[3]) / 1e3,
-        }
-    if keep_counts:
-        T = kx * (row_hi - row_lo)
-        # the workspace is reused by the next join: hand out copies
-        res.tile_counts = tuple(v.clone() for v in _tile_count_views(ws, kx, ky, T))
+        res.times = {"partition": ev[0].elapsed_time(ev[1]) / 1e3,
+                     "join": ev[1].elapsed_time(ev[2]) / 1e3,
+                     "total": ev[0].elapsed_time(ev[2]) / 1e3}
+    res.tile_counts = counts
     return res
 
 

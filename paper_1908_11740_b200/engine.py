@@ -146,7 +146,7 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
     return JoinReport(
         result_count=int(count), pairs=out,
         partition_time=t.get("partition", 0.0), sort_time=0.0,
-        join_time=t.get("join_count", 0.0) + t.get("emit", 0.0),
+        join_time=t.get("join", 0.0),
         total_time=time.perf_counter() - t0,
         _task_sizes=_task_sizes_fn(rd, sd, kx, ky))
 
@@ -156,8 +156,13 @@ def join(r: RectBatch | Sequence[Rect], s: RectBatch | Sequence[Rect],
     """Every intersecting (r, s) pair of R × S exactly once (engine.py:312-323)."""
     r, s = as_batch(r), as_batch(s)
     _resolve_policy(cfg)
-    r.validate()
-    s.validate()
+    if len(r) == 0 or len(s) == 0 or not torch.cuda.is_available():
+        r.validate()
+        s.validate()
+    # otherwise RectBatch.validate runs on the device inside the count pass
+    # (same checks, same ValueError messages and order: R before S); without
+    # a device the host check keeps the reference's ValueError ahead of the
+    # KernelError "no CUDA device"
     return _run(r, s, cfg, time.perf_counter())
 
 
