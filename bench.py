@@ -208,10 +208,10 @@ def count_launches(h: dict) -> int:
     """Our kernels per join step (see device.run_join / pbsm.cu host glue)."""
     n = 1            # k_bounds
     n += 2           # k_count R, S
-    n += 4           # k_plan_reduce, k_plan_partials, k_plan_apply, k_chunks
+    n += 5           # k_plan_reduce, k_plan_partials, k_plan_apply, k_chunks x2
     n += 2           # k_scatter R, S
     n += 1           # k_guard
-    n += 1 if h["n_chunks"] + h["n_items"] > 0 else 0   # k_join (fused sort/sweep/emit)
+    n += 1 if h["n_units"] > 0 else 0   # k_join (all mini-join strategies, count -> emit)
     return n
 
 

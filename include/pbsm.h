@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 2
+#define PBSM_ABI_VERSION 3
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -77,23 +77,34 @@ typedef struct pbsm_entry {
   uint64_t pad[3];
 } pbsm_entry;
 
-/* plan/result totals, device-resident at the start of the workspace */
+/* plan/result totals, device-resident at the start of the workspace.
+ * Join tiles (both inputs non-empty, build_task_queue engine.py:97) are
+ * split by a per-tile cost model into three mini-join strategies:
+ *   nested — |R_T|+|S_T| <= LMAX and |R_T|*|S_T| <= NESTED_MAX: every
+ *            (r, s) pair of the tile tested with the class rule (cheaper
+ *            than sorting when the tile is this small);
+ *   sorted — |R_T|+|S_T| <= LMAX otherwise: per-tile segmented sort by x-lower
+ *            + forward-scan sweep (Alg. 1) in shared memory;
+ *   large  — |R_T|+|S_T| > LMAX: split over several CTAs.
+ * Work units of one join launch: [nested chunks | sorted chunks | large items]. */
 typedef struct pbsm_header {
   int64_t a_r;            /* Σ per-tile R counts = PartitionedDataset.total_assigned */
   int64_t a_s;            /* same for S                                             */
   int64_t list_r;         /* R entries written to tile lists (join tiles only)     */
   int64_t list_s;         /* same for S                                             */
-  int64_t n_join;         /* join tiles (both inputs non-empty) on the chunk path  */
-  int64_t w_join;         /* entries (R+S) in those tiles                           */
-  int64_t n_chunks;       /* CTA work units of the chunk path                       */
-  int64_t n_large;        /* join tiles too large for one CTA's shared memory       */
-  int64_t n_items;        /* work units of the large-tile path                      */
+  int64_t n_nested;       /* join tiles per strategy                                */
+  int64_t n_sorted;
+  int64_t n_large;
+  int64_t w_nested;       /* entries (R+S) in nested / sorted tiles                 */
+  int64_t w_sorted;
+  int64_t chunks_nested;  /* CTA chunks of nested / sorted tiles                    */
+  int64_t chunks_sorted;
+  int64_t n_items;        /* work items of the large tiles                          */
   int64_t pairs;          /* result_count, valid after pbsm_join_count/emit         */
   int64_t pair_bound;     /* Σ |R_T|·|S_T| over join tiles (>= pairs)               */
   int64_t max_tile;       /* largest |R_T|+|S_T| over join tiles                   */
   uint32_t error;         /* PBSM_ERR_* bits                                        */
   uint32_t pad;
-  int64_t reserved[3];
 } pbsm_header;
 
 /* Bytes of the grid workspace for a kx × (row_hi-row_lo) strip. */
@@ -112,10 +123,12 @@ int pbsm_count(const double* xl, const double* xu, const double* yl,
                void* stream);
 
 /* compute_segment_offsets (partition.py:151-164) for both inputs plus the
- * join-task plan (build_task_queue, engine.py:84-100): CSR offsets, the list
- * of join tiles, their CTA chunks and the large-tile work items. */
+ * join-task plan (build_task_queue, engine.py:84-100): CSR offsets, the join
+ * tiles of each mini-join strategy, their CTA chunks and the large-tile work
+ * items.  nested_max: cost-model threshold on |R_T|*|S_T| for the nested
+ * strategy (< 0: the built-in default; 0: sort + sweep every small tile). */
 int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-              void* stream);
+              int64_t nested_max, void* stream);
 
 /* Copy the device header to *out and synchronise the stream. */
 int pbsm_read_header(void* ws, pbsm_header* out, void* stream);
@@ -130,29 +143,34 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu,
                  void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                  pbsm_entry* out, int64_t capacity, void* stream);
 
-/* Scratch bytes for one join launch (work ticket + look-back words). */
-int64_t pbsm_join_scratch_bytes(int64_t n_chunks, int64_t n_items);
+/* Scratch bytes for one join over n_units work units
+ * (n_units = chunks_nested + chunks_sorted + n_items).  The join entry points
+ * take `plan`, the host copy of the header read after pbsm_plan, for the
+ * work-unit counts (nested chunks run on a persistent double-buffered grid). */
+int64_t pbsm_join_scratch_bytes(int64_t n_units);
 
 /* sort_segment + sweep_count (_kernels.pyx:188-228, 231-315) for every join
- * tile: the write guard (partition.py:229-233), then per-tile segmented sort
- * by x-lower and forward-scan mini-joins over the class combinations; the
- * total lands in header.pairs (= JoinReport.result_count). */
+ * tile: the write guard (partition.py:229-233), then the mini-joins over the
+ * class combinations (nested / sorted+forward-scan / large, see pbsm_header);
+ * the total lands in header.pairs (= JoinReport.result_count). */
 int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                     const pbsm_entry* r_list, const pbsm_entry* s_list,
-                    int64_t n_chunks, int64_t n_items, void* scratch,
-                    void* stream);
+                    const pbsm_header* plan, void* scratch, void* stream);
 
 /* sweep_collect (_kernels.pyx:318-341) + aggregation (engine.py:293-309):
- * the same sort + sweep; each work unit counts its pairs, takes its output
- * offset from a decoupled look-back over the preceding units, and writes
- * (r_id, s_id) int64 pairs at pairs[2*i], i < header.pairs.  If header.pairs
- * exceeds `capacity` nothing past it is written and PBSM_ERR_PAIR_OVERFLOW is
- * set: re-run with capacity >= header.pairs (header.pair_bound always
- * suffices). */
+ * the same mini-joins; each work unit counts its pairs (pass 1 over shared
+ * memory), reserves its output range, and writes its (r_id, s_id) int64
+ * pairs there (pass 2): pairs[2*i], i < header.pairs.  Ranges are reserved
+ * with one atomic per unit (ordered = 0: the list is a permutation of the
+ * reference's, whose own order is unspecified, engine.py:61-62) or by a
+ * decoupled look-back (ordered = 1: deterministic unit-major order, slower).
+ * If header.pairs exceeds `capacity`, pairs past it are not written and
+ * PBSM_ERR_PAIR_OVERFLOW is set: re-run with capacity >= header.pairs
+ * (header.pair_bound always suffices). */
 int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                    const pbsm_entry* r_list, const pbsm_entry* s_list,
-                   int64_t n_chunks, int64_t n_items, void* scratch,
-                   int64_t* pairs, int64_t capacity, void* stream);
+                   const pbsm_header* plan, void* scratch,
+                   int64_t* pairs, int64_t capacity, int32_t ordered, void* stream);
 
 /* ε-distance refinement (engine.py:201-206, 298-300) of candidate pairs given
  * as ROW indices (cand[2i], cand[2i+1]) into the point arrays p / q: keeps the

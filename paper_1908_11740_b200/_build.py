@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_DIR = PKG / "_lib"
-LIB_PATH = LIB_DIR / "libpbsm.so"
+LIB_PATH = LIB_DIR / os.environ.get("PBSM_LIB_NAME", "libpbsm.so")
 CSRC = PKG / "csrc"
 SOURCES = [CSRC / "pbsm.cu"]
 HEADERS = [ROOT / "include" / "pbsm.h"]
@@ -49,7 +49,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
         return LIB_PATH
     LIB_DIR.mkdir(exist_ok=True)
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(tmp),
+    extra = os.environ.get("PBSM_DEFINES", "").split()  # experiments: -DPBSM_RPT=2 ...
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-o", str(tmp),
            *map(str, SOURCES)]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
@@ -37,15 +37,21 @@ class Header(C.Structure):
 
     _fields_ = [
         ("a_r", C.c_int64), ("a_s", C.c_int64), ("list_r", C.c_int64), ("list_s", C.c_int64),
-        ("n_join", C.c_int64), ("w_join", C.c_int64), ("n_chunks", C.c_int64),
-        ("n_large", C.c_int64), ("n_items", C.c_int64), ("pairs", C.c_int64),
+        ("n_nested", C.c_int64), ("n_sorted", C.c_int64), ("n_large", C.c_int64),
+        ("w_nested", C.c_int64), ("w_sorted", C.c_int64), ("chunks_nested", C.c_int64),
+        ("chunks_sorted", C.c_int64), ("n_items", C.c_int64), ("pairs", C.c_int64),
         ("pair_bound", C.c_int64), ("max_tile", C.c_int64), ("error", C.c_uint32),
-        ("pad", C.c_uint32), ("reserved", C.c_int64 * 3),
+        ("pad", C.c_uint32),
     ]
 
+    @property
+    def n_units(self) -> int:
+        return int(self.chunks_nested + self.chunks_sorted + self.n_items)
+
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_
-                if name not in ("pad", "reserved")}
+        d = {name: getattr(self, name) for name, _ in self._fields_ if name != "pad"}
+        d["n_units"] = self.n_units
+        return d
 
 
 _lock = threading.Lock()
@@ -61,14 +67,15 @@ _SIGNATURES = {
     "pbsm_workspace_bytes": (_I64, [_I32, _I32, _I32, _I32]),
     "pbsm_init": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
     "pbsm_count": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P]),
-    "pbsm_plan": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
+    "pbsm_plan": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _P]),
     "pbsm_read_header": (C.c_int, [_P, C.POINTER(Header), _P]),
     "pbsm_scatter": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32,
                                _P, _I64, _P]),
-    "pbsm_join_scratch_bytes": (_I64, [_I64, _I64]),
-    "pbsm_join_count": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I64, _I64, _P, _P]),
-    "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I64, _I64, _P, _P,
-                                 _I64, _P]),
+    "pbsm_join_scratch_bytes": (_I64, [_I64]),
+    "pbsm_join_count": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P,
+                                  _P]),
+    "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P, _P,
+                                 _I64, _I32, _P]),
     "pbsm_refine_scratch_bytes": (_I64, [_I64]),
     "pbsm_refine_result_offset": (_I64, [_I64]),
     "pbsm_refine": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),

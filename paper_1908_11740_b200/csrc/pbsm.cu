@@ -59,22 +59,43 @@ namespace {
 
 // ---------------------------------------------------------------- constants
 constexpr int kPlanThreads = 256;
-constexpr int kPlanPer = 16;                         // tiles per thread
-constexpr int kPlanTile = kPlanThreads * kPlanPer;   // 4096 tiles per CTA
-constexpr int kNV = 11;                              // plan scan lanes
+constexpr int kPlanPer = 4;                          // tiles per thread
+constexpr int kPlanTile = kPlanThreads * kPlanPer;   // 1024 tiles per CTA
+constexpr int kNV = 14;                              // plan scan lanes (see tile_vals)
+constexpr int kNTot = kNV + 2;                       // + extra totals slots
 
 constexpr int kJoinThreads = 256;
-constexpr int kChunkB = 640;        // chunk bucket width in entries
-constexpr int kLmax = 384;          // largest tile (|R_T|+|S_T|) on the chunk path
+#ifndef PBSM_CHUNK_B
+#define PBSM_CHUNK_B 320
+#endif
+#ifndef PBSM_LMAX
+#define PBSM_LMAX 192
+#endif
+#ifndef PBSM_NESTED_MAX
+#define PBSM_NESTED_MAX 1024
+#endif
+constexpr int kChunkB = PBSM_CHUNK_B;   // chunk bucket width in entries
+constexpr int kLmax = PBSM_LMAX;        // largest tile (|R_T|+|S_T|) staged by one CTA
+constexpr int kNestedMax = PBSM_NESTED_MAX;  // nested strategy iff |R_T|*|S_T| <= this
 constexpr int kCap = kChunkB + kLmax;   // max entries staged per chunk CTA
 constexpr int kMaxTiles = kCap / 2;     // a join tile holds >= 2 entries
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
+constexpr int kPad = 4;                 // SoA row padding (words): bank spread
 
 constexpr int kScanThreads = 256;
 constexpr int kScanPer = 16;
 constexpr int kScanTile = kScanThreads * kScanPer;
 
-constexpr int kRectsPerThread = 4;  // ILP in the count / scatter passes
+#ifndef PBSM_RPT
+#define PBSM_RPT 1
+#endif
+#ifndef PBSM_EF_STORE
+#define PBSM_EF_STORE 0
+#endif
+#ifndef PBSM_PART_MINB
+#define PBSM_PART_MINB 4
+#endif
+constexpr int kRectsPerThread = PBSM_RPT;  // ILP in the count / scatter passes
 
 constexpr u64 kXOut = 1ull << 63;
 constexpr u64 kYOut = 1ull << 62;
@@ -105,7 +126,8 @@ struct __align__(32) Half {  // the MBR half of a record: one sector
 
 // ---------------------------------------------------------------- workspace
 struct WsLayout {
-  size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec, je, cstart, lrec, lpre, partials, total;
+  size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec[2], je[2], cdesc[2], lrec, lpre,
+      partials, total;
   u64 tiles;
   u64 nblocks;
 };
@@ -125,12 +147,14 @@ inline WsLayout ws_layout(int kx, int ky, int row_lo, int row_hi) {
   L.cnt_s = o; o = align_up(o + 4 * T, 256);
   L.cur_r = o; o = align_up(o + 4 * T, 256);
   L.cur_s = o; o = align_up(o + 4 * T, 256);
-  L.jrec = o; o = align_up(o + 16 * T, 256);
-  L.je = o; o = align_up(o + 4 * (T + 1), 256);
-  L.cstart = o; o = align_up(o + 4 * (T + 2), 256);
+  for (int q = 0; q < 2; ++q) {  // 0 = nested tiles, 1 = sorted tiles
+    L.jrec[q] = o; o = align_up(o + 16 * T, 256);
+    L.je[q] = o; o = align_up(o + 4 * (T + 1), 256);
+    L.cdesc[q] = o; o = align_up(o + 16 * (T + 2), 256);
+  }
   L.lrec = o; o = align_up(o + 16 * T, 256);
   L.lpre = o; o = align_up(o + 4 * (T + 1), 256);
-  L.partials = o; o = align_up(o + sizeof(u64) * kNV * (L.nblocks + 1), 256);
+  L.partials = o; o = align_up(o + sizeof(u64) * kNTot * (L.nblocks + 1), 256);
   L.total = o;
   return L;
 }
@@ -139,8 +163,11 @@ struct Ws {
   pbsm_header* hdr;
   double* bx;
   double* by;
-  u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *je, *cstart, *lpre;
-  uint4 *jrec, *lrec;   // {r_start, s_start, nR, nS}
+  u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *lpre;
+  u32* je[2];
+  uint4* cdesc[2];  // chunk c: {first tile j0, r_start, s_start, -}; [n_chunks] = ends
+  uint4* jrec[2];   // {r_start, s_start, nR, nS}
+  uint4* lrec;
   u64* partials;
   u64 tiles, nblocks;
 };
@@ -155,9 +182,11 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
   w.cnt_s = (u32*)(b + L.cnt_s);
   w.cur_r = (u32*)(b + L.cur_r);
   w.cur_s = (u32*)(b + L.cur_s);
-  w.jrec = (uint4*)(b + L.jrec);
-  w.je = (u32*)(b + L.je);
-  w.cstart = (u32*)(b + L.cstart);
+  for (int q = 0; q < 2; ++q) {
+    w.jrec[q] = (uint4*)(b + L.jrec[q]);
+    w.je[q] = (u32*)(b + L.je[q]);
+    w.cdesc[q] = (uint4*)(b + L.cdesc[q]);
+  }
   w.lrec = (uint4*)(b + L.lrec);
   w.lpre = (u32*)(b + L.lpre);
   w.partials = (u64*)(b + L.partials);
@@ -171,8 +200,20 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
 // axis_tile_index (geometry.py:87-106) / tile_of (_kernels.pyx:20-31):
 // floor(p*k) clamped to [0,k-1], then nudged against the materialised
 // boundaries b[i] = i/k so it agrees with boundary comparisons exactly.
+//
+// Fast path (no table access): f = fl(p*k) is within 2^-53*k < 7.3e-12 of
+// p*k for k <= 65535, and fl(i/k) within 1.2e-16 of i/k.  So when the
+// fractional part of f lies in (1e-9, 1-1e-9), p is at least ~1.5e-14 away
+// from both boundaries of division floor(f): the nudge loops would not move,
+// and floor(f) (< k, since f < k) is the exact answer.  Otherwise — p within
+// ~1e-9/k of a boundary, or p = 1.0 — the reference's loop runs on the table.
 __device__ __forceinline__ int tile_of(double p, int k, const double* __restrict__ b) {
-  long long i = (long long)__dmul_rn(p, (double)k);
+  const double f = __dmul_rn(p, (double)k);
+  const double fl = floor(f);
+  const double frac = f - fl;
+  long long i = (long long)fl;
+  if (frac > 1e-9 && frac < 1.0 - 1e-9 && i >= 0 && i < k) return (int)i;
+  i = (long long)f;
   if (!(i >= 0)) i = 0;
   if (i > k - 1) i = k - 1;
   while (i > 0 && p < __ldg(b + i)) --i;
@@ -267,7 +308,7 @@ __global__ void k_bounds(double* bx, int kx, double* by, int ky) {
 // kRectsPerThread rectangles in flight.  The same pass applies
 // RectBatch.validate (geometry.py:166-177): inverted or out-of-[0,1]
 // rectangles raise error bits the host turns into the reference's ValueError.
-__global__ void __launch_bounds__(256) k_count(const double* __restrict__ xl,
+__global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __restrict__ xl,
                                                const double* __restrict__ xu,
                                                const double* __restrict__ yl,
                                                const double* __restrict__ yu, i64 n,
@@ -285,10 +326,10 @@ __global__ void __launch_bounds__(256) k_count(const double* __restrict__ xl,
     for (int u = 0; u < kRectsPerThread; ++u) {
       const i64 i = base + u * stride;
       if (i < n) {
-        a[u] = __ldg(xl + i);
-        b[u] = __ldg(xu + i);
-        c[u] = __ldg(yl + i);
-        d[u] = __ldg(yu + i);
+        a[u] = __ldcs(xl + i);  // streamed once: evict-first, keep the counters in L2
+        b[u] = __ldcs(xu + i);
+        c[u] = __ldcs(yl + i);
+        d[u] = __ldcs(yu + i);
       }
     }
 #pragma unroll
@@ -311,12 +352,34 @@ __global__ void __launch_bounds__(256) k_count(const double* __restrict__ xl,
 }
 
 // ---------------------------------------------------------------- 1c scatter
+// one 64-byte record = two full 32-byte sectors (no read-modify-write), stored
+// as 256-bit writes with an L2 evict-first policy so the streaming record
+// writes do not push the cursor array out of L2
+__device__ __forceinline__ u64 l2_evict_first_policy() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void st256_hint(void* p, u64 a, u64 b, u64 c, u64 d, u64 pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "l"(a),
+               "l"(b), "l"(c), "l"(d), "l"(pol)
+               : "memory");
+}
+
+__device__ __forceinline__ void write_rec(Rec* r, u64 key, double xu, double yl, double yu,
+                                          i64 id, u64 pol) {
+  st256_hint(r, key, (u64)__double_as_longlong(xu), (u64)__double_as_longlong(yl),
+             (u64)__double_as_longlong(yu), pol);
+  st256_hint(&r->id, (u64)id, 0ull, 0ull, 0ull, pol);
+}
+
 // write_tiles (_kernels.pyx:61-98): copy each rectangle into every tile it
 // overlaps, labelled with its class there.  Only tiles where both inputs are
 // non-empty get a list (the others cannot produce a pair: build_task_queue
 // joins only those, engine.py:97); their cursors start at kSkip and the write
 // is skipped, but the cursor still advances so k_guard can check every tile.
-__global__ void __launch_bounds__(256) k_scatter(const i64* __restrict__ ids,
+__global__ void __launch_bounds__(256, PBSM_PART_MINB) k_scatter(const i64* __restrict__ ids,
                                                  const double* __restrict__ xl,
                                                  const double* __restrict__ xu,
                                                  const double* __restrict__ yl,
@@ -326,57 +389,78 @@ __global__ void __launch_bounds__(256) k_scatter(const i64* __restrict__ ids,
                                                  const double* __restrict__ by,
                                                  u32* __restrict__ cursor, Rec* __restrict__ out,
                                                  i64 capacity, pbsm_header* hdr) {
-  const i64 stride = (i64)gridDim.x * blockDim.x;
   u32 bad = 0;
-  for (i64 base = blockIdx.x * (i64)blockDim.x + threadIdx.x; base < n;
-       base += stride * kRectsPerThread) {
-    double a[kRectsPerThread], b[kRectsPerThread], c[kRectsPerThread], d[kRectsPerThread];
-    i64 id[kRectsPerThread];
-#pragma unroll
-    for (int u = 0; u < kRectsPerThread; ++u) {
-      const i64 i = base + u * stride;
-      if (i < n) {
-        a[u] = __ldg(xl + i);
-        b[u] = __ldg(xu + i);
-        c[u] = __ldg(yl + i);
-        d[u] = __ldg(yu + i);
-        id[u] = __ldg(ids + i);
+  const u64 pol = l2_evict_first_policy();
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const double a = __ldcs(xl + i), b = __ldcs(xu + i), c = __ldcs(yl + i), d = __ldcs(yu + i);
+    const i64 id = __ldcs(ids + i);
+    const int c0 = tile_of(a, kx, bx);
+    const int c1 = tile_of(b, kx, bx);
+    const int rr0 = tile_of(c, ky, by);
+    const int r0 = max(rr0, row_lo);
+    const int r1 = min(tile_of(d, ky, by), row_hi - 1);
+    if (r0 > r1) continue;  // entirely outside this strip
+    const u64 xk = xl_bits(a);
+    const int nc = c1 - c0 + 1, nr = r1 - r0 + 1;
+    if (nc * nr == 1) {  // one tile: most rectangles
+      const u32 p = atomicAdd(cursor + (size_t)(r0 - row_lo) * kx + c0, 1u);
+      if (p < kSkip) {
+        if ((i64)p < capacity) write_rec(out + p, xk | ((r0 != rr0) ? kYOut : 0ull), b, c, d, id, pol);
+        else bad |= PBSM_ERR_SCATTER_OVERFLOW;
       }
+      continue;
     }
+    if (nc <= 2 && nr <= 2) {
+      // 2 or 4 tiles: their cursor atomics back to back (no branches in
+      // between) so the latencies overlap, then the record writes
+      u32* t00 = cursor + (size_t)(r0 - row_lo) * kx + c0;
+      u32* t01 = nc == 2 ? t00 + 1 : t00 + kx;   // second tile: right, or above
+      u32 pos[4];
+      int rows[4], cols[4];
+      rows[0] = r0;
+      cols[0] = c0;
+      rows[1] = nc == 2 ? r0 : r0 + 1;
+      cols[1] = nc == 2 ? c0 + 1 : c0;
+      int ns = 2;
+      if (nc == 2 && nr == 2) {
+        ns = 4;
+        pos[0] = atomicAdd(t00, 1u);
+        pos[1] = atomicAdd(t00 + 1, 1u);
+        pos[2] = atomicAdd(t00 + kx, 1u);
+        pos[3] = atomicAdd(t00 + kx + 1, 1u);
+        rows[2] = rows[3] = r0 + 1;
+        cols[2] = c0;
+        cols[3] = c0 + 1;
+      } else {
+        pos[0] = atomicAdd(t00, 1u);
+        pos[1] = atomicAdd(t01, 1u);
+        pos[2] = pos[3] = kSkip;
+        rows[2] = rows[3] = cols[2] = cols[3] = 0;
+      }
 #pragma unroll
-    for (int u = 0; u < kRectsPerThread; ++u) {
-      const i64 i = base + u * stride;
-      if (i >= n) continue;
-      const int c0 = tile_of(a[u], kx, bx);
-      const int c1 = tile_of(b[u], kx, bx);
-      const int rr0 = tile_of(c[u], ky, by);
-      const int r0 = max(rr0, row_lo);
-      const int r1 = min(tile_of(d[u], ky, by), row_hi - 1);
-      const u64 xk = xl_bits(a[u]);
-      for (int row = r0; row <= r1; ++row) {
-        u32* rowp = cursor + (size_t)(row - row_lo) * kx;
-        const u64 ylab = (row != rr0) ? kYOut : 0ull;
-        for (int col = c0; col <= c1; ++col) {
-          const u32 pos = atomicAdd(rowp + col, 1u);
-          if (pos >= kSkip) continue;  // not a join tile
-          if ((i64)pos >= capacity) {
-            bad |= PBSM_ERR_SCATTER_OVERFLOW;
-            continue;
-          }
-          Half h;
-          h.xl_key = xk | ylab | ((col != c0) ? kXOut : 0ull);
-          h.xu = b[u];
-          h.yl = c[u];
-          h.yu = d[u];
-          Rec* r = out + pos;
-          *reinterpret_cast<Half*>(r) = h;
-          Half t;
-          t.xl_key = (u64)id[u];
-          t.xu = 0.0;
-          t.yl = 0.0;
-          t.yu = 0.0;
-          *reinterpret_cast<Half*>(&r->id) = t;
+      for (int q = 0; q < 4; ++q) {
+        if (q >= ns || pos[q] >= kSkip) continue;  // absent / not a join tile
+        if ((i64)pos[q] >= capacity) {
+          bad |= PBSM_ERR_SCATTER_OVERFLOW;
+          continue;
         }
+        const u64 key = xk | ((rows[q] != rr0) ? kYOut : 0ull) | ((cols[q] != c0) ? kXOut : 0ull);
+        write_rec(out + pos[q], key, b, c, d, id, pol);
+      }
+      continue;
+    }
+    for (int row = r0; row <= r1; ++row) {
+      u32* rowp = cursor + (size_t)(row - row_lo) * kx;
+      const u64 ylab = (row != rr0) ? kYOut : 0ull;
+      for (int col = c0; col <= c1; ++col) {
+        const u32 p = atomicAdd(rowp + col, 1u);
+        if (p >= kSkip) continue;  // not a join tile
+        if ((i64)p >= capacity) {
+          bad |= PBSM_ERR_SCATTER_OVERFLOW;
+          continue;
+        }
+        write_rec(out + p, xk | ylab | ((col != c0) ? kXOut : 0ull), b, c, d, id, pol);
       }
     }
   }
@@ -396,56 +480,77 @@ __global__ void k_guard(const u32* __restrict__ cur_r, const u32* __restrict__ e
 }
 
 // ---------------------------------------------------------------- 1b plan
-// Per tile t the plan scans nine lanes at once:
-//   0 |R_T|  1 |S_T|                         (A_R, A_S: PartitionedDataset totals)
-//   2 small-join flag  3 small-join entries  (→ join tile list + CTA chunks)
-//   4 large-join flag  5 large-join items    (→ large tile list)
-//   6 |R_T| 7 |S_T| of small join tiles   ┐ tile-list offsets (compute_segment_
-//   9 |R_T| 10 |S_T| of large join tiles  ┘ offsets, partition.py:151-164)
-//   8 |R_T|·|S_T| of join tiles              (upper bound on the pair count)
-// A join tile has both inputs non-empty (build_task_queue, engine.py:97).
-// Small join tiles take the front of each tile list in tile order, so a
-// chunk of consecutive small tiles is one contiguous range per input; large
-// tiles follow in a second region.
-__device__ __forceinline__ void tile_vals(u32 a, u32 b, u64 v[kNV]) {
-  const bool join = a != 0u && b != 0u;
-  const u32 w = a + b;
-  const bool small = join && w <= (u32)kLmax;
-  const bool large = join && !small;
+// Per tile t the plan scans fourteen lanes at once (one exclusive scan each):
+//   0 |R_T|  1 |S_T|                          all tiles (A_R, A_S totals)
+//   2..5   nested tiles: flag, entries, |R_T|, |S_T|
+//   6..9   sorted tiles: flag, entries, |R_T|, |S_T|
+//   10..13 large tiles:  flag, work items, |R_T|, |S_T|
+// A join tile has both inputs non-empty (build_task_queue, engine.py:97);
+// its strategy comes from the cost model in include/pbsm.h.  The |R_T| /
+// |S_T| lanes of the three strategies give the tile-list offsets
+// (compute_segment_offsets, partition.py:151-164): each input's list holds
+// the nested tiles, then the sorted tiles, then the large tiles, each region
+// in tile order — so a chunk of consecutive nested (or sorted) tiles is one
+// contiguous range per input, fetched by one TMA bulk copy.
+enum TileKind { kNone = 0, kNested = 1, kSorted = 2, kLarge = 3 };
+
+__device__ __forceinline__ int tile_kind(u32 a, u32 b, i64 nested_max) {
+  if (a == 0u || b == 0u) return kNone;
+  if (a + b > (u32)kLmax) return kLarge;
+  return (i64)((u64)a * (u64)b) <= nested_max ? kNested : kSorted;
+}
+
+__device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u64 v[kNV]) {
+  const int kind = tile_kind(a, b, nm);
   const u32 lead = a >= b ? a : b;
+#pragma unroll
+  for (int q = 0; q < kNV; ++q) v[q] = 0;
   v[0] = a;
   v[1] = b;
-  v[2] = small;
-  v[3] = small ? w : 0u;
-  v[4] = large;
-  v[5] = large ? (lead + kLargeLead - 1) / kLargeLead : 0u;
-  v[6] = small ? a : 0u;
-  v[7] = small ? b : 0u;
-  v[8] = join ? (u64)a * (u64)b : 0ull;
-  v[9] = large ? a : 0u;
-  v[10] = large ? b : 0u;
+  if (kind == kNested) {
+    v[2] = 1;
+    v[3] = a + b;
+    v[4] = a;
+    v[5] = b;
+  } else if (kind == kSorted) {
+    v[6] = 1;
+    v[7] = a + b;
+    v[8] = a;
+    v[9] = b;
+  } else if (kind == kLarge) {
+    v[10] = 1;
+    v[11] = (lead + kLargeLead - 1) / kLargeLead;
+    v[12] = a;
+    v[13] = b;
+  }
 }
 
 __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restrict__ cr,
                                                               const u32* __restrict__ cs,
-                                                              u64 T, u64* __restrict__ partials,
+                                                              u64 T, i64 nm,
+                                                              u64* __restrict__ partials,
                                                               pbsm_header* hdr) {
   __shared__ u64 sh[kPlanThreads / 32][kNV];
   __shared__ u32 shmax[kPlanThreads / 32];
+  __shared__ u64 shb[kPlanThreads / 32];
   u64 acc[kNV];
 #pragma unroll
   for (int q = 0; q < kNV; ++q) acc[q] = 0;
   u32 mx = 0;
+  u64 bound = 0;
   const u64 base = (u64)blockIdx.x * kPlanTile;
   for (int i = 0; i < kPlanPer; ++i) {
     const u64 t = base + (u64)i * kPlanThreads + threadIdx.x;
     if (t < T) {
       const u32 a = cr[t], b = cs[t];
       u64 v[kNV];
-      tile_vals(a, b, v);
+      tile_vals(a, b, nm, v);
 #pragma unroll
       for (int q = 0; q < kNV; ++q) acc[q] += v[q];
-      if (a && b) mx = max(mx, a + b);
+      if (a && b) {
+        mx = max(mx, a + b);
+        bound += (u64)a * (u64)b;
+      }
     }
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -457,25 +562,37 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
     if (lane == 0) sh[wid][q] = v;
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
-  if (lane == 0) shmax[wid] = mx;
+  for (int o = 16; o; o >>= 1) {
+    mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    bound += __shfl_down_sync(0xffffffffu, bound, o);
+  }
+  if (lane == 0) {
+    shmax[wid] = mx;
+    shb[wid] = bound;
+  }
   __syncthreads();
   if (threadIdx.x < kNV) {
     u64 s = 0;
     for (int w = 0; w < kPlanThreads / 32; ++w) s += sh[w][threadIdx.x];
-    partials[(u64)blockIdx.x * kNV + threadIdx.x] = s;
+    partials[(u64)blockIdx.x * kNTot + threadIdx.x] = s;
   }
   if (threadIdx.x == 0) {
     u32 m = 0;
-    for (int w = 0; w < kPlanThreads / 32; ++w) m = max(m, shmax[w]);
+    u64 bs = 0;
+    for (int w = 0; w < kPlanThreads / 32; ++w) {
+      m = max(m, shmax[w]);
+      bs += shb[w];
+    }
     atomicMax((unsigned long long*)&hdr->max_tile, (unsigned long long)m);
+    if (bs) atomicAdd((unsigned long long*)&hdr->pair_bound, (unsigned long long)bs);
   }
 }
 
 // single CTA: exclusive scan of the per-CTA partial sums, totals → header
+// and into the extra row nb of `partials` (read by k_plan_apply)
 __global__ void __launch_bounds__(1024) k_plan_partials(u64* __restrict__ partials, u64 nb,
-                                                        pbsm_header* hdr, u32* je, u32* lpre,
-                                                        u32* cstart) {
+                                                        pbsm_header* hdr, u32* je_n, u32* je_s,
+                                                        u32* lpre) {
   __shared__ u64 sh[33];
   u64 carry[kNV];
 #pragma unroll
@@ -484,40 +601,51 @@ __global__ void __launch_bounds__(1024) k_plan_partials(u64* __restrict__ partia
     const u64 i = base + threadIdx.x;
 #pragma unroll
     for (int q = 0; q < kNV; ++q) {
-      const u64 v = i < nb ? partials[i * kNV + q] : 0ull;
+      const u64 v = i < nb ? partials[i * kNTot + q] : 0ull;
       u64 tot;
       const u64 ex = block_excl_scan<1024>(v, &tot, sh);
-      if (i < nb) partials[i * kNV + q] = carry[q] + ex;
+      if (i < nb) partials[i * kNTot + q] = carry[q] + ex;
       carry[q] += tot;
     }
   }
   if (threadIdx.x == 0) {
+    for (int q = 0; q < kNV; ++q) partials[nb * kNTot + q] = carry[q];
     hdr->a_r = (i64)carry[0];
     hdr->a_s = (i64)carry[1];
-    hdr->n_join = (i64)carry[2];
-    hdr->w_join = (i64)carry[3];
-    hdr->n_large = (i64)carry[4];
-    hdr->n_items = (i64)carry[5];
-    hdr->list_r = (i64)(carry[6] + carry[9]);
-    hdr->list_s = (i64)(carry[7] + carry[10]);
-    partials[nb * kNV + 0] = carry[6];   // small-region sizes, read by k_plan_apply
-    partials[nb * kNV + 1] = carry[7];
-    hdr->pair_bound = (i64)carry[8];
-    hdr->n_chunks = 0;
+    hdr->n_nested = (i64)carry[2];
+    hdr->w_nested = (i64)carry[3];
+    hdr->n_sorted = (i64)carry[6];
+    hdr->w_sorted = (i64)carry[7];
+    hdr->n_large = (i64)carry[10];
+    hdr->n_items = (i64)carry[11];
+    const u64 lr = carry[4] + carry[8] + carry[12], ls = carry[5] + carry[9] + carry[13];
+    hdr->list_r = (i64)lr;
+    hdr->list_s = (i64)ls;
+    hdr->chunks_nested = 0;
+    hdr->chunks_sorted = 0;
     hdr->pairs = 0;
-    if (carry[0] >= kSkip || carry[1] >= kSkip || carry[3] >= kSkip || carry[5] >= kSkip ||
-        carry[6] + carry[9] >= kSkip || carry[7] + carry[10] >= kSkip)
+    if (carry[0] >= kSkip || carry[1] >= kSkip || lr >= kSkip || ls >= kSkip ||
+        carry[3] >= kSkip || carry[7] >= kSkip || carry[11] >= kSkip)
       hdr->error |= PBSM_ERR_TOTAL_RANGE;
-    je[carry[2]] = (u32)carry[3];      // sentinel: end of the last join tile
-    lpre[carry[4]] = (u32)carry[5];    // sentinel: total large work items
-    cstart[0] = 0;
+    je_n[carry[2]] = (u32)carry[3];     // sentinels: end of the last tile
+    je_s[carry[6]] = (u32)carry[7];
+    lpre[carry[10]] = (u32)carry[11];
   }
 }
 
-__global__ void __launch_bounds__(kPlanThreads) k_plan_apply(
-    u32* __restrict__ cr, u32* __restrict__ cs, u64 T, u64 nb, const u64* __restrict__ partials,
-    u32* __restrict__ cur_r, u32* __restrict__ cur_s, uint4* __restrict__ jrec,
-    u32* __restrict__ je, uint4* __restrict__ lrec, u32* __restrict__ lpre) {
+struct PlanOut {
+  u32 *cur_r, *cur_s;
+  uint4* jrec[2];
+  u32* je[2];
+  uint4* lrec;
+  u32* lpre;
+};
+
+__global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ cr,
+                                                             u32* __restrict__ cs, u64 T, u64 nb,
+                                                             i64 nm,
+                                                             const u64* __restrict__ partials,
+                                                             PlanOut P) {
   __shared__ u32 sa[kPlanTile];
   __shared__ u32 sb[kPlanTile];
   __shared__ u64 shs[33];
@@ -529,48 +657,62 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(
   }
   __syncthreads();
   u32 a[kPlanPer], b[kPlanPer];
-  u64 acc[kNV];
+  u64 pre[kNV];
 #pragma unroll
-  for (int q = 0; q < kNV; ++q) acc[q] = 0;
+  for (int q = 0; q < kNV; ++q) pre[q] = 0;
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     a[i] = sa[threadIdx.x * kPlanPer + i];
     b[i] = sb[threadIdx.x * kPlanPer + i];
     u64 v[kNV];
-    tile_vals(a[i], b[i], v);
+    tile_vals(a[i], b[i], nm, v);
 #pragma unroll
-    for (int q = 0; q < kNV; ++q) acc[q] += v[q];
+    for (int q = 0; q < kNV; ++q) pre[q] += v[q];
   }
-  u64 pre[kNV];
 #pragma unroll
   for (int q = 0; q < kNV; ++q) {
     u64 tot;
-    pre[q] = block_excl_scan<kPlanThreads>(acc[q], &tot, shs) +
-             partials[(u64)blockIdx.x * kNV + q];
+    pre[q] = block_excl_scan<kPlanThreads>(pre[q], &tot, shs) +
+             partials[(u64)blockIdx.x * kNTot + q];
   }
-  const u64 small_r = partials[nb * kNV + 0], small_s = partials[nb * kNV + 1];
+  // region bases: [nested | sorted | large] in each input's list
+  const u64* tot = partials + nb * kNTot;
+  const u64 rs_base = tot[4], ss_base = tot[5];
+  const u64 rl_base = tot[4] + tot[8], sl_base = tot[5] + tot[9];
   // (block_excl_scan ends with a barrier, so sa/sb may be overwritten now:
   // they receive the cursor starts; the expected cursor ends go back into
   // cnt[] for k_guard.)
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     const u64 t = base + (u64)threadIdx.x * kPlanPer + i;
-    u64 v[kNV];
-    tile_vals(a[i], b[i], v);
-    const u32 r0 = v[2] ? (u32)pre[6] : v[4] ? (u32)(small_r + pre[9]) : kSkip;
-    const u32 s0 = v[2] ? (u32)pre[7] : v[4] ? (u32)(small_s + pre[10]) : kSkip;
+    const int kind = tile_kind(a[i], b[i], nm);
+    u32 r0 = kSkip, s0 = kSkip;
+    if (kind == kNested) {
+      r0 = (u32)pre[4];
+      s0 = (u32)pre[5];
+    } else if (kind == kSorted) {
+      r0 = (u32)(rs_base + pre[8]);
+      s0 = (u32)(ss_base + pre[9]);
+    } else if (kind == kLarge) {
+      r0 = (u32)(rl_base + pre[12]);
+      s0 = (u32)(sl_base + pre[13]);
+    }
     sa[threadIdx.x * kPlanPer + i] = r0;
     sb[threadIdx.x * kPlanPer + i] = s0;
     if (t < T) {
-      if (v[2]) {
-        jrec[pre[2]] = make_uint4(r0, s0, a[i], b[i]);
-        je[pre[2]] = (u32)pre[3];
-      }
-      if (v[4]) {
-        lrec[pre[4]] = make_uint4(r0, s0, a[i], b[i]);
-        lpre[pre[4]] = (u32)pre[5];
+      if (kind == kNested) {
+        P.jrec[0][pre[2]] = make_uint4(r0, s0, a[i], b[i]);
+        P.je[0][pre[2]] = (u32)pre[3];
+      } else if (kind == kSorted) {
+        P.jrec[1][pre[6]] = make_uint4(r0, s0, a[i], b[i]);
+        P.je[1][pre[6]] = (u32)pre[7];
+      } else if (kind == kLarge) {
+        P.lrec[pre[10]] = make_uint4(r0, s0, a[i], b[i]);
+        P.lpre[pre[10]] = (u32)pre[11];
       }
     }
+    u64 v[kNV];
+    tile_vals(a[i], b[i], nm, v);
 #pragma unroll
     for (int q = 0; q < kNV; ++q) pre[q] += v[q];
   }
@@ -581,24 +723,32 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(
       const u32 r0 = sa[i], s0 = sb[i];
       cr[t] = r0 + cr[t];   // expected end of tile t's R cursor
       cs[t] = s0 + cs[t];
-      cur_r[t] = r0;
-      cur_s[t] = s0;
+      P.cur_r[t] = r0;
+      P.cur_s[t] = s0;
     }
   }
 }
 
-// chunk c = the join tiles whose exclusive entry prefix lies in [c*B, (c+1)*B);
-// a chunk holds < B + kLmax = kCap entries.
-__global__ void k_chunks(const u32* __restrict__ je, u32* __restrict__ cstart, pbsm_header* hdr) {
-  const i64 nj = hdr->n_join;
+// chunk c = the tiles (of one strategy) whose exclusive entry prefix lies in
+// [c*B, (c+1)*B); a chunk holds < B + kLmax = kCap entries.  Its descriptor
+// {first tile, R list start, S list start} plus the next one's give the
+// chunk's three contiguous ranges (tile records, R entries, S entries).
+__global__ void k_chunks(const u32* __restrict__ je, const uint4* __restrict__ jrec,
+                         uint4* __restrict__ cdesc, pbsm_header* hdr, int which) {
+  const i64 nj = which ? hdr->n_sorted : hdr->n_nested;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nj;
        j += (i64)gridDim.x * blockDim.x) {
     const i64 c = je[j] / kChunkB;
     const i64 cp = j == 0 ? -1 : (i64)(je[j - 1] / kChunkB);
-    for (i64 cc = cp + 1; cc <= c; ++cc) cstart[cc] = (u32)j;
+    if (cp < c) {
+      const uint4 r = jrec[j];
+      for (i64 cc = cp + 1; cc <= c; ++cc) cdesc[cc] = make_uint4((u32)j, r.x, r.y, 0u);
+    }
     if (j == nj - 1) {
-      cstart[c + 1] = (u32)nj;
-      hdr->n_chunks = c + 1;
+      const uint4 r = jrec[j];
+      cdesc[c + 1] = make_uint4((u32)nj, r.x + r.z, r.y + r.w, 0u);
+      if (which) hdr->chunks_sorted = c + 1;
+      else hdr->chunks_nested = c + 1;
     }
   }
 }
@@ -667,17 +817,18 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const u32* __restri
 
 // ---------------------------------------------------------------- 2-4 join
 struct JoinArgs {
-  const uint4* jrec;
-  const u32* cstart;
+  const uint4* jrec[2];    // [0] nested tiles, [1] sorted tiles
+  const uint4* cdesc[2];
   const uint4* lrec;
   const u32* lpre;
   const Rec* rl;
   const Rec* sl;
   u32* ticket;
-  u64* status;     // [n_units] decoupled look-back words (emit mode)
+  u64* status;     // [n_units] decoupled look-back words (ordered emit)
+  unsigned long long* total;  // running pair total (unordered emit / count)
+  int ordered;
   i64* pairs;      // (r_id, s_id) int64 pairs
   i64 capacity;    // pairs the buffer holds
-  i64 n_chunks;
   i64 n_units;
   pbsm_header* hdr;
 };
@@ -715,8 +866,9 @@ union JoinSmem {
 // Decoupled look-back (one thread): publish this unit's count, accumulate the
 // predecessors' published values until an inclusive prefix is found, publish
 // ours.  Units are handed out by an atomic ticket in launch order, so every
-// predecessor is resident or finished — the spin cannot deadlock.
-__device__ u64 lookback(u64* status, i64 unit, u64 count, pbsm_header* hdr) {
+// predecessor is resident or finished — the spin cannot deadlock (and is
+// bounded anyway, so a bug can never hang the GPU).
+__device__ u64 lookback_thread(u64* status, i64 unit, u64 count, pbsm_header* hdr) {
   cuda::atomic_ref<u64, cuda::thread_scope_device> me(status[unit]);
   if (unit == 0) {
     me.store(kFlagPre | count, cuda::memory_order_release);
@@ -726,12 +878,11 @@ __device__ u64 lookback(u64* status, i64 unit, u64 count, pbsm_header* hdr) {
   u64 excl = 0;
   i64 j = unit - 1;
   u64 spins = 0;
-  while (true) {
+  while (j >= 0) {
     cuda::atomic_ref<u64, cuda::thread_scope_device> st(status[j]);
     const u64 v = st.load(cuda::memory_order_acquire);
     const u64 flag = v & ~kValMask;
     if (flag == 0) {
-      // a predecessor that never publishes is a bug; never hang the GPU on it
       if (++spins > (1ull << 24)) {
         atomicOr(&hdr->error, PBSM_ERR_INTERNAL);
         break;
@@ -745,6 +896,76 @@ __device__ u64 lookback(u64* status, i64 unit, u64 count, pbsm_header* hdr) {
   }
   me.store(kFlagPre | (excl + count), cuda::memory_order_release);
   return excl;
+}
+
+// Output range of one work unit, after its count pass.  Default: one atomic
+// on the running pair total — no unit ever waits for another, and the pair
+// list is a permutation of the reference's, which is itself unordered
+// (engine.py:61-62; with m > 1 threads its order varies run to run).  With
+// A.ordered the decoupled look-back gives every unit the exclusive prefix
+// of the units before it, i.e. a deterministic chunk-major order.
+__device__ __forceinline__ u64 reserve(const JoinArgs& A, i64 unit, u64 total) {
+  if (!A.ordered) return atomicAdd(A.total, total);
+  const u64 b = lookback_thread(A.status, unit, total, A.hdr);
+  if (unit == A.n_units - 1) A.hdr->pairs = (i64)(b + total);
+  return b;
+}
+
+// ---- nested mini-joins (small tiles)
+// For a tile this small, testing all |R_T|·|S_T| pairs costs less than the
+// per-tile sort it would need: the larger side leads (one thread per lead
+// entry, so lanes stay busy on lopsided tiles), the smaller side is scanned.
+// A pair is kept iff the closed rectangles intersect (intersects,
+// geometry.py:59-61) and at least one entry is x-in and one is y-in — the
+// nine valid class combinations AA AB AC AD BA BC CA CB DA,
+// i.e. exactly the tile that passes Eq. 1 for the pair.
+__device__ __forceinline__ bool pair_ok(u64 ka, double axu, double ayl, double ayu, u64 kb,
+                                        double bxu, double byl, double byu) {
+  const double axl = key_x(ka), bxl = key_x(kb);
+  // label bits set = "out"; the pair needs one x-in and one y-in: (ka & kb)
+  // must have neither label bit set
+  return (axl <= bxu) & (bxl <= axu) & (ayl <= byu) & (byl <= ayu) &
+         (((ka & kb) & kLabelMask) == 0ull);
+}
+
+// Stage a chunk of consecutive tiles of one strategy: TMA bulk copies of its
+// R range and S range (contiguous, see k_plan_apply) into `recs`, plus the
+// tile table.  Returns false (and flags) if the chunk breaks a plan invariant.
+template <typename Smem>
+__device__ __forceinline__ void stage_chunk(Smem& S, const JoinArgs& A, int which, int c) {
+  const int tid = threadIdx.x;
+  const uint4* jrec = A.jrec[which];
+  const uint4 d0 = A.cdesc[which][c], d1 = A.cdesc[which][c + 1];
+  const u32 j0 = d0.x;
+  const int nt = (int)(d1.x - d0.x);
+  if (tid == 0) {
+    const int NR = (int)(d1.y - d0.y);
+    const int NS = (int)(d1.z - d0.z);
+    // a chunk never exceeds the staging buffer by construction (k_chunks);
+    // if it somehow did, flag it and contribute 0 pairs (no early return:
+    // the ordered mode's look-back chain must still be fed)
+    const bool fits = nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles;
+    if (!fits) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
+    S.nt = fits ? nt : 0;
+    S.NR = fits ? NR : 0;
+    S.NS = fits ? NS : 0;
+    if (fits) {
+      mbar_init(&S.bar, 1);
+      mbar_expect_tx(&S.bar, (u32)(NR + NS) * (u32)sizeof(Rec));
+      bulk_g2s(&S.recs[0], A.rl + d0.y, (u32)NR * (u32)sizeof(Rec), &S.bar);
+      bulk_g2s(&S.recs[NR], A.sl + d0.z, (u32)NS * (u32)sizeof(Rec), &S.bar);
+    }
+  }
+  __syncthreads();
+  // tile table, while the copies are in flight
+  const int NR = S.NR;
+  for (int lt = tid; lt < S.nt; lt += kJoinThreads) {
+    const uint4 r = jrec[j0 + lt];
+    S.tR0[lt] = (u16)(r.x - d0.y);
+    S.tS0[lt] = (u16)(NR + (int)(r.y - d0.z));
+    S.tNR[lt] = (u16)r.z;
+    S.tNS[lt] = (u16)r.w;
+  }
 }
 
 // One leader element of the forward scan (Alg. 1, _kernels.pyx:231-293,
@@ -808,46 +1029,14 @@ __device__ __forceinline__ u32 sweep_one(const ChunkSmem& S, int p, i64* out) {
 }
 
 template <bool EMIT>
-__device__ void join_chunk(ChunkSmem& S, const JoinArgs& A, int c) {
+__device__ void join_sorted(ChunkSmem& S, const JoinArgs& A, i64 unit, int c) {
   const int tid = threadIdx.x;
-  const u32 j0 = A.cstart[c], j1 = A.cstart[c + 1];
-  const int nt = (int)(j1 - j0);
-  if (tid == 0) {
-    const uint4 first = A.jrec[j0], last = A.jrec[j1 - 1];
-    const int NR = (int)(last.x + last.z - first.x);
-    const int NS = (int)(last.y + last.w - first.y);
-    // a chunk never exceeds the staging buffer by construction (k_chunks);
-    // if it somehow did, flag it and contribute 0 pairs (the look-back chain
-    // must still be fed, so no early return)
-    const bool fits = NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles;
-    if (!fits) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
-    S.nt = fits ? nt : 0;
-    S.NR = fits ? NR : 0;
-    S.NS = fits ? NS : 0;
-    if (fits) {
-      // TMA: two bulk copies (the chunk's R and S ranges are contiguous
-      // because small join tiles get consecutive list offsets in tile order)
-      mbar_init(&S.bar, 1);
-      mbar_expect_tx(&S.bar, (u32)(NR + NS) * (u32)sizeof(Rec));
-      bulk_g2s(&S.recs[0], A.rl + first.x, (u32)NR * (u32)sizeof(Rec), &S.bar);
-      bulk_g2s(&S.recs[NR], A.sl + first.y, (u32)NS * (u32)sizeof(Rec), &S.bar);
-    }
-  }
-  __syncthreads();
+  stage_chunk(S, A, 1, c);
   const int NR = S.NR, N = S.NR + S.NS;
-  // tile table + position → tile map, while the copies are in flight
-  {
-    const uint4 first = A.jrec[j0];
-    for (int lt = tid; lt < S.nt; lt += kJoinThreads) {
-      const uint4 r = A.jrec[j0 + lt];
-      const int r0 = (int)(r.x - first.x), s0 = NR + (int)(r.y - first.y);
-      S.tR0[lt] = (u16)r0;
-      S.tS0[lt] = (u16)s0;
-      S.tNR[lt] = (u16)r.z;
-      S.tNS[lt] = (u16)r.w;
-      for (int e = 0; e < (int)r.z; ++e) S.seg[r0 + e] = (u16)lt;
-      for (int e = 0; e < (int)r.w; ++e) S.seg[s0 + e] = (u16)lt;
-    }
+  // position → tile map (the table is complete for this thread's tiles)
+  for (int lt = tid; lt < S.nt; lt += kJoinThreads) {
+    for (int e = 0; e < (int)S.tNR[lt]; ++e) S.seg[S.tR0[lt] + e] = (u16)lt;
+    for (int e = 0; e < (int)S.tNS[lt]; ++e) S.seg[S.tS0[lt] + e] = (u16)lt;
   }
   if (N > 0) mbar_wait(&S.bar, 0);
   for (int e = tid; e < N; e += kJoinThreads) S.key[e] = S.recs[e].xl_key;
@@ -893,14 +1082,10 @@ __device__ void join_chunk(ChunkSmem& S, const JoinArgs& A, int c) {
   u64 total;
   const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
   if (!EMIT) {
-    if (tid == 0 && total) atomicAdd((unsigned long long*)&A.hdr->pairs, total);
+    if (tid == 0 && total) atomicAdd(A.total, total);
     return;
   }
-  if (tid == 0) {
-    const u64 b = lookback(A.status, c, total, A.hdr);
-    S.base = b;
-    if (c == A.n_units - 1) A.hdr->pairs = (i64)(b + total);
-  }
+  if (tid == 0) S.base = reserve(A, unit, total);
   __syncthreads();
   const i64 start = (i64)(S.base + excl);
   if (start + (i64)cnt > A.capacity) {
@@ -940,9 +1125,8 @@ __device__ __forceinline__ u32 large_pass(const LargeSmem& S, int n, bool have, 
 }
 
 template <bool EMIT>
-__device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit) {
+__device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) {
   const int tid = threadIdx.x;
-  const i64 item = unit - A.n_chunks;
   // item → large tile (binary search over the work-item prefix)
   int lo = 0, hi = (int)A.hdr->n_large;
   while (lo < hi) {
@@ -992,14 +1176,10 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit) {
       u64 total;
       const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
       if (!EMIT) {
-        if (tid == 0 && total) atomicAdd((unsigned long long*)&A.hdr->pairs, total);
+        if (tid == 0 && total) atomicAdd(A.total, total);
         return;
       }
-      if (tid == 0) {
-        const u64 b = lookback(A.status, unit, total, A.hdr);
-        S.base = b;
-        if (unit == A.n_units - 1) A.hdr->pairs = (i64)(b + total);
-      }
+      if (tid == 0) S.base = reserve(A, unit, total);
       __syncthreads();
       const i64 start = (i64)(S.base + excl);
       ok = start + (i64)cnt <= A.capacity;
@@ -1009,16 +1189,202 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit) {
   }
 }
 
+// ---- nested mini-joins: one CTA per chunk, pairs flattened over lanes
+// Every (r, s) pair of every tile in the chunk gets an index (tile-major,
+// then r, then s); thread q of a warp-step tests pair q.  All lanes stay busy
+// however small and lopsided the tiles are, and the hits of a warp-step are
+// compacted with a ballot + popcount into consecutive output slots (one
+// coalesced 16-byte store per hit).
+struct NestedSmem {
+  Rec recs[kCap];                // TMA: the chunk's R range, then its S range
+  uint4 jr[kMaxTiles];           // TMA: the chunk's tile records
+  u64 f[4][kCap + kPad];         // SoA copy of the MBR words (padded rows)
+  u32 tP[kMaxTiles + 1];         // pair-index prefix per tile
+  u16 tR0[kMaxTiles], tS0[kMaxTiles], tNS[kMaxTiles];
+  float tInvS[kMaxTiles];        // 1 / |S_T|
+  u64 wtot[kJoinThreads / 32 + 1];
+  u64 scan[kJoinThreads / 32 + 1];
+  u64 bar;
+  u64 base;
+  int nt, NR, NS;
+};
+
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// first tile of warp-step q0: binary search over the pair prefix (the same
+// addresses in every lane: broadcast reads)
+__device__ __forceinline__ int nested_tile_of(const NestedSmem& S, int nt, u32 q0) {
+  int lo = 0, hi = nt;  // last lt with tP[lt] <= q0
+  while (hi - lo > 1) {
+    const int m = (lo + hi) >> 1;
+    if (S.tP[m] <= q0) lo = m; else hi = m;
+  }
+  return lo;
+}
+
+// pair q of the chunk → (position of r, position of s), or false past the end;
+// lt enters as the tile of the warp-step's first pair
+__device__ __forceinline__ bool nested_pair(const NestedSmem& S, int nt, u32 q, int lt, int& pr,
+                                            int& ps) {
+  if (q >= S.tP[nt]) return false;
+  while (q >= S.tP[lt + 1]) ++lt;  // within a warp-step: a few tiles at most
+  const u32 local = q - S.tP[lt];
+  const u32 nS = S.tNS[lt];
+  // local / nS: local < 2^16 and |local/nS - integer| >= 0.5/nS, so the
+  // float estimate of (local + 0.5) / nS truncates to the exact quotient
+  const u32 r = (u32)__float2int_rz(((float)local + 0.5f) * S.tInvS[lt]);
+  pr = S.tR0[lt] + (int)r;
+  ps = S.tS0[lt] + (int)(local - r * nS);
+  return true;
+}
+
+__device__ __forceinline__ bool nested_hit(const NestedSmem& S, int pr, int ps) {
+  const double rxu = __longlong_as_double((long long)S.f[1][pr]);
+  const double ryl = __longlong_as_double((long long)S.f[2][pr]);
+  const double ryu = __longlong_as_double((long long)S.f[3][pr]);
+  const double sxu = __longlong_as_double((long long)S.f[1][ps]);
+  const double syl = __longlong_as_double((long long)S.f[2][ps]);
+  const double syu = __longlong_as_double((long long)S.f[3][ps]);
+  return pair_ok(S.f[0][pr], rxu, ryl, ryu, S.f[0][ps], sxu, syl, syu);
+}
+
+template <bool EMIT>
+__global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64 n_chunks) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
+  __shared__ int s_unit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (A.ordered) {  // the look-back needs units handed out in launch order
+    if (tid == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
+    __syncthreads();
+  }
+  const i64 c = A.ordered ? s_unit : blockIdx.x;
+  if (tid == 0) {
+    const uint4 d0 = A.cdesc[0][c], d1 = A.cdesc[0][c + 1];
+    int nt = (int)(d1.x - d0.x), NR = (int)(d1.y - d0.y), NS = (int)(d1.z - d0.z);
+    const bool fits = nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles;
+    if (!fits) {  // never by construction; contribute 0 pairs, keep the chain fed
+      atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
+      nt = NR = NS = 0;
+    }
+    S.nt = nt;
+    S.NR = NR;
+    S.NS = NS;
+    mbar_init(&S.bar, 1);
+    if (fits) {
+      mbar_expect_tx(&S.bar, (u32)nt * 16u + (u32)(NR + NS) * (u32)sizeof(Rec));
+      bulk_g2s(&S.jr[0], A.jrec[0] + d0.x, (u32)nt * 16u, &S.bar);
+      bulk_g2s(&S.recs[0], A.rl + d0.y, (u32)NR * (u32)sizeof(Rec), &S.bar);
+      bulk_g2s(&S.recs[NR], A.sl + d0.z, (u32)NS * (u32)sizeof(Rec), &S.bar);
+    } else {
+      mbar_arrive(&S.bar);
+    }
+  }
+  __syncthreads();
+  const int nt = S.nt, NR = S.NR, N = S.NR + S.NS;
+  mbar_wait(&S.bar, 0);
+  // tile table + pair prefix (nt <= kMaxTiles <= 2 * kJoinThreads)
+  static_assert(kMaxTiles <= 2 * kJoinThreads, "two tiles per thread");
+  u32 np = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int lt = 2 * tid + h;
+    if (lt < nt) {
+      const uint4 r = S.jr[lt], r0 = S.jr[0];
+      S.tR0[lt] = (u16)(r.x - r0.x);
+      S.tS0[lt] = (u16)(NR + (int)(r.y - r0.y));
+      S.tNS[lt] = (u16)r.w;
+      S.tInvS[lt] = 1.0f / (float)r.w;
+      np += r.z * r.w;
+    }
+  }
+  u64 tot;
+  u32 pre = (u32)block_excl_scan<kJoinThreads>((u64)np, &tot, S.scan);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int lt = 2 * tid + h;
+    if (lt < nt) {
+      S.tP[lt] = pre;
+      pre += S.jr[lt].z * S.jr[lt].w;
+    }
+  }
+  if (tid == 0) S.tP[nt] = (u32)tot;
+  // SoA transpose, conflict-free: a warp reads 4 whole records per step
+  {
+    const u64* words = reinterpret_cast<const u64*>(S.recs);
+    for (int r0 = warp * 4; r0 < N; r0 += 4 * (kJoinThreads / 32)) {
+      const int r = r0 + (lane >> 3), word = lane & 7;
+      if (r < N && word < 4) S.f[word][r] = words[r * 8 + word];
+    }
+  }
+  __syncthreads();
+  const u32 NP = (u32)tot;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // pass 1: count
+  u32 wcnt = 0;
+  for (u32 q0 = (u32)warp * 32u; q0 < NP; q0 += kJoinThreads) {
+    int pr, ps;
+    const int lt = nested_tile_of(S, nt, q0);
+    const bool hit = nested_pair(S, nt, q0 + lane, lt, pr, ps) && nested_hit(S, pr, ps);
+    wcnt += __popc(__ballot_sync(0xffffffffu, hit));
+  }
+  if (lane == 0) S.wtot[warp] = wcnt;
+  __syncthreads();
+  if (tid == 0) {
+    u64 t = 0;
+    for (int w = 0; w < kJoinThreads / 32; ++w) {
+      const u64 v = S.wtot[w];
+      S.wtot[w] = t;
+      t += v;
+    }
+    if (!EMIT) {
+      if (t) atomicAdd(A.total, t);
+    } else {
+      S.base = reserve(A, c, t);
+      if ((i64)(S.base + t) > A.capacity) {
+        if (t) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
+        S.base = ~0ull;  // nothing written
+      }
+    }
+  }
+  if (!EMIT) return;
+  __syncthreads();
+  if (S.base == ~0ull) return;
+  // pass 2: emit, ballot-compacted
+  i64* out = A.pairs + 2 * (i64)(S.base + S.wtot[warp]);
+  for (u32 q0 = (u32)warp * 32u; q0 < NP; q0 += kJoinThreads) {
+    int pr = 0, ps = 0;
+    const int lt = nested_tile_of(S, nt, q0);
+    const bool hit = nested_pair(S, nt, q0 + lane, lt, pr, ps) && nested_hit(S, pr, ps);
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+      const i64 o = __popc(m & lt_mask);
+      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(S.recs[pr].id, S.recs[ps].id);
+    }
+    out += 2 * (i64)__popc(m);
+  }
+}
+
 template <bool EMIT>
 __global__ void __launch_bounds__(kJoinThreads, 2) k_join(JoinArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   JoinSmem& U = *reinterpret_cast<JoinSmem*>(smem_raw);
+  // ordered mode hands out units by ticket (launch order, for the look-back);
+  // otherwise any CTA may take any unit
   __shared__ int s_unit;
-  if (threadIdx.x == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
-  __syncthreads();
-  const int unit = s_unit;
-  if (unit < A.n_chunks) join_chunk<EMIT>(U.c, A, unit);
-  else join_large<EMIT>(U.l, A, unit);
+  if (A.ordered) {
+    if (threadIdx.x == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
+    __syncthreads();
+  }
+  const int local = A.ordered ? s_unit : (int)blockIdx.x;
+  // units of this launch: [sorted chunks | large items]; the look-back ids
+  // continue after the nested chunks (k_join_nested)
+  const i64 cn = A.hdr->chunks_nested, cs = A.hdr->chunks_sorted;
+  const i64 unit = cn + local;
+  if (local < cs) join_sorted<EMIT>(U.c, A, unit, local);
+  else join_large<EMIT>(U.l, A, unit, local - cs);
 }
 
 // ---------------------------------------------------------------- ε refinement
@@ -1112,28 +1478,37 @@ int set_smem_attrs() {
   e = cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(JoinSmem));
   if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(k_join_nested<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(NestedSmem));
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(k_join_nested<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(NestedSmem));
+  if (e != cudaSuccess) return (int)e;
   done = true;
   return 0;
 }
 
-int launch_join(bool emit, void* ws, int kx, int ky, int row_lo, int row_hi,
-                const pbsm_entry* r_list, const pbsm_entry* s_list, i64 n_chunks, i64 n_items,
+int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, int row_hi,
+                const pbsm_entry* r_list, const pbsm_entry* s_list, const pbsm_header* plan,
                 void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s) {
   int rc = set_smem_attrs();
   if (rc) return rc;
   const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
   Ws w = ws_bind(ws, L);
-  const i64 n_units = n_chunks + n_items;
+  const i64 cn = plan->chunks_nested, rest = plan->chunks_sorted + plan->n_items;
+  const i64 n_units = cn + rest;
   // write guard first (reads the cursors the scatter left behind)
   const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
                                                                 (i64)num_sms() * 8));
   k_guard<<<gb, 256, 0, s>>>(w.cur_r, w.cnt_r, w.cur_s, w.cnt_s, L.tiles, w.hdr);
   cudaMemsetAsync(&w.hdr->pairs, 0, sizeof(int64_t), s);
   if (n_units == 0) return launch_status();
-  cudaMemsetAsync(scratch, 0, join_scratch(n_units), s);
+  if (ordered) cudaMemsetAsync(scratch, 0, join_scratch(n_units), s);
   JoinArgs A;
-  A.jrec = w.jrec;
-  A.cstart = w.cstart;
+  for (int q = 0; q < 2; ++q) {
+    A.jrec[q] = w.jrec[q];
+    A.cdesc[q] = w.cdesc[q];
+  }
   A.lrec = w.lrec;
   A.lpre = w.lpre;
   A.rl = reinterpret_cast<const Rec*>(r_list);
@@ -1142,13 +1517,25 @@ int launch_join(bool emit, void* ws, int kx, int ky, int row_lo, int row_hi,
   A.status = (u64*)((char*)scratch + 256);
   A.pairs = (i64*)pairs;
   A.capacity = capacity;
-  A.n_chunks = n_chunks;
   A.n_units = n_units;
   A.hdr = w.hdr;
-  if (emit)
-    k_join<true><<<(unsigned)n_units, kJoinThreads, sizeof(JoinSmem), s>>>(A);
-  else
-    k_join<false><<<(unsigned)n_units, kJoinThreads, sizeof(JoinSmem), s>>>(A);
+  A.total = (unsigned long long*)&w.hdr->pairs;
+  A.ordered = ordered ? 1 : 0;
+  if (cn > 0) {
+    if (emit)
+      k_join_nested<true><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+    else
+      k_join_nested<false><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+  }
+  if (rest > 0) {
+    // the sorted/large launch keeps its own ticket (the look-back ids follow
+    // the nested chunks', whose kernel has finished by then)
+    if (ordered) cudaMemsetAsync(scratch, 0, 4, s);
+    if (emit)
+      k_join<true><<<(unsigned)rest, kJoinThreads, sizeof(JoinSmem), s>>>(A);
+    else
+      k_join<false><<<(unsigned)rest, kJoinThreads, sizeof(JoinSmem), s>>>(A);
+  }
   return launch_status();
 }
 
@@ -1159,10 +1546,13 @@ extern "C" {
 
 int32_t pbsm_abi_version(void) { return PBSM_ABI_VERSION; }
 
+#define PBSM_STR2(x) #x
+#define PBSM_STR(x) PBSM_STR2(x)
 const char* pbsm_build_info(void) {
-  return "pbsm sm_100a v2: count+validate / plan / scatter(64B records, join tiles only) / "
-         "guard / fused TMA-staged sort+sweep join with decoupled look-back; "
-         "kCap=1024 kLmax=384";
+  return "pbsm sm_100a v3: count+validate / plan / scatter (64B records, join tiles only) / "
+         "guard / TMA-staged mini-joins (nested | sort+forward-scan | large) with count->emit; "
+         "B=" PBSM_STR(PBSM_CHUNK_B) " Lmax=" PBSM_STR(PBSM_LMAX) " nested<=" PBSM_STR(
+             PBSM_NESTED_MAX) " rpt=" PBSM_STR(PBSM_RPT);
 }
 
 int64_t pbsm_workspace_bytes(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi) {
@@ -1200,18 +1590,30 @@ int pbsm_count(const double* xl, const double* xu, const double* yl, const doubl
   return launch_status();
 }
 
-int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi, void* stream) {
+int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+              int64_t nested_max, void* stream) {
   if (!ws || !grid_ok(kx, ky, row_lo, row_hi)) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
   cudaStream_t s = as_stream(stream);
-  k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles,
+  const i64 nm = nested_max < 0 ? (i64)kNestedMax : (i64)nested_max;
+  k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles, nm,
                                                               w.partials, w.hdr);
-  k_plan_partials<<<1, 1024, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je, w.lpre, w.cstart);
+  k_plan_partials<<<1, 1024, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je[0], w.je[1], w.lpre);
+  PlanOut P;
+  P.cur_r = w.cur_r;
+  P.cur_s = w.cur_s;
+  for (int q = 0; q < 2; ++q) {
+    P.jrec[q] = w.jrec[q];
+    P.je[q] = w.je[q];
+  }
+  P.lrec = w.lrec;
+  P.lpre = w.lpre;
   k_plan_apply<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles,
-                                                             w.nblocks, w.partials, w.cur_r, w.cur_s,
-                                                             w.jrec, w.je, w.lrec, w.lpre);
-  const i64 blocks = std::min<i64>((i64)((w.tiles + 255) / 256), (i64)num_sms() * 8);
-  k_chunks<<<(unsigned)std::max<i64>(blocks, 1), 256, 0, s>>>(w.je, w.cstart, w.hdr);
+                                                             w.nblocks, nm, w.partials, P);
+  const unsigned blocks =
+      (unsigned)std::max<i64>(1, std::min<i64>((i64)((w.tiles + 255) / 256), (i64)num_sms() * 8));
+  for (int q = 0; q < 2; ++q)
+    k_chunks<<<blocks, 256, 0, s>>>(w.je[q], w.jrec[q], w.cdesc[q], w.hdr, q);
   return launch_status();
 }
 
@@ -1242,28 +1644,27 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu, const d
   return launch_status();
 }
 
-int64_t pbsm_join_scratch_bytes(int64_t n_chunks, int64_t n_items) {
-  if (n_chunks < 0 || n_items < 0) return PBSM_E_ARG;
-  return (int64_t)join_scratch(n_chunks + n_items);
+int64_t pbsm_join_scratch_bytes(int64_t n_units) {
+  if (n_units < 0) return PBSM_E_ARG;
+  return (int64_t)join_scratch(n_units);
 }
 
 int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-                    const pbsm_entry* r_list, const pbsm_entry* s_list, int64_t n_chunks,
-                    int64_t n_items, void* scratch, void* stream) {
-  if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || n_chunks < 0 || n_items < 0)
-    return PBSM_E_ARG;
-  return launch_join(false, ws, kx, ky, row_lo, row_hi, r_list, s_list, n_chunks, n_items,
-                     scratch, nullptr, 0, as_stream(stream));
+                    const pbsm_entry* r_list, const pbsm_entry* s_list,
+                    const pbsm_header* plan, void* scratch, void* stream) {
+  if (!ws || !scratch || !plan || !grid_ok(kx, ky, row_lo, row_hi)) return PBSM_E_ARG;
+  return launch_join(false, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan, scratch,
+                     nullptr, 0, as_stream(stream));
 }
 
 int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-                   const pbsm_entry* r_list, const pbsm_entry* s_list, int64_t n_chunks,
-                   int64_t n_items, void* scratch, int64_t* pairs, int64_t capacity,
-                   void* stream) {
-  if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || n_chunks < 0 || n_items < 0 ||
-      capacity < 0 || (capacity > 0 && !pairs))
+                   const pbsm_entry* r_list, const pbsm_entry* s_list,
+                   const pbsm_header* plan, void* scratch, int64_t* pairs, int64_t capacity,
+                   int32_t ordered, void* stream) {
+  if (!ws || !scratch || !plan || !grid_ok(kx, ky, row_lo, row_hi) || capacity < 0 ||
+      (capacity > 0 && !pairs))
     return PBSM_E_ARG;
-  return launch_join(true, ws, kx, ky, row_lo, row_hi, r_list, s_list, n_chunks, n_items,
+  return launch_join(true, ordered != 0, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan,
                      scratch, pairs, capacity, as_stream(stream));
 }
 

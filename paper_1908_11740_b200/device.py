@@ -142,11 +142,14 @@ def pair_capacity(h) -> int:
 
 def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool = True,
              row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
-             keep_counts: bool = False, probe: PhaseProbe | None = None) -> DeviceJoinResult:
+             keep_counts: bool = False, probe: PhaseProbe | None = None,
+             ordered: bool = False, nested_max: int = -1) -> DeviceJoinResult:
     """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
 
     ``probe`` (optional) gets an event after each library call, named after
     the phase that call ran: init, count, plan, header, scatter, join, header2.
+    ``nested_max`` overrides the mini-join cost-model threshold (pbsm_plan);
+    ``ordered`` selects the deterministic look-back output order.
     """
     mark = probe.mark if probe is not None else (lambda name: None)
     lib = _native.load()
@@ -173,7 +176,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     counts = None
     if keep_counts:  # per-tile counts, before the plan turns them into cursor ends
         counts = tuple(v.clone() for v in _tile_count_views(ws, kx, ky, kx * (row_hi - row_lo)))
-    _native.check(lib.pbsm_plan(wsp, *grid, stream), "pbsm_plan")
+    _native.check(lib.pbsm_plan(wsp, *grid, nested_max, stream), "pbsm_plan")
     mark("plan")
     h = _read_header(lib, ws, stream)
     mark("header")
@@ -189,15 +192,14 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     if ev:
         ev[1].record()
 
-    n_chunks, n_items = h.n_chunks, h.n_items
-    scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(n_chunks, n_items)),
-                          dtype=torch.uint8, device=device)
+    n_units = h.n_units
+    scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(n_units)), dtype=torch.uint8,
+                          device=device)
     rl, sl = lists
     pairs = None
     if not collect:
-        _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), n_chunks,
-                                          n_items, scratch.data_ptr(), stream),
-                      "pbsm_join_count")
+        _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), C.byref(h),
+                                          scratch.data_ptr(), stream), "pbsm_join_count")
         mark("join")
         h2 = _read_header(lib, ws, stream)
         mark("header2")
@@ -207,8 +209,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         while True:
             pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
             _native.check(lib.pbsm_join_emit(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
-                                             n_chunks, n_items, scratch.data_ptr(),
-                                             pairs.data_ptr(), cap, stream), "pbsm_join_emit")
+                                             C.byref(h), scratch.data_ptr(), pairs.data_ptr(),
+                                             cap, int(ordered), stream), "pbsm_join_emit")
             mark("join")
             h2 = _read_header(lib, ws, stream, allow=_native.ERR_PAIR_OVERFLOW)
             mark("header2")
