@@ -61,15 +61,15 @@ namespace {
 constexpr int kPlanThreads = 256;
 constexpr int kPlanPer = 4;                          // tiles per thread
 constexpr int kPlanTile = kPlanThreads * kPlanPer;   // 1024 tiles per CTA
-constexpr int kNV = 14;                              // plan scan lanes (see tile_vals)
-constexpr int kNTot = kNV + 2;                       // + extra totals slots
+constexpr int kNV = 12;                              // plan scan lanes (see tile_vals)
+constexpr int kNTot = kNV;                           // partials row stride
 
 constexpr int kJoinThreads = 256;
 #ifndef PBSM_CHUNK_B
-#define PBSM_CHUNK_B 320
+#define PBSM_CHUNK_B 256
 #endif
 #ifndef PBSM_LMAX
-#define PBSM_LMAX 192
+#define PBSM_LMAX 128
 #endif
 #ifndef PBSM_NESTED_MAX
 #define PBSM_NESTED_MAX 1024
@@ -202,18 +202,23 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
 // boundaries b[i] = i/k so it agrees with boundary comparisons exactly.
 //
 // Fast path (no table access): f = fl(p*k) is within 2^-53*k < 7.3e-12 of
-// p*k for k <= 65535, and fl(i/k) within 1.2e-16 of i/k.  So when the
-// fractional part of f lies in (1e-9, 1-1e-9), p is at least ~1.5e-14 away
-// from both boundaries of division floor(f): the nudge loops would not move,
-// and floor(f) (< k, since f < k) is the exact answer.  Otherwise — p within
-// ~1e-9/k of a boundary, or p = 1.0 — the reference's loop runs on the table.
+// p*k for k <= 65535, and fl(i/k) within 1.2e-16 of i/k.  So when f is more
+// than 1e-9 away from the nearest integer, p is at least ~1.5e-14 away from
+// both boundaries of division floor(f): the nudge loops would not move, and
+// floor(f) is the exact answer.  Otherwise — p within ~1e-9/k of a boundary,
+// or p = 1.0 — the reference's loop runs on the table.
 __device__ __forceinline__ int tile_of(double p, int k, const double* __restrict__ b) {
   const double f = __dmul_rn(p, (double)k);
-  const double fl = floor(f);
-  const double frac = f - fl;
-  long long i = (long long)fl;
-  if (frac > 1e-9 && frac < 1.0 - 1e-9 && i >= 0 && i < k) return (int)i;
-  i = (long long)f;
+  // round f to the nearest integer without a conversion instruction: adding
+  // 1.5*2^52 leaves round(f) in the low mantissa bits (|f| < 2^31 here)
+  const double kMagic = 6755399441055744.0;
+  const double t = __dadd_rn(f, kMagic);
+  const double r = __dsub_rn(t, kMagic);
+  const double dlt = __dsub_rn(f, r);  // f - round(f), exact
+  const int ri = (int)__double2loint(t);
+  const int i0 = ri - (dlt < 0.0 ? 1 : 0);  // floor(f)
+  if (fabs(dlt) > 1e-9 && i0 >= 0 && i0 < k) return i0;
+  long long i = (long long)f;
   if (!(i >= 0)) i = 0;
   if (i > k - 1) i = k - 1;
   while (i > 0 && p < __ldg(b + i)) --i;
@@ -263,6 +268,35 @@ __device__ __forceinline__ u64 block_excl_scan(u64 v, u64* total, u64* sh /* >= 
   return r;
 }
 
+
+// Block-wide exclusive scan of NV u64 lanes at once (two barriers for all
+// lanes).  v[] is replaced by the exclusive prefixes, tot[] gets the sums.
+template <int NT, int NV, typename T>
+__device__ __forceinline__ void block_excl_scan_multi(T v[NV], T tot[NV],
+                                                      T (*sh)[NV] /* [NT/32] */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T inc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    inc[q] = warp_incl_scan<T>(v[q]);
+    if (lane == 31) sh[wid][q] = inc[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    T before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+      const T x = sh[w][q];
+      before += w < wid ? x : (T)0;
+      all += x;
+    }
+    v[q] = inc[q] - v[q] + before;
+    tot[q] = all;
+  }
+  __syncthreads();
+}
+
 // ---- TMA bulk copy (cp.async.bulk) + mbarrier, one elected thread issues
 __device__ __forceinline__ u32 smem_u32(const void* p) {
   return (u32)__cvta_generic_to_shared(p);
@@ -304,8 +338,8 @@ __global__ void k_bounds(double* bx, int kx, double* by, int ky) {
 }
 
 // ---------------------------------------------------------------- 1a count
-// count_tiles (_kernels.pyx:34-58) for all rectangles; each thread keeps
-// kRectsPerThread rectangles in flight.  The same pass applies
+// count_tiles (_kernels.pyx:34-58) for all rectangles, one per thread and
+// loop step with the next one prefetched.  The same pass applies
 // RectBatch.validate (geometry.py:166-177): inverted or out-of-[0,1]
 // rectangles raise error bits the host turns into the reference's ValueError.
 __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __restrict__ xl,
@@ -318,35 +352,44 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
                                                u32* __restrict__ cnt, int side,
                                                pbsm_header* hdr) {
   const i64 stride = (i64)gridDim.x * blockDim.x;
+  i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   u32 bad = 0;
-  for (i64 base = blockIdx.x * (i64)blockDim.x + threadIdx.x; base < n;
-       base += stride * kRectsPerThread) {
-    double a[kRectsPerThread], b[kRectsPerThread], c[kRectsPerThread], d[kRectsPerThread];
-#pragma unroll
-    for (int u = 0; u < kRectsPerThread; ++u) {
-      const i64 i = base + u * stride;
-      if (i < n) {
-        a[u] = __ldcs(xl + i);  // streamed once: evict-first, keep the counters in L2
-        b[u] = __ldcs(xu + i);
-        c[u] = __ldcs(yl + i);
-        d[u] = __ldcs(yu + i);
-      }
+  // software pipeline: the next rectangle's loads are in flight while this
+  // one is binned (streamed once: evict-first keeps the counters in L2)
+  double a = 0, b = 0, c = 0, d = 0;
+  if (i < n) {
+    a = __ldcs(xl + i);
+    b = __ldcs(xu + i);
+    c = __ldcs(yl + i);
+    d = __ldcs(yu + i);
+  }
+  for (; i < n; i += stride) {
+    const i64 nx = i + stride;
+    double na = 0, nb = 0, nc = 0, nd = 0;
+    if (nx < n) {
+      na = __ldcs(xl + nx);
+      nb = __ldcs(xu + nx);
+      nc = __ldcs(yl + nx);
+      nd = __ldcs(yu + nx);
     }
-#pragma unroll
-    for (int u = 0; u < kRectsPerThread; ++u) {
-      const i64 i = base + u * stride;
-      if (i >= n) continue;
-      if (!(a[u] <= b[u]) || !(c[u] <= d[u])) bad |= PBSM_ERR_INVERTED;
-      if (a[u] < 0.0 || c[u] < 0.0 || b[u] > 1.0 || d[u] > 1.0) bad |= PBSM_ERR_RANGE;
-      const int c0 = tile_of(a[u], kx, bx);
-      const int c1 = tile_of(b[u], kx, bx);
-      const int r0 = max(tile_of(c[u], ky, by), row_lo);
-      const int r1 = min(tile_of(d[u], ky, by), row_hi - 1);
+    if (!(a <= b) || !(c <= d)) bad |= PBSM_ERR_INVERTED;
+    if (a < 0.0 || c < 0.0 || b > 1.0 || d > 1.0) bad |= PBSM_ERR_RANGE;
+    const int c0 = tile_of(a, kx, bx);
+    const int c1 = tile_of(b, kx, bx);
+    const int r0 = max(tile_of(c, ky, by), row_lo);
+    const int r1 = min(tile_of(d, ky, by), row_hi - 1);
+    if (c0 == c1 && r0 == r1) {
+      atomicAdd(cnt + (size_t)(r0 - row_lo) * kx + c0, 1u);
+    } else {
       for (int row = r0; row <= r1; ++row) {
         u32* rowp = cnt + (size_t)(row - row_lo) * kx;
         for (int col = c0; col <= c1; ++col) atomicAdd(rowp + col, 1u);
       }
     }
+    a = na;
+    b = nb;
+    c = nc;
+    d = nd;
   }
   if (bad) atomicOr(&hdr->error, bad << (2 * side));
 }
@@ -391,10 +434,27 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_scatter(const i64* __re
                                                  i64 capacity, pbsm_header* hdr) {
   u32 bad = 0;
   const u64 pol = l2_evict_first_policy();
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
-       i += (i64)gridDim.x * blockDim.x) {
-    const double a = __ldcs(xl + i), b = __ldcs(xu + i), c = __ldcs(yl + i), d = __ldcs(yu + i);
-    const i64 id = __ldcs(ids + i);
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  double pa = 0, pb = 0, pc = 0, pd = 0;
+  i64 pid = 0;
+  if (i < n) {  // software pipeline: the next rectangle's loads in flight
+    pa = __ldcs(xl + i);
+    pb = __ldcs(xu + i);
+    pc = __ldcs(yl + i);
+    pd = __ldcs(yu + i);
+    pid = __ldcs(ids + i);
+  }
+  for (; i < n; i += stride) {
+    const double a = pa, b = pb, c = pc, d = pd;
+    const i64 id = pid;
+    if (i + stride < n) {
+      pa = __ldcs(xl + i + stride);
+      pb = __ldcs(xu + i + stride);
+      pc = __ldcs(yl + i + stride);
+      pd = __ldcs(yu + i + stride);
+      pid = __ldcs(ids + i + stride);
+    }
     const int c0 = tile_of(a, kx, bx);
     const int c1 = tile_of(b, kx, bx);
     const int rr0 = tile_of(c, ky, by);
@@ -480,19 +540,22 @@ __global__ void k_guard(const u32* __restrict__ cur_r, const u32* __restrict__ e
 }
 
 // ---------------------------------------------------------------- 1b plan
-// Per tile t the plan scans fourteen lanes at once (one exclusive scan each):
+// Per tile t the plan scans twelve lanes at once (one exclusive scan each):
 //   0 |R_T|  1 |S_T|                          all tiles (A_R, A_S totals)
-//   2..5   nested tiles: flag, entries, |R_T|, |S_T|
-//   6..9   sorted tiles: flag, entries, |R_T|, |S_T|
-//   10..13 large tiles:  flag, work items, |R_T|, |S_T|
+//   2..4   nested tiles: flag, |R_T|, |S_T|
+//   5..7   sorted tiles: flag, |R_T|, |S_T|
+//   8..11  large tiles:  flag, work items, |R_T|, |S_T|
 // A join tile has both inputs non-empty (build_task_queue, engine.py:97);
 // its strategy comes from the cost model in include/pbsm.h.  The |R_T| /
 // |S_T| lanes of the three strategies give the tile-list offsets
 // (compute_segment_offsets, partition.py:151-164): each input's list holds
 // the nested tiles, then the sorted tiles, then the large tiles, each region
 // in tile order — so a chunk of consecutive nested (or sorted) tiles is one
-// contiguous range per input, fetched by one TMA bulk copy.
+// contiguous range per input, fetched by one TMA bulk copy.  Within a CTA the
+// lanes are u32 (a CTA's sums never exceed the u32-checked totals); the
+// per-CTA partial sums are u64.
 enum TileKind { kNone = 0, kNested = 1, kSorted = 2, kLarge = 3 };
+enum Lane { L_A, L_B, L_NF, L_NA, L_NB, L_SF, L_SA, L_SB, L_LF, L_LI, L_LA, L_LB };
 
 __device__ __forceinline__ int tile_kind(u32 a, u32 b, i64 nested_max) {
   if (a == 0u || b == 0u) return kNone;
@@ -500,28 +563,26 @@ __device__ __forceinline__ int tile_kind(u32 a, u32 b, i64 nested_max) {
   return (i64)((u64)a * (u64)b) <= nested_max ? kNested : kSorted;
 }
 
-__device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u64 v[kNV]) {
+__device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u32 v[kNV]) {
   const int kind = tile_kind(a, b, nm);
   const u32 lead = a >= b ? a : b;
 #pragma unroll
   for (int q = 0; q < kNV; ++q) v[q] = 0;
-  v[0] = a;
-  v[1] = b;
+  v[L_A] = a;
+  v[L_B] = b;
   if (kind == kNested) {
-    v[2] = 1;
-    v[3] = a + b;
-    v[4] = a;
-    v[5] = b;
+    v[L_NF] = 1;
+    v[L_NA] = a;
+    v[L_NB] = b;
   } else if (kind == kSorted) {
-    v[6] = 1;
-    v[7] = a + b;
-    v[8] = a;
-    v[9] = b;
+    v[L_SF] = 1;
+    v[L_SA] = a;
+    v[L_SB] = b;
   } else if (kind == kLarge) {
-    v[10] = 1;
-    v[11] = (lead + kLargeLead - 1) / kLargeLead;
-    v[12] = a;
-    v[13] = b;
+    v[L_LF] = 1;
+    v[L_LI] = (lead + kLargeLead - 1) / kLargeLead;
+    v[L_LA] = a;
+    v[L_LB] = b;
   }
 }
 
@@ -530,33 +591,32 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
                                                               u64 T, i64 nm,
                                                               u64* __restrict__ partials,
                                                               pbsm_header* hdr) {
-  __shared__ u64 sh[kPlanThreads / 32][kNV];
+  __shared__ u32 sh[kPlanThreads / 32][kNV];
   __shared__ u32 shmax[kPlanThreads / 32];
   __shared__ u64 shb[kPlanThreads / 32];
-  u64 acc[kNV];
+  u32 acc[kNV];
 #pragma unroll
   for (int q = 0; q < kNV; ++q) acc[q] = 0;
   u32 mx = 0;
   u64 bound = 0;
   const u64 base = (u64)blockIdx.x * kPlanTile;
+#pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     const u64 t = base + (u64)i * kPlanThreads + threadIdx.x;
-    if (t < T) {
-      const u32 a = cr[t], b = cs[t];
-      u64 v[kNV];
-      tile_vals(a, b, nm, v);
+    const u32 a = t < T ? cr[t] : 0u, b = t < T ? cs[t] : 0u;
+    u32 v[kNV];
+    tile_vals(a, b, nm, v);
 #pragma unroll
-      for (int q = 0; q < kNV; ++q) acc[q] += v[q];
-      if (a && b) {
-        mx = max(mx, a + b);
-        bound += (u64)a * (u64)b;
-      }
+    for (int q = 0; q < kNV; ++q) acc[q] += v[q];
+    if (a && b) {
+      mx = max(mx, a + b);
+      bound += (u64)a * (u64)b;
     }
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < kNV; ++q) {
-    u64 v = acc[q];
+    u32 v = acc[q];
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if (lane == 0) sh[wid][q] = v;
@@ -583,53 +643,63 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
       m = max(m, shmax[w]);
       bs += shb[w];
     }
-    atomicMax((unsigned long long*)&hdr->max_tile, (unsigned long long)m);
+    if (m) atomicMax((unsigned long long*)&hdr->max_tile, (unsigned long long)m);
     if (bs) atomicAdd((unsigned long long*)&hdr->pair_bound, (unsigned long long)bs);
   }
 }
 
-// single CTA: exclusive scan of the per-CTA partial sums, totals → header
-// and into the extra row nb of `partials` (read by k_plan_apply)
-__global__ void __launch_bounds__(1024) k_plan_partials(u64* __restrict__ partials, u64 nb,
-                                                        pbsm_header* hdr, u32* je_n, u32* je_s,
-                                                        u32* lpre) {
-  __shared__ u64 sh[33];
-  u64 carry[kNV];
+// single CTA, one warp per lane: exclusive scan of the per-CTA partial sums
+// (loads issued kBatch steps ahead), totals → header and into the extra row
+// nb of `partials` (read by k_plan_apply)
+__global__ void __launch_bounds__(kNV * 32) k_plan_partials(u64* __restrict__ partials, u64 nb,
+                                                             pbsm_header* hdr, u32* je_n,
+                                                             u32* je_s, u32* lpre) {
+  constexpr int kBatch = 8;
+  __shared__ u64 tot[kNV];
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  u64 carry = 0;
+  for (u64 b0 = 0; b0 < nb; b0 += 32 * kBatch) {
+    u64 v[kBatch];
 #pragma unroll
-  for (int q = 0; q < kNV; ++q) carry[q] = 0;
-  for (u64 base = 0; base < nb; base += 1024) {
-    const u64 i = base + threadIdx.x;
+    for (int u = 0; u < kBatch; ++u) {
+      const u64 i = b0 + u * 32 + lane;
+      v[u] = i < nb ? partials[i * kNTot + q] : 0ull;
+    }
 #pragma unroll
-    for (int q = 0; q < kNV; ++q) {
-      const u64 v = i < nb ? partials[i * kNTot + q] : 0ull;
-      u64 tot;
-      const u64 ex = block_excl_scan<1024>(v, &tot, sh);
-      if (i < nb) partials[i * kNTot + q] = carry[q] + ex;
-      carry[q] += tot;
+    for (int u = 0; u < kBatch; ++u) {
+      const u64 i = b0 + u * 32 + lane;
+      const u64 inc = warp_incl_scan<u64>(v[u]);
+      if (i < nb) partials[i * kNTot + q] = carry + inc - v[u];
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
   }
+  if (lane == 0) tot[q] = carry;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kNV; ++q) partials[nb * kNTot + q] = carry[q];
-    hdr->a_r = (i64)carry[0];
-    hdr->a_s = (i64)carry[1];
-    hdr->n_nested = (i64)carry[2];
-    hdr->w_nested = (i64)carry[3];
-    hdr->n_sorted = (i64)carry[6];
-    hdr->w_sorted = (i64)carry[7];
-    hdr->n_large = (i64)carry[10];
-    hdr->n_items = (i64)carry[11];
-    const u64 lr = carry[4] + carry[8] + carry[12], ls = carry[5] + carry[9] + carry[13];
+    u64 c[kNV];
+    for (int qq = 0; qq < kNV; ++qq) {
+      c[qq] = tot[qq];
+      partials[nb * kNTot + qq] = c[qq];
+    }
+    hdr->a_r = (i64)c[L_A];
+    hdr->a_s = (i64)c[L_B];
+    hdr->n_nested = (i64)c[L_NF];
+    hdr->w_nested = (i64)(c[L_NA] + c[L_NB]);
+    hdr->n_sorted = (i64)c[L_SF];
+    hdr->w_sorted = (i64)(c[L_SA] + c[L_SB]);
+    hdr->n_large = (i64)c[L_LF];
+    hdr->n_items = (i64)c[L_LI];
+    const u64 lr = c[L_NA] + c[L_SA] + c[L_LA], ls = c[L_NB] + c[L_SB] + c[L_LB];
     hdr->list_r = (i64)lr;
     hdr->list_s = (i64)ls;
     hdr->chunks_nested = 0;
     hdr->chunks_sorted = 0;
     hdr->pairs = 0;
-    if (carry[0] >= kSkip || carry[1] >= kSkip || lr >= kSkip || ls >= kSkip ||
-        carry[3] >= kSkip || carry[7] >= kSkip || carry[11] >= kSkip)
+    if (c[L_A] >= kSkip || c[L_B] >= kSkip || lr >= kSkip || ls >= kSkip || c[L_LI] >= kSkip)
       hdr->error |= PBSM_ERR_TOTAL_RANGE;
-    je_n[carry[2]] = (u32)carry[3];     // sentinels: end of the last tile
-    je_s[carry[6]] = (u32)carry[7];
-    lpre[carry[10]] = (u32)carry[11];
+    je_n[c[L_NF]] = (u32)(c[L_NA] + c[L_NB]);   // sentinels: end of the last tile
+    je_s[c[L_SF]] = (u32)(c[L_SA] + c[L_SB]);
+    lpre[c[L_LF]] = (u32)c[L_LI];
   }
 }
 
@@ -648,7 +718,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ c
                                                              PlanOut P) {
   __shared__ u32 sa[kPlanTile];
   __shared__ u32 sb[kPlanTile];
-  __shared__ u64 shs[33];
+  __shared__ u32 shs[kPlanThreads / 32][kNV];
   const u64 base = (u64)blockIdx.x * kPlanTile;
   for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
     const u64 t = base + i;
@@ -657,64 +727,67 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ c
   }
   __syncthreads();
   u32 a[kPlanPer], b[kPlanPer];
-  u64 pre[kNV];
+  u32 pre[kNV];
 #pragma unroll
   for (int q = 0; q < kNV; ++q) pre[q] = 0;
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     a[i] = sa[threadIdx.x * kPlanPer + i];
     b[i] = sb[threadIdx.x * kPlanPer + i];
-    u64 v[kNV];
+    u32 v[kNV];
     tile_vals(a[i], b[i], nm, v);
 #pragma unroll
     for (int q = 0; q < kNV; ++q) pre[q] += v[q];
   }
-#pragma unroll
-  for (int q = 0; q < kNV; ++q) {
-    u64 tot;
-    pre[q] = block_excl_scan<kPlanThreads>(pre[q], &tot, shs) +
-             partials[(u64)blockIdx.x * kNTot + q];
+  {
+    u32 tot[kNV];
+    block_excl_scan_multi<kPlanThreads, kNV, u32>(pre, tot, shs);
   }
-  // region bases: [nested | sorted | large] in each input's list
+  // global prefixes = this CTA's partial + the u32 in-CTA prefix
+  const u64* part = partials + (u64)blockIdx.x * kNTot;
   const u64* tot = partials + nb * kNTot;
-  const u64 rs_base = tot[4], ss_base = tot[5];
-  const u64 rl_base = tot[4] + tot[8], sl_base = tot[5] + tot[9];
-  // (block_excl_scan ends with a barrier, so sa/sb may be overwritten now:
-  // they receive the cursor starts; the expected cursor ends go back into
-  // cnt[] for k_guard.)
+  u64 g[kNV];
+#pragma unroll
+  for (int q = 0; q < kNV; ++q) g[q] = part[q] + pre[q];
+  // region bases: [nested | sorted | large] in each input's list
+  const u64 rs_base = tot[L_NA], ss_base = tot[L_NB];
+  const u64 rl_base = tot[L_NA] + tot[L_SA], sl_base = tot[L_NB] + tot[L_SB];
+  // (the scan ended with a barrier, so sa/sb may be overwritten now: they
+  // receive the cursor starts; the expected cursor ends go back into cnt[]
+  // for k_guard)
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     const u64 t = base + (u64)threadIdx.x * kPlanPer + i;
     const int kind = tile_kind(a[i], b[i], nm);
     u32 r0 = kSkip, s0 = kSkip;
     if (kind == kNested) {
-      r0 = (u32)pre[4];
-      s0 = (u32)pre[5];
+      r0 = (u32)g[L_NA];
+      s0 = (u32)g[L_NB];
     } else if (kind == kSorted) {
-      r0 = (u32)(rs_base + pre[8]);
-      s0 = (u32)(ss_base + pre[9]);
+      r0 = (u32)(rs_base + g[L_SA]);
+      s0 = (u32)(ss_base + g[L_SB]);
     } else if (kind == kLarge) {
-      r0 = (u32)(rl_base + pre[12]);
-      s0 = (u32)(sl_base + pre[13]);
+      r0 = (u32)(rl_base + g[L_LA]);
+      s0 = (u32)(sl_base + g[L_LB]);
     }
     sa[threadIdx.x * kPlanPer + i] = r0;
     sb[threadIdx.x * kPlanPer + i] = s0;
     if (t < T) {
       if (kind == kNested) {
-        P.jrec[0][pre[2]] = make_uint4(r0, s0, a[i], b[i]);
-        P.je[0][pre[2]] = (u32)pre[3];
+        P.jrec[0][g[L_NF]] = make_uint4(r0, s0, a[i], b[i]);
+        P.je[0][g[L_NF]] = (u32)(g[L_NA] + g[L_NB]);
       } else if (kind == kSorted) {
-        P.jrec[1][pre[6]] = make_uint4(r0, s0, a[i], b[i]);
-        P.je[1][pre[6]] = (u32)pre[7];
+        P.jrec[1][g[L_SF]] = make_uint4(r0, s0, a[i], b[i]);
+        P.je[1][g[L_SF]] = (u32)(g[L_SA] + g[L_SB]);
       } else if (kind == kLarge) {
-        P.lrec[pre[10]] = make_uint4(r0, s0, a[i], b[i]);
-        P.lpre[pre[10]] = (u32)pre[11];
+        P.lrec[g[L_LF]] = make_uint4(r0, s0, a[i], b[i]);
+        P.lpre[g[L_LF]] = (u32)g[L_LI];
       }
     }
-    u64 v[kNV];
+    u32 v[kNV];
     tile_vals(a[i], b[i], nm, v);
 #pragma unroll
-    for (int q = 0; q < kNV; ++q) pre[q] += v[q];
+    for (int q = 0; q < kNV; ++q) g[q] += v[q];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
@@ -1195,22 +1268,61 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
 // however small and lopsided the tiles are, and the hits of a warp-step are
 // compacted with a ballot + popcount into consecutive output slots (one
 // coalesced 16-byte store per hit).
+#ifndef PBSM_NESTED_BUFS
+#define PBSM_NESTED_BUFS 1   // 2 = persistent CTAs with a double-buffered chunk pipeline
+#endif
+constexpr int kNestedBufs = PBSM_NESTED_BUFS;
+
 struct NestedSmem {
-  Rec recs[kCap];                // TMA: the chunk's R range, then its S range
-  uint4 jr[kMaxTiles];           // TMA: the chunk's tile records
+  Rec recs[kNestedBufs][kCap];   // TMA: the chunk's R range, then its S range
+  uint4 jr[kNestedBufs][kMaxTiles];  // TMA: the chunk's tile records
   u64 f[4][kCap + kPad];         // SoA copy of the MBR words (padded rows)
   u32 tP[kMaxTiles + 1];         // pair-index prefix per tile
   u16 tR0[kMaxTiles], tS0[kMaxTiles], tNS[kMaxTiles];
   float tInvS[kMaxTiles];        // 1 / |S_T|
   u64 wtot[kJoinThreads / 32 + 1];
   u64 scan[kJoinThreads / 32 + 1];
-  u64 bar;
+  u64 bar[kNestedBufs];
   u64 base;
-  int nt, NR, NS;
+  int nt[kNestedBufs], NR[kNestedBufs], NS[kNestedBufs];
 };
 
 __device__ __forceinline__ void mbar_arrive(u64* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// thread 0 only: start loading chunk c into buffer b; always completes one
+// phase of bar[b] (with or without data)
+__device__ __forceinline__ void nested_prefetch(NestedSmem& S, const JoinArgs& A, int b, i64 c,
+                                                i64 n_chunks) {
+  b = kNestedBufs == 1 ? 0 : b;
+  int nt = 0, NR = 0, NS = 0;
+  uint4 d0 = make_uint4(0, 0, 0, 0);
+  if (c < n_chunks) {
+    d0 = A.cdesc[0][c];
+    const uint4 d1 = A.cdesc[0][c + 1];
+    nt = (int)(d1.x - d0.x);
+    NR = (int)(d1.y - d0.y);
+    NS = (int)(d1.z - d0.z);
+    if (!(nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles)) {
+      atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);  // never by construction
+      nt = NR = NS = 0;
+    }
+  }
+  S.nt[b] = nt;
+  S.NR[b] = NR;
+  S.NS[b] = NS;
+  if (nt == 0) {
+    mbar_arrive(&S.bar[b]);
+    return;
+  }
+  // the buffer was last read through the generic proxy: order those reads
+  // before the async-proxy (TMA) writes
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  mbar_expect_tx(&S.bar[b], (u32)nt * 16u + (u32)(NR + NS) * (u32)sizeof(Rec));
+  bulk_g2s(&S.jr[b][0], A.jrec[0] + d0.x, (u32)nt * 16u, &S.bar[b]);
+  bulk_g2s(&S.recs[b][0], A.rl + d0.y, (u32)NR * (u32)sizeof(Rec), &S.bar[b]);
+  bulk_g2s(&S.recs[b][NR], A.sl + d0.z, (u32)NS * (u32)sizeof(Rec), &S.bar[b]);
 }
 
 // first tile of warp-step q0: binary search over the pair prefix (the same
@@ -1250,41 +1362,11 @@ __device__ __forceinline__ bool nested_hit(const NestedSmem& S, int pr, int ps) 
   return pair_ok(S.f[0][pr], rxu, ryl, ryu, S.f[0][ps], sxu, syl, syu);
 }
 
+// One chunk from buffer b (staged and waited for by the caller).
 template <bool EMIT>
-__global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64 n_chunks) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
-  __shared__ int s_unit;
+__device__ __forceinline__ void nested_chunk(NestedSmem& S, const JoinArgs& A, int b, i64 c) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (A.ordered) {  // the look-back needs units handed out in launch order
-    if (tid == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
-    __syncthreads();
-  }
-  const i64 c = A.ordered ? s_unit : blockIdx.x;
-  if (tid == 0) {
-    const uint4 d0 = A.cdesc[0][c], d1 = A.cdesc[0][c + 1];
-    int nt = (int)(d1.x - d0.x), NR = (int)(d1.y - d0.y), NS = (int)(d1.z - d0.z);
-    const bool fits = nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles;
-    if (!fits) {  // never by construction; contribute 0 pairs, keep the chain fed
-      atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
-      nt = NR = NS = 0;
-    }
-    S.nt = nt;
-    S.NR = NR;
-    S.NS = NS;
-    mbar_init(&S.bar, 1);
-    if (fits) {
-      mbar_expect_tx(&S.bar, (u32)nt * 16u + (u32)(NR + NS) * (u32)sizeof(Rec));
-      bulk_g2s(&S.jr[0], A.jrec[0] + d0.x, (u32)nt * 16u, &S.bar);
-      bulk_g2s(&S.recs[0], A.rl + d0.y, (u32)NR * (u32)sizeof(Rec), &S.bar);
-      bulk_g2s(&S.recs[NR], A.sl + d0.z, (u32)NS * (u32)sizeof(Rec), &S.bar);
-    } else {
-      mbar_arrive(&S.bar);
-    }
-  }
-  __syncthreads();
-  const int nt = S.nt, NR = S.NR, N = S.NR + S.NS;
-  mbar_wait(&S.bar, 0);
+  const int nt = S.nt[b], NR = S.NR[b], N = S.NR[b] + S.NS[b];
   // tile table + pair prefix (nt <= kMaxTiles <= 2 * kJoinThreads)
   static_assert(kMaxTiles <= 2 * kJoinThreads, "two tiles per thread");
   u32 np = 0;
@@ -1292,7 +1374,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64
   for (int h = 0; h < 2; ++h) {
     const int lt = 2 * tid + h;
     if (lt < nt) {
-      const uint4 r = S.jr[lt], r0 = S.jr[0];
+      const uint4 r = S.jr[b][lt], r0 = S.jr[b][0];
       S.tR0[lt] = (u16)(r.x - r0.x);
       S.tS0[lt] = (u16)(NR + (int)(r.y - r0.y));
       S.tNS[lt] = (u16)r.w;
@@ -1307,13 +1389,13 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64
     const int lt = 2 * tid + h;
     if (lt < nt) {
       S.tP[lt] = pre;
-      pre += S.jr[lt].z * S.jr[lt].w;
+      pre += S.jr[b][lt].z * S.jr[b][lt].w;
     }
   }
   if (tid == 0) S.tP[nt] = (u32)tot;
   // SoA transpose, conflict-free: a warp reads 4 whole records per step
   {
-    const u64* words = reinterpret_cast<const u64*>(S.recs);
+    const u64* words = reinterpret_cast<const u64*>(S.recs[b]);
     for (int r0 = warp * 4; r0 < N; r0 += 4 * (kJoinThreads / 32)) {
       const int r = r0 + (lane >> 3), word = lane & 7;
       if (r < N && word < 4) S.f[word][r] = words[r * 8 + word];
@@ -1322,19 +1404,27 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64
   __syncthreads();
   const u32 NP = (u32)tot;
   const unsigned lt_mask = (1u << lane) - 1u;
+  // each warp owns one contiguous slice of the pair index space, so the tile
+  // of its current step only moves forward: one binary search per warp
+  constexpr int kW = kJoinThreads / 32;
+  const u32 per = ((NP + kW - 1) / kW + 31u) & ~31u;
+  const u32 q_beg = min(NP, (u32)warp * per), q_end = min(NP, q_beg + per);
+  const int lt_beg = q_beg < NP ? nested_tile_of(S, nt, q_beg) : 0;
   // pass 1: count
   u32 wcnt = 0;
-  for (u32 q0 = (u32)warp * 32u; q0 < NP; q0 += kJoinThreads) {
+  int lt = lt_beg;
+  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
+    while (q0 >= S.tP[lt + 1]) ++lt;  // warp-uniform
     int pr, ps;
-    const int lt = nested_tile_of(S, nt, q0);
-    const bool hit = nested_pair(S, nt, q0 + lane, lt, pr, ps) && nested_hit(S, pr, ps);
+    const bool hit = q0 + lane < q_end && nested_pair(S, nt, q0 + lane, lt, pr, ps) &&
+                     nested_hit(S, pr, ps);
     wcnt += __popc(__ballot_sync(0xffffffffu, hit));
   }
   if (lane == 0) S.wtot[warp] = wcnt;
   __syncthreads();
   if (tid == 0) {
     u64 t = 0;
-    for (int w = 0; w < kJoinThreads / 32; ++w) {
+    for (int w = 0; w < kW; ++w) {
       const u64 v = S.wtot[w];
       S.wtot[w] = t;
       t += v;
@@ -1352,18 +1442,63 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64
   if (!EMIT) return;
   __syncthreads();
   if (S.base == ~0ull) return;
-  // pass 2: emit, ballot-compacted
+  // pass 2: emit, ballot-compacted (same slices, same order)
   i64* out = A.pairs + 2 * (i64)(S.base + S.wtot[warp]);
-  for (u32 q0 = (u32)warp * 32u; q0 < NP; q0 += kJoinThreads) {
+  lt = lt_beg;
+  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
+    while (q0 >= S.tP[lt + 1]) ++lt;
     int pr = 0, ps = 0;
-    const int lt = nested_tile_of(S, nt, q0);
-    const bool hit = nested_pair(S, nt, q0 + lane, lt, pr, ps) && nested_hit(S, pr, ps);
+    const bool hit = q0 + lane < q_end && nested_pair(S, nt, q0 + lane, lt, pr, ps) &&
+                     nested_hit(S, pr, ps);
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (hit) {
       const i64 o = __popc(m & lt_mask);
-      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(S.recs[pr].id, S.recs[ps].id);
+      *reinterpret_cast<longlong2*>(out + 2 * o) =
+          make_longlong2(S.recs[b][pr].id, S.recs[b][ps].id);
     }
     out += 2 * (i64)__popc(m);
+  }
+}
+
+// One CTA per chunk (default), or with PBSM_NESTED_BUFS=2 persistent CTAs
+// walking chunks c = blockIdx.x + i * gridDim.x while the TMA engine fills the
+// other buffer with chunk i+1.  Measured on B200 the single-buffer form wins:
+// the per-chunk cost is dominated by the in-CTA barriers and scans, so more
+// resident CTAs beat a deeper load pipeline.
+template <bool EMIT>
+__global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64 n_chunks) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  if (kNestedBufs == 1) {
+    __shared__ int s_unit;
+    if (A.ordered) {  // the look-back needs units handed out in launch order
+      if (tid == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
+      __syncthreads();
+    }
+    const i64 c = A.ordered ? s_unit : blockIdx.x;
+    if (tid == 0) {
+      mbar_init(&S.bar[0], 1);
+      nested_prefetch(S, A, 0, c, n_chunks);
+    }
+    __syncthreads();
+    mbar_wait(&S.bar[0], 0);
+    nested_chunk<EMIT>(S, A, 0, c);
+    return;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < kNestedBufs; ++b) mbar_init(&S.bar[b], 1);
+    nested_prefetch(S, A, 0, blockIdx.x, n_chunks);
+  }
+  for (i64 i = 0;; ++i) {
+    const i64 c = blockIdx.x + i * gridDim.x;
+    if (c >= n_chunks) break;
+    const int b = (int)(i & 1);
+    if (tid == 0) nested_prefetch(S, A, b ^ 1, c + gridDim.x, n_chunks);
+    __syncthreads();  // S.nt[b] & co (written by thread 0 an iteration ago) visible
+    mbar_wait(&S.bar[b], (u32)((i >> 1) & 1));
+    nested_chunk<EMIT>(S, A, b, c);
+    __syncthreads();  // buffer b and the chunk scratch free for reuse
   }
 }
 
@@ -1522,10 +1657,19 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.total = (unsigned long long*)&w.hdr->pairs;
   A.ordered = ordered ? 1 : 0;
   if (cn > 0) {
+    // persistent grid: at most the resident CTAs (the ordered look-back waits
+    // on chunks of other CTAs, so every CTA must be resident)
+    const void* fn = emit ? (const void*)k_join_nested<true> : (const void*)k_join_nested<false>;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads,
+                                                      sizeof(NestedSmem)) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    const i64 grid = kNestedBufs == 1 ? cn : std::min<i64>(cn, (i64)per_sm * num_sms());
     if (emit)
-      k_join_nested<true><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+      k_join_nested<true><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
     else
-      k_join_nested<false><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+      k_join_nested<false><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
   }
   if (rest > 0) {
     // the sorted/large launch keeps its own ticket (the look-back ids follow
@@ -1598,7 +1742,7 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
   const i64 nm = nested_max < 0 ? (i64)kNestedMax : (i64)nested_max;
   k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles, nm,
                                                               w.partials, w.hdr);
-  k_plan_partials<<<1, 1024, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je[0], w.je[1], w.lpre);
+  k_plan_partials<<<1, kNV * 32, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je[0], w.je[1], w.lpre);
   PlanOut P;
   P.cur_r = w.cur_r;
   P.cur_s = w.cur_s;

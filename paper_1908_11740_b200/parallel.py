@@ -95,7 +95,10 @@ def exchange_counts(count: int, a_r: int, a_s: int, device=None, group=None) -> 
         allv = mine.view(1, 3)
     else:
         allv = torch.empty((world, 3), dtype=torch.int64, device=device)
-        dist.all_gather_into_tensor(allv, mine, group=group)
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(allv, mine, group=group)
+        else:  # gloo (CPU ranks) has no all_gather_into_tensor
+            dist.all_gather(list(allv.unbind(0)), mine, group=group)
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     v = allv.cpu().numpy()
     offs = np.concatenate([[0], np.cumsum(v[:, 0])])
@@ -116,3 +119,33 @@ def combine_counts(count: int, a_r: int, a_s: int, t_local: float, world: int,
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     out["t_max"] = float(t.item())
     return out
+
+
+def owner_rows(r, s, pairs: np.ndarray, k: int) -> np.ndarray:
+    """Tile row that owns each (r_id, s_id) pair: the row of max(r.yl, s.yl)
+    (Eq. 1's reference point, geometry.py:64-72).  Ids must be row indices."""
+    yl = np.maximum(r[3][pairs[:, 0]], s[3][pairs[:, 1]])
+    return _tile_index(yl, k)
+
+
+def distributed_join(r, s, k: int, device=None, collect: bool = True):
+    """One rank's share of a strip-sharded K×K join (call under torchrun).
+
+    Every rank plans the same strips, keeps the rectangles meeting its strip,
+    joins its tile rows on its GPU and learns its global pair offset from the
+    single all_gather.  Returns (DeviceJoinResult, exchange dict)."""
+    import torch.distributed as dist
+
+    from . import device as dev
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    cuts = plan_strips(r, s, k, world)
+    lo, hi = cuts[rank], cuts[rank + 1]
+    rr = strip_inputs(r, k, lo, hi)
+    ss = rr if s is r else strip_inputs(s, k, lo, hi)
+    rd = dev.to_device(rr, device)
+    sd = rd if s is r else dev.to_device(ss, device)
+    res = dev.run_join(rd, sd, k, k, collect=collect, row_lo=lo, row_hi=hi)
+    ex = exchange_counts(res.count, res.header["a_r"], res.header["a_s"], device=device)
+    return res, ex

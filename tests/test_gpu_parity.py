@@ -239,3 +239,48 @@ def test_instances_all_strategies(golden):
             assert res.count == count, (tag, nested_max)
             got = oracle.sorted_pairs(res.pairs.cpu().numpy())
             assert np.array_equal(got, g[f"{tag}_pairs"]), (tag, nested_max)
+
+
+@pytest.mark.parametrize("cfg,world", [(1, 3), (2, 4), (5, 8)])
+def test_strips_on_one_gpu_reassemble_full_join(golden, cfg, world):
+    """The per-rank pipeline of a strip-sharded join (row_lo/row_hi), run for
+    every strip one after another on one GPU: the strips' pair lists are
+    disjoint and their union is the reference result (no cross-strip
+    duplicates thanks to the global class labels)."""
+    from paper_1908_11740_b200 import parallel
+
+    g = golden["configs"]
+    r, s, k = make_config(cfg, float(g[f"cfg{cfg}_scale"]))
+    cuts = parallel.plan_strips(r, s, k, world)
+    parts = []
+    for lo, hi in zip(cuts, cuts[1:]):
+        rr = parallel.strip_inputs(r, k, lo, hi)
+        ss = rr if s is r else parallel.strip_inputs(s, k, lo, hi)
+        rd = dev.to_device(rr)
+        sd = rd if s is r else dev.to_device(ss)
+        res = dev.run_join(rd, sd, k, k, row_lo=lo, row_hi=hi)
+        parts.append(res.pairs.cpu().numpy())
+    got = oracle.sorted_pairs(np.concatenate(parts))
+    assert len(got) == int(g[f"cfg{cfg}_count"])
+    assert np.array_equal(got, g[f"cfg{cfg}_pairs"])
+
+
+def test_device_tile_of_at_boundaries(golden):
+    """Points exactly on, just below and just above every boundary i/k (the
+    reference's axis_tile_index known answers): the device per-tile counts
+    equal the oracle's count_tiles, i.e. the device tile_of (fast path and
+    table path) agrees with the reference bit for bit."""
+    g = golden["tile_of"]
+    for k in sorted(set(int(x) for x in g["k"])):
+        if k > 4000:
+            continue  # K^2 counters; the host KAT test covers the large k
+        p = g["p"][g["k"] == k]
+        n = len(p)
+        rng = np.random.default_rng(k)
+        q = rng.permutation(p)  # y coordinates: the same values, shuffled
+        pts = (np.arange(n, dtype=np.int64), p, p, q, q)
+        res = dev.run_join(dev.to_device(pts), dev.to_device(pts), k, k, collect=False,
+                           keep_counts=True)
+        got = res.tile_counts[0].cpu().numpy().astype(np.int64)
+        want = oracle.count_tiles(pts, "2d", k)
+        assert np.array_equal(got, want), k
