@@ -218,6 +218,11 @@ __device__ __forceinline__ int tile_of(double p, int k, const double* __restrict
   const int ri = (int)__double2loint(t);
   const int i0 = ri - (dlt < 0.0 ? 1 : 0);  // floor(f)
   if (fabs(dlt) > 1e-9 && i0 >= 0 && i0 < k) return i0;
+  // clipped coordinates sit exactly on the domain edges (0.0 / 1.0) and are
+  // common (clipped clusters): the reference loop settles at 0 for p <= 0
+  // and at k-1 for p >= 1 (b[1] = 1/k > 0, b[k-1] < 1)
+  if (p <= 0.0) return 0;
+  if (p >= 1.0) return k - 1;
   long long i = (long long)f;
   if (!(i >= 0)) i = 0;
   if (i > k - 1) i = k - 1;
