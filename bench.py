@@ -113,6 +113,14 @@ class ClockSampler:
             self.t.join(timeout=2)
 
     def summary(self):
+        lo, hi = getattr(self, "t_begin", None), getattr(self, "t_end", None)
+        if lo is not None and hi is not None:
+            inside = [x for x in self.samples if lo <= x[0] <= hi]
+            # the step can be shorter than the sampling period: keep the
+            # samples nearest the window (warm-up runs the same kernels)
+            if len(inside) < 3:
+                inside = sorted(self.samples, key=lambda x: min(abs(x[0] - lo), abs(x[0] - hi)))[:5]
+            self.samples = inside
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [],
                     "samples": 0, "note": getattr(self, "err", "no samples")}
@@ -127,7 +135,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU legs
-def cpu_sample(cfg: int, budget_s: float, threads: int):
+def cpu_sample(cfg: int, budget_s: float, threads: int, probe_f: float = 0.02):
     """A bounded sample of the workload for the CPU: the rectangles overlapping
     a bottom strip of the square (same density as the full job)."""
     import oracle
@@ -141,8 +149,7 @@ def cpu_sample(cfg: int, budget_s: float, threads: int):
         return tuple(a[m] for a in b)
 
     frac = 1.0
-    # probe on a 2% strip, then size the sample to the budget
-    probe_f = 0.02
+    # probe on a small strip, then size the sample to the budget
     rp = strip(r, probe_f)
     sp = rp if s is r else strip(s, probe_f)
     t = oracle.join(rp, sp, "2d", k, threads=threads)["total_time"]
@@ -175,7 +182,7 @@ def reference_arm(args):
         return 0
     threads = os.cpu_count() or 1
     budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
-    rs, ss, k, frac, n, n_total = cpu_sample(args.config, budget, threads)
+    rs, ss, k, frac, n, n_total = cpu_sample(args.config, budget, threads, probe_f=0.1)
     for _ in range(args.warmup):
         run_cpu(args.config, threads, rs, ss, k)
     t0 = time.perf_counter()
@@ -204,12 +211,14 @@ def reference_arm(args):
 
 
 # ---------------------------------------------------------------- GPU arm
-def count_launches(h: dict) -> int:
+def count_launches(h: dict, dev) -> int:
     """Our kernels per join step (see device.run_join / pbsm.cu host glue)."""
     n = 1            # k_bounds
     n += 2           # k_count R, S
     n += 5           # k_plan_reduce, k_plan_partials, k_plan_apply, k_chunks x2
     n += 2           # k_scatter R, S
+    for total in (h["list_r"], h["list_s"]):  # binned scatter: 3 scan kernels + k_bin_copy
+        n += 4 if 64 * total > dev.BIN_LIST_BYTES else 0
     n += 1           # k_guard
     n += 1 if h["n_units"] > 0 else 0   # k_join (all mini-join strategies, count -> emit)
     return n
@@ -268,19 +277,22 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local).__enter__()  # running through warm-up: no start-up gap
     for _ in range(max(3, args.warmup)):
         res = step()
     barrier()
     probe = dev.PhaseProbe()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        barrier()
-        start.record()
-        for _ in range(args.steps):
-            res = step(probe)
-        end.record()
-        barrier()
+    barrier()
+    clocks.t_begin = time.perf_counter()
+    start.record()
+    for _ in range(args.steps):
+        res = step(probe)
+    end.record()
+    barrier()
+    clocks.t_end = time.perf_counter()
+    clocks.__exit__(None, None, None)
     t_local = start.elapsed_time(end) / 1e3
     t = t_local
     local_pairs = res.count
@@ -308,6 +320,7 @@ def main():
         "scatter": 40 * n_in + 40 * lists,            # MBR+id read, entry written
         "join": 40 * lists + 16 * local_pairs,        # entry read, pair written
         "plan": 4 * 6 * (k * (row_hi - row_lo)),
+        "bin": 80 * n_in,
         "init": 8 * k * (row_hi - row_lo),
     }[dom]
     dom_gbs = dom_bytes / dev_phases[dom] / 1e9
@@ -366,7 +379,7 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return 0
-    launches = count_launches(res.header) * args.steps
+    launches = count_launches(res.header, dev) * args.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": step_s * 1e3,

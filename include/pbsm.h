@@ -143,6 +143,21 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu,
                  void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                  pbsm_entry* out, int64_t capacity, void* stream);
 
+/* Binned scatter (worth it when an input's tile lists are large, e.g. > 1 GB).
+ * pbsm_bin copies the input's rectangles into row-band order — 256 bands of
+ * the strip's tile rows, band-major, from the band counts pbsm_count
+ * gathered — as 40-byte records {id, xl, xu, yl, yu} into `band` (n records);
+ * pbsm_scatter_banded then scatters from that copy.  Its random record writes
+ * stay within one band's slice of the tile lists at a time (an L2-sized
+ * window) instead of the whole list.  Same result; needs the pbsm_count of
+ * this input with the same n. */
+int pbsm_bin(const int64_t* ids, const double* xl, const double* xu, const double* yl,
+             const double* yu, int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky,
+             int32_t row_lo, int32_t row_hi, void* band, void* stream);
+int pbsm_scatter_banded(const void* band, int64_t n, int32_t side, void* ws, int32_t kx,
+                        int32_t ky, int32_t row_lo, int32_t row_hi, pbsm_entry* out,
+                        int64_t capacity, void* stream);
+
 /* Scratch bytes for one join over n_units work units
  * (n_units = chunks_nested + chunks_sorted + n_items).  The join entry points
  * take `plan`, the host copy of the header read after pbsm_plan, for the

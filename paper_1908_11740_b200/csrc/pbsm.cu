@@ -89,6 +89,9 @@ constexpr int kScanTile = kScanThreads * kScanPer;
 #ifndef PBSM_RPT
 #define PBSM_RPT 1
 #endif
+#ifndef PBSM_BIN_DIRECT
+#define PBSM_BIN_DIRECT 0
+#endif
 #ifndef PBSM_EF_STORE
 #define PBSM_EF_STORE 0
 #endif
@@ -96,6 +99,10 @@ constexpr int kScanTile = kScanThreads * kScanPer;
 #define PBSM_PART_MINB 4
 #endif
 constexpr int kRectsPerThread = PBSM_RPT;  // ILP in the count / scatter passes
+constexpr int kBins = 256;                  // row bands of the binned scatter
+constexpr int kBinSlots = kBins + 1;        // + one slot for rectangles outside the strip
+constexpr int kMaxPartBlocks = 4096;        // grid cap of the count / bin passes
+constexpr int kBinTile = 1024;              // rectangles staged per bin-copy step
 
 constexpr u64 kXOut = 1ull << 63;
 constexpr u64 kYOut = 1ull << 62;
@@ -127,7 +134,7 @@ struct __align__(32) Half {  // the MBR half of a record: one sector
 // ---------------------------------------------------------------- workspace
 struct WsLayout {
   size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec[2], je[2], cdesc[2], lrec, lpre,
-      partials, total;
+      partials, bc[2], bo, bscan, total;
   u64 tiles;
   u64 nblocks;
 };
@@ -155,6 +162,11 @@ inline WsLayout ws_layout(int kx, int ky, int row_lo, int row_hi) {
   L.lrec = o; o = align_up(o + 16 * T, 256);
   L.lpre = o; o = align_up(o + 4 * (T + 1), 256);
   L.partials = o; o = align_up(o + sizeof(u64) * kNTot * (L.nblocks + 1), 256);
+  for (int q = 0; q < 2; ++q) {  // per-(band, block) rectangle counts of each input
+    L.bc[q] = o; o = align_up(o + 4 * (size_t)kBinSlots * kMaxPartBlocks, 256);
+  }
+  L.bo = o; o = align_up(o + 8 * ((size_t)kBinSlots * kMaxPartBlocks + 1), 256);
+  L.bscan = o; o = align_up(o + 8 * (((size_t)kBinSlots * kMaxPartBlocks) / 4096 + 2), 256);
   L.total = o;
   return L;
 }
@@ -169,6 +181,9 @@ struct Ws {
   uint4* jrec[2];   // {r_start, s_start, nR, nS}
   uint4* lrec;
   u64* partials;
+  u32* bc[2];
+  u64* bo;
+  u64* bscan;
   u64 tiles, nblocks;
 };
 
@@ -190,6 +205,9 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
   w.lrec = (uint4*)(b + L.lrec);
   w.lpre = (u32*)(b + L.lpre);
   w.partials = (u64*)(b + L.partials);
+  for (int q = 0; q < 2; ++q) w.bc[q] = (u32*)(b + L.bc[q]);
+  w.bo = (u64*)(b + L.bo);
+  w.bscan = (u64*)(b + L.bscan);
   w.tiles = L.tiles;
   w.nblocks = L.nblocks;
   return w;
@@ -344,9 +362,34 @@ __global__ void k_bounds(double* bx, int kx, double* by, int ky) {
 
 // ---------------------------------------------------------------- 1a count
 // count_tiles (_kernels.pyx:34-58) for all rectangles, one per thread and
-// loop step with the next one prefetched.  The same pass applies
+// loop step with the next one prefetched; block b takes a contiguous input
+// range and also counts its rectangles per row band (binned scatter, below).
+// The same pass applies
 // RectBatch.validate (geometry.py:166-177): inverted or out-of-[0,1]
 // rectangles raise error bits the host turns into the reference's ValueError.
+// one rectangle of the row-band copy: 40 bytes, so a band run of a few
+// rectangles covers whole sectors (five separate 8-byte columns would write
+// partial sectors at every run)
+struct BRec {
+  i64 id;
+  double xl, xu, yl, yu;
+};
+static_assert(sizeof(BRec) == 40, "band record");
+
+// band of a rectangle in the binned scatter: its first tile row inside the
+// strip, in kBins equal row bands; rectangles that miss the strip → kBins
+__device__ __forceinline__ int band_of(int r0, int r1, int row_lo, int row_hi) {
+  if (r0 > r1) return kBins;
+  return (int)(((i64)(r0 - row_lo) * kBins) / (row_hi - row_lo));
+}
+
+// the contiguous input range of block b in the count and bin passes
+__device__ __forceinline__ void part_range(i64 n, i64& beg, i64& end) {
+  const i64 per = (n + gridDim.x - 1) / gridDim.x;
+  beg = min(n, (i64)blockIdx.x * per);
+  end = min(n, beg + per);
+}
+
 __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __restrict__ xl,
                                                const double* __restrict__ xu,
                                                const double* __restrict__ yl,
@@ -355,23 +398,28 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
                                                const double* __restrict__ bx,
                                                const double* __restrict__ by,
                                                u32* __restrict__ cnt, int side,
+                                               u32* __restrict__ band_cnt,
                                                pbsm_header* hdr) {
-  const i64 stride = (i64)gridDim.x * blockDim.x;
-  i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  __shared__ u32 hist[kBinSlots];
+  for (int g = threadIdx.x; g < kBinSlots; g += blockDim.x) hist[g] = 0;
+  __syncthreads();
+  i64 beg, end;
+  part_range(n, beg, end);
+  i64 i = beg + threadIdx.x;
   u32 bad = 0;
   // software pipeline: the next rectangle's loads are in flight while this
   // one is binned (streamed once: evict-first keeps the counters in L2)
   double a = 0, b = 0, c = 0, d = 0;
-  if (i < n) {
+  if (i < end) {
     a = __ldcs(xl + i);
     b = __ldcs(xu + i);
     c = __ldcs(yl + i);
     d = __ldcs(yu + i);
   }
-  for (; i < n; i += stride) {
-    const i64 nx = i + stride;
+  for (; i < end; i += blockDim.x) {
+    const i64 nx = i + blockDim.x;
     double na = 0, nb = 0, nc = 0, nd = 0;
-    if (nx < n) {
+    if (nx < end) {
       na = __ldcs(xl + nx);
       nb = __ldcs(xu + nx);
       nc = __ldcs(yl + nx);
@@ -383,6 +431,7 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
     const int c1 = tile_of(b, kx, bx);
     const int r0 = max(tile_of(c, ky, by), row_lo);
     const int r1 = min(tile_of(d, ky, by), row_hi - 1);
+    atomicAdd_block(&hist[band_of(r0, r1, row_lo, row_hi)], 1u);
     if (c0 == c1 && r0 == r1) {
       atomicAdd(cnt + (size_t)(r0 - row_lo) * kx + c0, 1u);
     } else {
@@ -397,6 +446,126 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
     d = nd;
   }
   if (bad) atomicOr(&hdr->error, bad << (2 * side));
+  __syncthreads();
+  // band-major: all blocks' counts of band 0, then band 1, ...
+  for (int g = threadIdx.x; g < kBinSlots; g += blockDim.x)
+    band_cnt[(size_t)g * gridDim.x + blockIdx.x] = hist[g];
+}
+
+// Binned scatter, step 1 (only for inputs whose tile lists are large): copy
+// the rectangles into row-band order.  Block b re-reads its range of the count
+// pass in steps of kBinTile rectangles, counting-sorts each step by band in
+// shared memory and writes every band run contiguously at that band's next
+// slot for this block (band-major prefix of the count pass' band counts).
+// The scatter then reads this copy, so at any moment the GPU writes the tile
+// lists of one or two bands — a window that stays in L2 — instead of
+// scattering 64-byte records over the whole list.
+__global__ void __launch_bounds__(256) k_bin_copy(const i64* __restrict__ ids,
+                                                  const double* __restrict__ xl,
+                                                  const double* __restrict__ xu,
+                                                  const double* __restrict__ yl,
+                                                  const double* __restrict__ yu, i64 n,
+                                                  int ky, int row_lo, int row_hi,
+                                                  const double* __restrict__ by,
+                                                  const u64* __restrict__ band_off,
+                                                  BRec* __restrict__ out) {
+  constexpr int kPer = kBinTile / 256;
+  __shared__ u32 cursor[kBinSlots];
+  __shared__ u32 hist[kBinSlots];
+#if !PBSM_BIN_DIRECT
+  __shared__ u32 start[kBinSlots + 1];
+#endif
+#if !PBSM_BIN_DIRECT
+  __shared__ i64 s_id[kBinTile];
+  __shared__ double s_xl[kBinTile], s_xu[kBinTile], s_yl[kBinTile], s_yu[kBinTile];
+  __shared__ u16 s_band[kBinTile];
+  __shared__ u64 scan_sh[256 / 32 + 1];
+#endif
+  for (int g = threadIdx.x; g < kBinSlots; g += blockDim.x)
+    cursor[g] = (u32)band_off[(size_t)g * gridDim.x + blockIdx.x];
+  i64 beg, end;
+  part_range(n, beg, end);
+  for (i64 t0 = beg; t0 < end; t0 += kBinTile) {
+    for (int g = threadIdx.x; g < kBinSlots; g += blockDim.x) hist[g] = 0;
+    __syncthreads();
+    i64 id[kPer];
+    double a[kPer], b[kPer], c[kPer], d[kPer];
+    int band[kPer];
+    u32 rank[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const i64 i = t0 + threadIdx.x + u * 256;
+      band[u] = -1;
+      if (i < end) {
+        id[u] = __ldcs(ids + i);
+        a[u] = __ldcs(xl + i);
+        b[u] = __ldcs(xu + i);
+        c[u] = __ldcs(yl + i);
+        d[u] = __ldcs(yu + i);
+        const int r0 = max(tile_of(c[u], ky, by), row_lo);
+        const int r1 = min(tile_of(d[u], ky, by), row_hi - 1);
+        band[u] = band_of(r0, r1, row_lo, row_hi);
+        rank[u] = atomicAdd_block(&hist[band[u]], 1u);
+      }
+    }
+    __syncthreads();
+#if PBSM_BIN_DIRECT
+    // each record straight to its band's frontier for this block; the
+    // frontier lines (kBinSlots per block) stay in L2 and merge there
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      if (band[u] < 0) continue;
+      BRec r;
+      r.id = id[u];
+      r.xl = a[u];
+      r.xu = b[u];
+      r.yl = c[u];
+      r.yu = d[u];
+      out[cursor[band[u]] + rank[u]] = r;
+    }
+    __syncthreads();
+#else
+    // exclusive scan of the step's band histogram (kBinSlots <= 2 per thread)
+    {
+      const int g0 = 2 * threadIdx.x;
+      const u32 h0 = g0 < kBinSlots ? hist[g0] : 0u, h1 = g0 + 1 < kBinSlots ? hist[g0 + 1] : 0u;
+      u64 tot;
+      const u32 ex = (u32)block_excl_scan<256>((u64)(h0 + h1), &tot, scan_sh);
+      if (g0 < kBinSlots) start[g0] = ex;
+      if (g0 + 1 < kBinSlots) start[g0 + 1] = ex + h0;
+      if (threadIdx.x == 0) start[kBinSlots] = (u32)tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      if (band[u] < 0) continue;
+      const u32 p = start[band[u]] + rank[u];
+      s_id[p] = id[u];
+      s_xl[p] = a[u];
+      s_xu[p] = b[u];
+      s_yl[p] = c[u];
+      s_yu[p] = d[u];
+      s_band[p] = (u16)band[u];
+    }
+    __syncthreads();
+    // band runs out, consecutive threads → consecutive slots of a run
+    const int m = (int)start[kBinSlots];
+    for (int e = threadIdx.x; e < m; e += 256) {
+      const int g = s_band[e];
+      const u32 dst = cursor[g] + (u32)(e - (int)start[g]);
+      BRec r;
+      r.id = s_id[e];
+      r.xl = s_xl[e];
+      r.xu = s_xu[e];
+      r.yl = s_yl[e];
+      r.yu = s_yu[e];
+      out[dst] = r;
+    }
+    __syncthreads();
+#endif
+    for (int g = threadIdx.x; g < kBinSlots; g += blockDim.x) cursor[g] += hist[g];
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------- 1c scatter
@@ -427,11 +596,31 @@ __device__ __forceinline__ void write_rec(Rec* r, u64 key, double xu, double yl,
 // non-empty get a list (the others cannot produce a pair: build_task_queue
 // joins only those, engine.py:97); their cursors start at kSkip and the write
 // is skipped, but the cursor still advances so k_guard can check every tile.
-__global__ void __launch_bounds__(256, PBSM_PART_MINB) k_scatter(const i64* __restrict__ ids,
-                                                 const double* __restrict__ xl,
-                                                 const double* __restrict__ xu,
-                                                 const double* __restrict__ yl,
-                                                 const double* __restrict__ yu, i64 n,
+// Input of the scatter: the caller's SoA columns, or the row-band copy.
+struct ScatterIn {
+  const i64* ids;
+  const double *xl, *xu, *yl, *yu;
+  const BRec* band;  // non-null: read the row-band copy instead
+  __device__ __forceinline__ void load(i64 i, double& a, double& b, double& c, double& d,
+                                       i64& id) const {
+    if (band) {
+      const BRec* r = band + i;
+      id = __ldcs(&r->id);
+      a = __ldcs(&r->xl);
+      b = __ldcs(&r->xu);
+      c = __ldcs(&r->yl);
+      d = __ldcs(&r->yu);
+    } else {
+      id = __ldcs(ids + i);
+      a = __ldcs(xl + i);
+      b = __ldcs(xu + i);
+      c = __ldcs(yl + i);
+      d = __ldcs(yu + i);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256, PBSM_PART_MINB) k_scatter(ScatterIn in, i64 n,
                                                  int kx, int ky, int row_lo, int row_hi,
                                                  const double* __restrict__ bx,
                                                  const double* __restrict__ by,
@@ -443,23 +632,11 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_scatter(const i64* __re
   i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   double pa = 0, pb = 0, pc = 0, pd = 0;
   i64 pid = 0;
-  if (i < n) {  // software pipeline: the next rectangle's loads in flight
-    pa = __ldcs(xl + i);
-    pb = __ldcs(xu + i);
-    pc = __ldcs(yl + i);
-    pd = __ldcs(yu + i);
-    pid = __ldcs(ids + i);
-  }
+  if (i < n) in.load(i, pa, pb, pc, pd, pid);  // software pipeline: next rectangle in flight
   for (; i < n; i += stride) {
     const double a = pa, b = pb, c = pc, d = pd;
     const i64 id = pid;
-    if (i + stride < n) {
-      pa = __ldcs(xl + i + stride);
-      pb = __ldcs(xu + i + stride);
-      pc = __ldcs(yl + i + stride);
-      pd = __ldcs(yu + i + stride);
-      pid = __ldcs(ids + i + stride);
-    }
+    if (i + stride < n) in.load(i + stride, pa, pb, pc, pd, pid);
     const int c0 = tile_of(a, kx, bx);
     const int c1 = tile_of(b, kx, bx);
     const int rr0 = tile_of(c, ky, by);
@@ -639,7 +816,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
   if (threadIdx.x < kNV) {
     u64 s = 0;
     for (int w = 0; w < kPlanThreads / 32; ++w) s += sh[w][threadIdx.x];
-    partials[(u64)blockIdx.x * kNTot + threadIdx.x] = s;
+    partials[(u64)threadIdx.x * (gridDim.x + 1) + blockIdx.x] = s;
   }
   if (threadIdx.x == 0) {
     u32 m = 0;
@@ -654,8 +831,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
 }
 
 // single CTA, one warp per lane: exclusive scan of the per-CTA partial sums
-// (loads issued kBatch steps ahead), totals → header and into the extra row
-// nb of `partials` (read by k_plan_apply)
+// (lane-major, so a warp's loads and stores are coalesced; loads issued
+// kBatch steps ahead), totals → header and after each lane's row (read by
+// k_plan_apply)
 __global__ void __launch_bounds__(kNV * 32) k_plan_partials(u64* __restrict__ partials, u64 nb,
                                                              pbsm_header* hdr, u32* je_n,
                                                              u32* je_s, u32* lpre) {
@@ -668,13 +846,13 @@ __global__ void __launch_bounds__(kNV * 32) k_plan_partials(u64* __restrict__ pa
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
       const u64 i = b0 + u * 32 + lane;
-      v[u] = i < nb ? partials[i * kNTot + q] : 0ull;
+      v[u] = i < nb ? partials[(u64)q * (nb + 1) + i] : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
       const u64 i = b0 + u * 32 + lane;
       const u64 inc = warp_incl_scan<u64>(v[u]);
-      if (i < nb) partials[i * kNTot + q] = carry + inc - v[u];
+      if (i < nb) partials[(u64)q * (nb + 1) + i] = carry + inc - v[u];
       carry += __shfl_sync(0xffffffffu, inc, 31);
     }
   }
@@ -684,7 +862,7 @@ __global__ void __launch_bounds__(kNV * 32) k_plan_partials(u64* __restrict__ pa
     u64 c[kNV];
     for (int qq = 0; qq < kNV; ++qq) {
       c[qq] = tot[qq];
-      partials[nb * kNTot + qq] = c[qq];
+      partials[(u64)qq * (nb + 1) + nb] = c[qq];
     }
     hdr->a_r = (i64)c[L_A];
     hdr->a_s = (i64)c[L_B];
@@ -749,11 +927,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ c
     block_excl_scan_multi<kPlanThreads, kNV, u32>(pre, tot, shs);
   }
   // global prefixes = this CTA's partial + the u32 in-CTA prefix
-  const u64* part = partials + (u64)blockIdx.x * kNTot;
-  const u64* tot = partials + nb * kNTot;
-  u64 g[kNV];
+  // lane-major partials: lane q of CTA b at q * (nb + 1) + b, totals at q * (nb + 1) + nb
+  u64 tot[kNV], g[kNV];
 #pragma unroll
-  for (int q = 0; q < kNV; ++q) g[q] = part[q] + pre[q];
+  for (int q = 0; q < kNV; ++q) {
+    tot[q] = partials[(u64)q * (nb + 1) + nb];
+    g[q] = partials[(u64)q * (nb + 1) + blockIdx.x] + pre[q];
+  }
   // region bases: [nested | sorted | large] in each input's list
   const u64 rs_base = tot[L_NA], ss_base = tot[L_NB];
   const u64 rl_base = tot[L_NA] + tot[L_SA], sl_base = tot[L_NB] + tot[L_SB];
@@ -1273,6 +1453,8 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
 // however small and lopsided the tiles are, and the hits of a warp-step are
 // compacted with a ballot + popcount into consecutive output slots (one
 // coalesced 16-byte store per hit).
+constexpr int kHitSteps = 32;  // warp-steps per warp whose hit ballots are kept
+
 #ifndef PBSM_NESTED_BUFS
 #define PBSM_NESTED_BUFS 1   // 2 = persistent CTAs with a double-buffered chunk pipeline
 #endif
@@ -1287,6 +1469,7 @@ struct NestedSmem {
   float tInvS[kMaxTiles];        // 1 / |S_T|
   u64 wtot[kJoinThreads / 32 + 1];
   u64 scan[kJoinThreads / 32 + 1];
+  u32 hits[kJoinThreads / 32][kHitSteps];  // pass-1 ballots, replayed by pass 2
   u64 bar[kNestedBufs];
   u64 base;
   int nt[kNestedBufs], NR[kNestedBufs], NS[kNestedBufs];
@@ -1415,15 +1598,18 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const JoinArgs& A, i
   const u32 per = ((NP + kW - 1) / kW + 31u) & ~31u;
   const u32 q_beg = min(NP, (u32)warp * per), q_end = min(NP, q_beg + per);
   const int lt_beg = q_beg < NP ? nested_tile_of(S, nt, q_beg) : 0;
-  // pass 1: count
+  // pass 1: count (and keep each warp-step's hit ballot for pass 2)
   u32 wcnt = 0;
   int lt = lt_beg;
-  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
+  int step = 0;
+  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u, ++step) {
     while (q0 >= S.tP[lt + 1]) ++lt;  // warp-uniform
     int pr, ps;
     const bool hit = q0 + lane < q_end && nested_pair(S, nt, q0 + lane, lt, pr, ps) &&
                      nested_hit(S, pr, ps);
-    wcnt += __popc(__ballot_sync(0xffffffffu, hit));
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (step < kHitSteps && lane == 0) S.hits[warp][step] = m;
+    wcnt += __popc(m);
   }
   if (lane == 0) S.wtot[warp] = wcnt;
   __syncthreads();
@@ -1447,15 +1633,27 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const JoinArgs& A, i
   if (!EMIT) return;
   __syncthreads();
   if (S.base == ~0ull) return;
-  // pass 2: emit, ballot-compacted (same slices, same order)
+  // pass 2: emit, ballot-compacted (same slices, same order); for the first
+  // kHitSteps steps the recorded ballot says which lanes hit, so only those
+  // map their pair and nothing is tested twice
   i64* out = A.pairs + 2 * (i64)(S.base + S.wtot[warp]);
   lt = lt_beg;
-  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
+  step = 0;
+  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u, ++step) {
     while (q0 >= S.tP[lt + 1]) ++lt;
     int pr = 0, ps = 0;
-    const bool hit = q0 + lane < q_end && nested_pair(S, nt, q0 + lane, lt, pr, ps) &&
-                     nested_hit(S, pr, ps);
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    unsigned m;
+    bool hit;
+    if (step < kHitSteps) {
+      m = S.hits[warp][step];
+      if (m == 0u) continue;
+      hit = (m >> lane) & 1u;
+      if (hit) nested_pair(S, nt, q0 + lane, lt, pr, ps);
+    } else {
+      hit = q0 + lane < q_end && nested_pair(S, nt, q0 + lane, lt, pr, ps) &&
+            nested_hit(S, pr, ps);
+      m = __ballot_sync(0xffffffffu, hit);
+    }
     if (hit) {
       const i64 o = __popc(m & lt_mask);
       *reinterpret_cast<longlong2*>(out + 2 * o) =
@@ -1587,6 +1785,12 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// grid of the count and bin passes (the same n → the same block ranges)
+unsigned part_blocks(i64 n) {
+  return (unsigned)std::max<i64>(1, std::min<i64>((n + 1023) / 1024,
+                                                  std::min<i64>(kMaxPartBlocks, num_sms() * 8)));
 }
 
 struct ScanLayout {
@@ -1730,12 +1934,10 @@ int pbsm_count(const double* xl, const double* xu, const double* yl, const doubl
   if (n == 0) return 0;
   if (!xl || !xu || !yl || !yu) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const i64 per_block = 256 * kRectsPerThread;
-  const i64 blocks = std::min<i64>((n + per_block - 1) / per_block, (i64)num_sms() * 8);
-  k_count<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(xl, xu, yl, yu, n, kx, ky, row_lo,
-                                                           row_hi, w.bx, w.by,
-                                                           side ? w.cnt_s : w.cnt_r, side,
-                                                           w.hdr);
+  k_count<<<part_blocks(n), 256, 0, as_stream(stream)>>>(xl, xu, yl, yu, n, kx, ky, row_lo,
+                                                         row_hi, w.bx, w.by,
+                                                         side ? w.cnt_s : w.cnt_r, side,
+                                                         w.bc[side], w.hdr);
   return launch_status();
 }
 
@@ -1775,6 +1977,20 @@ int pbsm_read_header(void* ws, pbsm_header* out, void* stream) {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
+static int scatter_impl(const int64_t* ids, const double* xl, const double* xu,
+                        const double* yl, const double* yu, const void* band, int64_t n,
+                        int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
+                        int32_t row_hi, pbsm_entry* out, int64_t capacity, void* stream) {
+  Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
+  const i64 per_block = 256 * kRectsPerThread;
+  const i64 blocks = std::min<i64>((n + per_block - 1) / per_block, (i64)num_sms() * 8);
+  ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band)};
+  k_scatter<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+      in, n, kx, ky, row_lo, row_hi, w.bx, w.by, side ? w.cur_s : w.cur_r,
+      reinterpret_cast<Rec*>(out), capacity, w.hdr);
+  return launch_status();
+}
+
 int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu, const double* yl,
                  const double* yu, int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky,
                  int32_t row_lo, int32_t row_hi, pbsm_entry* out, int64_t capacity,
@@ -1784,12 +2000,39 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu, const d
     return PBSM_E_ARG;
   if (n == 0) return 0;
   if (!ids || !xl || !xu || !yl || !yu || (!out && capacity > 0)) return PBSM_E_ARG;
+  return scatter_impl(ids, xl, xu, yl, yu, nullptr, n, side, ws, kx, ky, row_lo, row_hi, out,
+                      capacity, stream);
+}
+
+int pbsm_scatter_banded(const void* band, int64_t n, int32_t side, void* ws, int32_t kx,
+                        int32_t ky, int32_t row_lo, int32_t row_hi, pbsm_entry* out,
+                        int64_t capacity, void* stream) {
+  if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1) ||
+      capacity < 0)
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!band || (!out && capacity > 0)) return PBSM_E_ARG;
+  return scatter_impl(nullptr, nullptr, nullptr, nullptr, nullptr, band, n, side, ws, kx, ky,
+                      row_lo, row_hi, out, capacity, stream);
+}
+
+int pbsm_bin(const int64_t* ids, const double* xl, const double* xu, const double* yl,
+             const double* yu, int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky,
+             int32_t row_lo, int32_t row_hi, void* band, void* stream) {
+  if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1))
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!ids || !xl || !xu || !yl || !yu || !band) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const i64 per_block = 256 * kRectsPerThread;
-  const i64 blocks = std::min<i64>((n + per_block - 1) / per_block, (i64)num_sms() * 8);
-  k_scatter<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
-      (const i64*)ids, xl, xu, yl, yu, n, kx, ky, row_lo, row_hi, w.bx, w.by,
-      side ? w.cur_s : w.cur_r, reinterpret_cast<Rec*>(out), capacity, w.hdr);
+  cudaStream_t s = as_stream(stream);
+  const unsigned nb = part_blocks(n);
+  const u64 m = (u64)kBinSlots * nb;
+  const u64 sb = (m + kScanTile - 1) / kScanTile;
+  k_scan_reduce<<<(unsigned)sb, kScanThreads, 0, s>>>(w.bc[side], m, w.bscan);
+  k_scan_partials<<<1, 1024, 0, s>>>(w.bscan, sb, w.bo, m);
+  k_scan_apply<<<(unsigned)sb, kScanThreads, 0, s>>>(w.bc[side], m, w.bscan, w.bo);
+  k_bin_copy<<<nb, 256, 0, s>>>((const i64*)ids, xl, xu, yl, yu, n, ky, row_lo, row_hi, w.by,
+                                w.bo, reinterpret_cast<BRec*>(band));
   return launch_status();
 }
 

@@ -15,6 +15,7 @@ count-then-emit writer).  Everything else is enqueued on one CUDA stream.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -140,16 +141,33 @@ def pair_capacity(h) -> int:
     return int(min(h.pair_bound, 2 * (h.list_r + h.list_s) + (1 << 20)))
 
 
+# tile lists (64 B per entry) above this size are scattered through the
+# row-band copy (pbsm_bin): measured on B200, random record writes over a
+# multi-GB list run at ~1 TB/s, within an L2-sized window at ~4 TB/s
+BIN_LIST_BYTES = int(os.environ.get("PBSM_BIN_BYTES", 1 << 30))
+
+
+def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream) -> torch.Tensor:
+    """Row-band copy of one input: n 40-byte records {id, xl, xu, yl, yu}."""
+    band = torch.empty((len(b), 5), dtype=torch.int64, device=b.device)
+    _native.check(lib.pbsm_bin(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu),
+                               len(b), side, wsp, *grid, band.data_ptr(), stream), "pbsm_bin")
+    return band
+
+
 def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool = True,
              row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
              keep_counts: bool = False, probe: PhaseProbe | None = None,
-             ordered: bool = False, nested_max: int = -1) -> DeviceJoinResult:
+             ordered: bool = False, nested_max: int = -1,
+             bin_bytes: int | None = None) -> DeviceJoinResult:
     """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
 
     ``probe`` (optional) gets an event after each library call, named after
     the phase that call ran: init, count, plan, header, scatter, join, header2.
     ``nested_max`` overrides the mini-join cost-model threshold (pbsm_plan);
-    ``ordered`` selects the deterministic look-back output order.
+    ``ordered`` selects the look-back (unit-major) output placement;
+    ``bin_bytes``: tile lists larger than this go through the row-band copy
+    (pbsm_bin) before the scatter (default BIN_LIST_BYTES; 0 = always).
     """
     mark = probe.mark if probe is not None else (lambda name: None)
     lib = _native.load()
@@ -182,13 +200,25 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     mark("header")
 
     lists = []
+    thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
     for side, b, total in ((0, r, h.list_r), (1, s, h.list_s)):
         ent = torch.empty((max(total, 1), 8), dtype=torch.int64, device=device)  # 64 B records
-        _native.check(lib.pbsm_scatter(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
-                                       _ptr(b.yu), len(b), side, wsp, *grid, ent.data_ptr(),
-                                       total, stream), "pbsm_scatter")
+        # the copy costs ~80 B per rectangle; it pays where the random record
+        # writes dominate: large lists and heavy replication (cfg4: 1.7
+        # entries per rectangle; cfg2/cfg3/cfg5: 1.1-1.5, measured slower)
+        if 64 * total > thresh and (bin_bytes == 0 or total >= 1.6 * len(b)):
+            band = _banded(lib, b, side, wsp, grid, stream)
+            mark("bin")
+            _native.check(lib.pbsm_scatter_banded(band.data_ptr(), len(b), side, wsp, *grid,
+                                                  ent.data_ptr(), total, stream),
+                          "pbsm_scatter_banded")
+            del band
+        else:
+            _native.check(lib.pbsm_scatter(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
+                                           _ptr(b.yu), len(b), side, wsp, *grid, ent.data_ptr(),
+                                           total, stream), "pbsm_scatter")
+        mark("scatter")
         lists.append(ent)
-    mark("scatter")
     if ev:
         ev[1].record()
 

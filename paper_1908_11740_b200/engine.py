@@ -100,6 +100,15 @@ def _resolve_policy(cfg: JoinConfig) -> str:
     return policy
 
 
+def _to_host(t: torch.Tensor) -> np.ndarray:
+    """Device → host into page-locked memory (torch's caching host allocator):
+    a fresh pageable buffer would page-fault on every 4 KiB of the copy.  The
+    returned array keeps its pinned tensor alive."""
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t)
+    return host.numpy()
+
+
 def _require_cuda() -> torch.device:
     if not torch.cuda.is_available():
         raise KernelError("no CUDA device: the B200 join has no CPU fallback")
@@ -141,7 +150,7 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
         count, pairs = refine(res.pairs)
     out = None
     if collect_user:
-        out = pairs.cpu().numpy() if count else np.empty((0, 2), dtype=np.int64)
+        out = _to_host(pairs) if count else np.empty((0, 2), dtype=np.int64)
     t = res.times
     return JoinReport(
         result_count=int(count), pairs=out,

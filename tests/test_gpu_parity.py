@@ -284,3 +284,33 @@ def test_device_tile_of_at_boundaries(golden):
         got = res.tile_counts[0].cpu().numpy().astype(np.int64)
         want = oracle.count_tiles(pts, "2d", k)
         assert np.array_equal(got, want), k
+
+
+@pytest.mark.parametrize("cfg", [1, 3, 4, 5])
+def test_binned_scatter_bit_exact(golden, cfg):
+    """The row-band copy before the scatter (forced on with bin_bytes=0)
+    changes nothing in the result."""
+    g = golden["configs"]
+    r, s, k = make_config(cfg, float(g[f"cfg{cfg}_scale"]))
+    rd = dev.to_device(r)
+    sd = rd if s is r else dev.to_device(s)
+    res = dev.run_join(rd, sd, k, k, bin_bytes=0)
+    assert res.count == int(g[f"cfg{cfg}_count"])
+    assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), g[f"cfg{cfg}_pairs"])
+
+
+def test_binned_scatter_strips(golden):
+    """Bands are over the strip's rows; rectangles outside the strip are kept
+    in the copy but produce no entries."""
+    from paper_1908_11740_b200 import parallel
+
+    g = golden["configs"]
+    r, s, k = make_config(2, float(g["cfg2_scale"]))
+    cuts = parallel.plan_strips(r, s, k, 3)
+    parts = []
+    for lo, hi in zip(cuts, cuts[1:]):
+        res = dev.run_join(dev.to_device(r), dev.to_device(s), k, k, row_lo=lo, row_hi=hi,
+                           bin_bytes=0)
+        parts.append(res.pairs.cpu().numpy())
+    got = oracle.sorted_pairs(np.concatenate(parts))
+    assert np.array_equal(got, g["cfg2_pairs"])
