@@ -80,6 +80,7 @@ constexpr int kNestedMax = PBSM_NESTED_MAX;  // nested strategy iff |R_T|*|S_T| 
 constexpr int kCap = kChunkB + kLmax;   // max entries staged per chunk CTA
 constexpr int kMaxTiles = kCap / 2;     // a join tile holds >= 2 entries
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
+constexpr int kLargeOther = 2048;         // other-side entries per large work item
 constexpr int kPad = 4;                 // SoA row padding (words): bank spread
 
 constexpr int kScanThreads = 256;
@@ -747,7 +748,7 @@ __device__ __forceinline__ int tile_kind(u32 a, u32 b, i64 nested_max) {
 
 __device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u32 v[kNV]) {
   const int kind = tile_kind(a, b, nm);
-  const u32 lead = a >= b ? a : b;
+  const u32 lead = a >= b ? a : b, other = a >= b ? b : a;
 #pragma unroll
   for (int q = 0; q < kNV; ++q) v[q] = 0;
   v[L_A] = a;
@@ -762,7 +763,7 @@ __device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u32 v[kNV]) {
     v[L_SB] = b;
   } else if (kind == kLarge) {
     v[L_LF] = 1;
-    v[L_LI] = (lead + kLargeLead - 1) / kLargeLead;
+    v[L_LI] = ((lead + kLargeLead - 1) / kLargeLead) * ((other + kLargeOther - 1) / kLargeOther);
     v[L_LA] = a;
     v[L_LB] = b;
   }
@@ -1354,9 +1355,9 @@ __device__ void join_sorted(ChunkSmem& S, const JoinArgs& A, i64 unit, int c) {
   for (int p = tid; p < N; p += kJoinThreads) out += 2 * (i64)sweep_one<true>(S, p, out);
 }
 
-// Large join tiles (|R_T|+|S_T| > kLmax): the larger side is split into work
-// items of kLargeLead entries, one per thread; the other side streams through
-// shared memory.  Every (lead, other) pair is tested with the full
+// Large join tiles (|R_T|+|S_T| > kLmax): work items of kLargeLead entries of
+// the larger side (one per thread) × kLargeOther entries of the other side,
+// which stream through shared memory.  Every (lead, other) pair is tested with the full
 // closed-interval predicate (intersects, geometry.py:59-61) and the class rule
 // (>= 1 x-in and >= 1 y-in ⇔ Eq. 1 owner tile).
 template <bool EMIT>
@@ -1399,7 +1400,12 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
   const Rec* L = lead_r ? A.rl + rec.x : A.sl + rec.y;
   const Rec* O = lead_r ? A.sl + rec.y : A.rl + rec.x;
   const u32 nl = lead_r ? nR : nS;
-  const u32 a = (u32)(item - (i64)A.lpre[lj]) * kLargeLead + tid;
+  // work item = (block of kLargeLead lead entries) × (block of kLargeOther
+  // other entries), so a huge tile spreads over many CTAs both ways
+  const u32 nob = (no + kLargeOther - 1) / kLargeOther;
+  const u32 li = (u32)(item - (i64)A.lpre[lj]);
+  const u32 a = (li / nob) * kLargeLead + tid;
+  const u32 o_beg = (li % nob) * kLargeOther, o_end = min(no, o_beg + kLargeOther);
   const bool have = a < nl;
   Half me;
   i64 my_id = 0;
@@ -1415,8 +1421,8 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
   i64* out = nullptr;
   bool ok = true;
   for (int pass = 0; pass < passes; ++pass) {
-    for (u32 ob = 0; ob < no; ob += kCap) {
-      const int n = (int)min((u32)kCap, no - ob);
+    for (u32 ob = o_beg; ob < o_end; ob += kCap) {
+      const int n = (int)min((u32)kCap, o_end - ob);
       __syncthreads();  // previous piece fully consumed
       if (tid == 0) {
         mbar_expect_tx(&S.bar, (u32)n * (u32)sizeof(Rec));
