@@ -8,21 +8,27 @@ data-path collective:
   per-row entry counts (|R|+|S| assignments) are balanced by a prefix sum;
 * ``strip_inputs`` — the rectangles a rank needs: those whose tile-row range
   [tile_of(yl), tile_of(yu)] meets the strip (host-side distribution, before
-  the timed window; a device all-to-all is SURVEY §8(f) rank 1);
+  the timed window) — or, when every rank starts from its own slice of the
+  inputs, ``distributed_join_slices``: a distributed strip plan (one
+  all_reduce of per-row counts) and a device all_to_all (``distribute``);
 * each rank runs the full pipeline restricted to its rows
   (``device.run_join(..., row_lo, row_hi)``); class labels use the GLOBAL
   tile_of, so a pair is emitted only in its global owner tile — no cross-rank
   duplicates, no candidate exchange;
 * ``exchange_counts`` — the one collective: an all_gather of each rank's
   {pair_count, A_R, A_S}; its exclusive prefix gives the rank's global pair
-  offset and the global result_count.
+  offset and the global result_count (SURVEY §8(e));
+* ``gather_pairs`` / ``canonical_pairs`` — the pair shards on one rank, in
+  lexicographic order when a canonical list is wanted.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["combine_counts", "exchange_counts", "plan_strips", "row_range", "strip_inputs"]
+__all__ = ["canonical_pairs", "combine_counts", "distribute", "distributed_join",
+           "distributed_join_slices", "exchange_counts", "gather_pairs", "plan_strips",
+           "plan_strips_distributed", "row_range", "strip_inputs"]
 
 
 def _tile_index(p: np.ndarray, k: int) -> np.ndarray:
@@ -61,16 +67,7 @@ def plan_strips(r, s, k: int, world: int) -> list[int]:
         raise ValueError(f"cannot split {k} tile rows over {world} ranks")
     w_r = _row_entries(r, k)
     w = w_r + (w_r if s is r else _row_entries(s, k))
-    cum = np.cumsum(w)
-    total = cum[-1]
-    cuts = [0]
-    for g in range(1, world):
-        c = int(np.searchsorted(cum, total * g / world, side="left")) + 1
-        c = max(c, cuts[-1] + 1)             # non-empty strips
-        c = min(c, k - (world - g))           # leave a row for each later strip
-        cuts.append(c)
-    cuts.append(k)
-    return cuts
+    return _cut_rows(w, k, world)
 
 
 def strip_inputs(b, k: int, row_lo: int, row_hi: int):
@@ -149,3 +146,160 @@ def distributed_join(r, s, k: int, device=None, collect: bool = True):
     res = dev.run_join(rd, sd, k, k, collect=collect, row_lo=lo, row_hi=hi)
     ex = exchange_counts(res.count, res.header["a_r"], res.header["a_s"], device=device)
     return res, ex
+
+
+# ---------------------------------------------------------------- §8(f) next
+def tile_rows_torch(yl, yu, k: int):
+    """Exact first/last tile row of torch float64 tensors (any device): the
+    same floor-then-nudge against the boundaries i/k as axis_tile_index
+    (geometry.py:87-106); torch's float64 mul/div are correctly rounded."""
+    import torch
+
+    bounds = torch.arange(k + 1, dtype=torch.float64, device=yl.device) / k
+
+    def idx(p):
+        i = torch.clamp((p * k).to(torch.int64), 0, k - 1)
+        while True:
+            down = (i > 0) & (p < bounds[i])
+            up = (i < k - 1) & (p >= bounds[torch.clamp(i + 1, max=k)])
+            if not bool((down | up).any()):
+                return i
+            i = i - down.to(torch.int64) + up.to(torch.int64)
+
+    return idx(yl), idx(yu)
+
+
+def distribute(cols, k: int, cuts, group=None):
+    """Device-side input distribution.
+
+    Every rank holds an arbitrary slice of one input as (ids, xl, xu, yl, yu)
+    tensors; afterwards every rank holds exactly the rectangles whose tile-row
+    range meets its strip [cuts[rank], cuts[rank+1]) — a rectangle spanning a
+    strip boundary goes to every strip it touches, as the strip join needs.
+    One all_to_all of the per-destination counts, one all_to_all_single per
+    column (NCCL over NVLink on GPUs, gloo on CPU ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    ids, xl, xu, yl, yu = cols
+    r0, r1 = tile_rows_torch(yl, yu, k)
+    c = torch.as_tensor(cuts, dtype=torch.int64, device=yl.device)
+    first = torch.searchsorted(c, r0, right=True) - 1   # strip of the first row
+    last = torch.searchsorted(c, r1, right=True) - 1
+    span = (last - first + 1)
+    # one copy per (rectangle, destination), grouped by destination rank
+    rep = torch.repeat_interleave(torch.arange(len(ids), device=yl.device), span)
+    dest = torch.repeat_interleave(first, span) + (
+        torch.arange(len(rep), device=yl.device) - torch.repeat_interleave(
+            torch.cumsum(span, 0) - span, span))
+    keep = c[dest] < c[dest + 1]            # skip empty strips in a span
+    rep, dest = rep[keep], dest[keep]
+    order = torch.argsort(dest, stable=True)
+    rep, dest = rep[order], dest[order]
+    send_counts = torch.bincount(dest, minlength=world)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    sc, rc = send_counts.tolist(), recv_counts.tolist()
+    out = []
+    for col in cols:
+        buf = torch.empty(sum(rc), dtype=col.dtype, device=col.device)
+        dist.all_to_all_single(buf, col[rep].contiguous(), rc, sc, group=group)
+        out.append(buf)
+    return tuple(out)
+
+
+def _cut_rows(w, k: int, world: int) -> list[int]:
+    """The cut rule of plan_strips on a per-row entry vector."""
+    cum = np.cumsum(w)
+    total = cum[-1]
+    cuts = [0]
+    for g in range(1, world):
+        c = int(np.searchsorted(cum, total * g / world, side="left")) + 1
+        c = max(c, cuts[-1] + 1)             # non-empty strips
+        c = min(c, k - (world - g))           # leave a row for each later strip
+        cuts.append(c)
+    cuts.append(k)
+    return cuts
+
+
+def plan_strips_distributed(r_cols, s_cols, k: int, group=None) -> list[int]:
+    """plan_strips when every rank holds only a slice of R and S: per-row
+    entry counts of the local slices (torch, on the slices' device), one
+    all_reduce, then the same cut rule — every rank gets identical cuts."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if world <= 1:
+        return [0, k]
+    if world > k:
+        raise ValueError(f"cannot split {k} tile rows over {world} ranks")
+    dev = r_cols[0].device
+    d = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+    for cols in ((r_cols,) if s_cols is None else (r_cols, s_cols)):
+        _, xl, xu, yl, yu = cols
+        c0, c1 = tile_rows_torch(xl, xu, k)
+        r0, r1 = tile_rows_torch(yl, yu, k)
+        span = c1 - c0 + 1
+        d.scatter_add_(0, r0, span)
+        d.scatter_add_(0, r1 + 1, -span)
+    if s_cols is None:
+        d *= 2
+    dist.all_reduce(d, group=group)
+    w = torch.cumsum(d[:k], 0).cpu().numpy()
+    return _cut_rows(w, k, world)
+
+
+def distributed_join_slices(r_cols, s_cols, k: int, collect: bool = True, group=None):
+    """Strip-sharded join when each rank starts from an arbitrary slice of R
+    and S already on its GPU (e.g. its shard of a file): distributed strip
+    plan, device all_to_all of the inputs, local strip join, count exchange.
+    ``s_cols=None`` is a self-join.  Returns (DeviceJoinResult, exchange)."""
+    import torch.distributed as dist
+
+    from . import device as dev
+
+    rank = dist.get_rank(group)
+    cuts = plan_strips_distributed(r_cols, s_cols, k, group)
+    lo, hi = cuts[rank], cuts[rank + 1]
+    rd = dev.DeviceRects(*distribute(r_cols, k, cuts, group))
+    sd = rd if s_cols is None else dev.DeviceRects(*distribute(s_cols, k, cuts, group))
+    res = dev.run_join(rd, sd, k, k, collect=collect, row_lo=lo, row_hi=hi)
+    ex = exchange_counts(res.count, res.header["a_r"], res.header["a_s"],
+                         device=rd.device, group=group)
+    ex["cuts"] = cuts
+    return res, ex
+
+
+def gather_pairs(pairs, exchange: dict, dst: int = 0, group=None):
+    """Pair gather: the ranks' pair shards concatenated
+    on rank `dst` in rank order (each rank's shard starts at its global pair
+    offset).  Returns the (P, 2) tensor on `dst`, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    counts = exchange["per_rank_pairs"]
+    width = max(max(counts), 1)
+    padded = torch.zeros((width, 2), dtype=torch.int64, device=pairs.device)
+    padded[:len(pairs)] = pairs
+    bufs = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(bufs, padded, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([b[:n] for b, n in zip(bufs, counts)])
+
+
+def canonical_pairs(pairs):
+    """(r_id, s_id) pairs in lexicographic order (the parity form; the
+    reference's own list is unordered, engine.py:61-62) — two stable sorts."""
+    import torch
+
+    if len(pairs) == 0:
+        return pairs
+    o = torch.argsort(pairs[:, 1], stable=True)
+    p = pairs[o]
+    o = torch.argsort(p[:, 0], stable=True)
+    return p[o]

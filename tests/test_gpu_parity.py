@@ -314,3 +314,29 @@ def test_binned_scatter_strips(golden):
         parts.append(res.pairs.cpu().numpy())
     got = oracle.sorted_pairs(np.concatenate(parts))
     assert np.array_equal(got, g["cfg2_pairs"])
+
+
+def test_slice_distribution_nccl_single_rank(golden):
+    """distributed_join_slices through NCCL (world 1: the all_reduce / all_to_all
+    / all_gather run on the device with no peer to wait for) + gather_pairs +
+    canonical_pairs reproduce the reference list; the input routing itself is
+    covered at world 2 by the gloo test."""
+    import os
+
+    import torch.distributed as dist
+    from paper_1908_11740_b200 import parallel
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29631")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = golden["configs"]
+        r, s, k = make_config(2, float(g["cfg2_scale"]))
+        cols = lambda b: tuple(torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in b)
+        res, ex = parallel.distributed_join_slices(cols(r), cols(s), k)
+        assert ex["pairs"] == int(g["cfg2_count"]) and ex["cuts"] == [0, k]
+        allp = parallel.gather_pairs(res.pairs, ex)
+        got = parallel.canonical_pairs(allp).cpu().numpy()
+        assert np.array_equal(got, g["cfg2_pairs"])
+    finally:
+        dist.destroy_process_group()

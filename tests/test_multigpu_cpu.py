@@ -96,3 +96,59 @@ def test_exchange_counts_gloo_two_ranks():
         res = dict(out)
     assert res[0] == (0, 12, 21, 41, 1.5)
     assert res[1] == (7, 12, 21, 41, 1.5)
+
+
+def _dist_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, s, k = make_config(1, 0.3)
+        cuts = parallel.plan_strips(r, s, k, world)
+        sl_r = tuple(torch.from_numpy(np.ascontiguousarray(a[rank::world])) for a in r)
+        sl_s = tuple(torch.from_numpy(np.ascontiguousarray(a[rank::world])) for a in s)
+        assert parallel.plan_strips_distributed(sl_r, sl_s, k) == cuts
+        lo, hi = cuts[rank], cuts[rank + 1]
+        got = {}
+        for name, b in (("r", r), ("s", s)):
+            # this rank's arbitrary input slice: every world-th rectangle
+            sl = tuple(torch.from_numpy(np.ascontiguousarray(a[rank::world])) for a in b)
+            mine = parallel.distribute(sl, k, cuts)
+            got[name] = mine[0].numpy()
+            want = parallel.strip_inputs(b, k, lo, hi)[0]
+            assert np.array_equal(np.sort(got[name]), np.sort(want)), (rank, name)
+        # strip join with the oracle, owner-row filter, then the pair gather
+        rr = parallel.strip_inputs(r, k, lo, hi)
+        ss = parallel.strip_inputs(s, k, lo, hi)
+        p = oracle.join(rr, ss, "2d", k)["pairs"]
+        own = parallel.owner_rows(r, s, p, k)
+        p = torch.from_numpy(p[(own >= lo) & (own < hi)])
+        ex = parallel.exchange_counts(len(p), 0, 0)
+        allp = parallel.gather_pairs(p, ex, dst=0)
+        if rank == 0:
+            full = oracle.sorted_pairs(oracle.join(r, s, "2d", k)["pairs"])
+            got_sorted = parallel.canonical_pairs(allp).numpy()
+            out[rank] = bool(np.array_equal(got_sorted, full))
+        else:
+            out[rank] = allp is None
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distribute_and_gather_gloo_two_ranks():
+    """Device-side input distribution (all_to_all) + pair gather, on 2 gloo
+    ranks: each rank ends with exactly its strip's rectangles, and rank 0
+    reassembles the reference pair list."""
+    world, port = 2, _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_dist_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    assert res == {0: True, 1: True}
+
+
+def test_tile_rows_torch_matches_host():
+    r, _, k = make_config(5, 0.02)
+    y0, y1 = parallel.tile_rows_torch(torch.from_numpy(r[3]), torch.from_numpy(r[4]), k)
+    h0, h1 = parallel.row_range(r, k)
+    assert np.array_equal(y0.numpy(), h0) and np.array_equal(y1.numpy(), h1)
