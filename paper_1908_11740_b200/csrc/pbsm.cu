@@ -96,6 +96,9 @@ constexpr int kScanTile = kScanThreads * kScanPer;
 #ifndef PBSM_EF_STORE
 #define PBSM_EF_STORE 0
 #endif
+#ifndef PBSM_DIAG
+#define PBSM_DIAG 0
+#endif
 #ifndef PBSM_PART_MINB
 #define PBSM_PART_MINB 4
 #endif
@@ -432,10 +435,17 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
     const int c1 = tile_of(b, kx, bx);
     const int r0 = max(tile_of(c, ky, by), row_lo);
     const int r1 = min(tile_of(d, ky, by), row_hi - 1);
+#if PBSM_DIAG != 2 && PBSM_DIAG != 3
     atomicAdd_block(&hist[band_of(r0, r1, row_lo, row_hi)], 1u);
+#endif
+#if PBSM_DIAG == 1 || PBSM_DIAG == 3
+    bad |= (u32)(c0 + c1 + r0 + r1) & 0x40000000u;
+    if (false) {
+#else
     if (c0 == c1 && r0 == r1) {
       atomicAdd(cnt + (size_t)(r0 - row_lo) * kx + c0, 1u);
     } else {
+#endif
       for (int row = r0; row <= r1; ++row) {
         u32* rowp = cnt + (size_t)(row - row_lo) * kx;
         for (int col = c0; col <= c1; ++col) atomicAdd(rowp + col, 1u);
@@ -831,40 +841,44 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
   }
 }
 
-// single CTA, one warp per lane: exclusive scan of the per-CTA partial sums
-// (lane-major, so a warp's loads and stores are coalesced; loads issued
-// kBatch steps ahead), totals → header and after each lane's row (read by
-// k_plan_apply)
-__global__ void __launch_bounds__(kNV * 32) k_plan_partials(u64* __restrict__ partials, u64 nb,
-                                                             pbsm_header* hdr, u32* je_n,
-                                                             u32* je_s, u32* lpre) {
-  constexpr int kBatch = 8;
-  __shared__ u64 tot[kNV];
-  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// one CTA per scan lane: exclusive scan of lane q's per-CTA partial sums (a
+// lane-major row, so loads and stores are coalesced; 4 consecutive values per
+// thread, 4096 per block-scan step).  The lane total goes after the row (read
+// by k_plan_apply); the last CTA to finish writes the header.
+constexpr int kPartThreads = 1024;
+__global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict__ partials, u64 nb,
+                                                                 pbsm_header* hdr, u32* je_n,
+                                                                 u32* je_s, u32* lpre) {
+  __shared__ u64 sh[kPartThreads / 32 + 1];
+  __shared__ bool last;
+  u64* row = partials + (u64)blockIdx.x * (nb + 1);
   u64 carry = 0;
-  for (u64 b0 = 0; b0 < nb; b0 += 32 * kBatch) {
-    u64 v[kBatch];
+  for (u64 base = 0; base < nb; base += 4 * kPartThreads) {
+    const u64 i0 = base + 4 * (u64)threadIdx.x;
+    u64 v[4];
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const u64 i = b0 + u * 32 + lane;
-      v[u] = i < nb ? partials[(u64)q * (nb + 1) + i] : 0ull;
-    }
+    for (int u = 0; u < 4; ++u) v[u] = i0 + u < nb ? row[i0 + u] : 0ull;
+    u64 tot;
+    u64 run = carry + block_excl_scan<kPartThreads>(v[0] + v[1] + v[2] + v[3], &tot, sh);
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const u64 i = b0 + u * 32 + lane;
-      const u64 inc = warp_incl_scan<u64>(v[u]);
-      if (i < nb) partials[(u64)q * (nb + 1) + i] = carry + inc - v[u];
-      carry += __shfl_sync(0xffffffffu, inc, 31);
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + u < nb) row[i0 + u] = run;
+      run += v[u];
     }
+    carry += tot;
   }
-  if (lane == 0) tot[q] = carry;
-  __syncthreads();
   if (threadIdx.x == 0) {
+    row[nb] = carry;
+    __threadfence();
+    last = atomicAdd(&hdr->pad, 1u) == (u32)(kNV - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  hdr->pad = 0;  // the lane counter, ready for the next plan
+  {
     u64 c[kNV];
-    for (int qq = 0; qq < kNV; ++qq) {
-      c[qq] = tot[qq];
-      partials[(u64)qq * (nb + 1) + nb] = c[qq];
-    }
+    for (int qq = 0; qq < kNV; ++qq) c[qq] = __ldcg(partials + (u64)qq * (nb + 1) + nb);
     hdr->a_r = (i64)c[L_A];
     hdr->a_s = (i64)c[L_B];
     hdr->n_nested = (i64)c[L_NF];
@@ -903,7 +917,14 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ c
   __shared__ u32 sa[kPlanTile];
   __shared__ u32 sb[kPlanTile];
   __shared__ u32 shs[kPlanThreads / 32][kNV];
+  __shared__ u64 shp[2][kNV];  // this CTA's global prefixes, the totals
   const u64 base = (u64)blockIdx.x * kPlanTile;
+  // lane-major partials: lane q of CTA b at q * (nb + 1) + b, totals at q * (nb + 1) + nb;
+  // fetched first so their latency overlaps the count loads
+  if (threadIdx.x < 2 * kNV) {
+    const int q = threadIdx.x % kNV;
+    shp[threadIdx.x / kNV][q] = partials[(u64)q * (nb + 1) + (threadIdx.x < kNV ? blockIdx.x : nb)];
+  }
   for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
     const u64 t = base + i;
     sa[i] = t < T ? cr[t] : 0u;
@@ -927,13 +948,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ c
     u32 tot[kNV];
     block_excl_scan_multi<kPlanThreads, kNV, u32>(pre, tot, shs);
   }
-  // global prefixes = this CTA's partial + the u32 in-CTA prefix
-  // lane-major partials: lane q of CTA b at q * (nb + 1) + b, totals at q * (nb + 1) + nb
+  // global prefixes = this CTA's partial + the u32 in-CTA prefix (the scan's
+  // barriers made shp visible)
   u64 tot[kNV], g[kNV];
 #pragma unroll
   for (int q = 0; q < kNV; ++q) {
-    tot[q] = partials[(u64)q * (nb + 1) + nb];
-    g[q] = partials[(u64)q * (nb + 1) + blockIdx.x] + pre[q];
+    tot[q] = shp[1][q];
+    g[q] = shp[0][q] + pre[q];
   }
   // region bases: [nested | sorted | large] in each input's list
   const u64 rs_base = tot[L_NA], ss_base = tot[L_NB];
@@ -1596,6 +1617,10 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const JoinArgs& A, i
     }
   }
   __syncthreads();
+#if PBSM_DIAG == 6
+  if (tid == 0 && S.f[0][N - 1] == 12345ull) atomicAdd(A.total, 1ull);
+  return;
+#endif
   const u32 NP = (u32)tot;
   const unsigned lt_mask = (1u << lane) - 1u;
   // each warp owns one contiguous slice of the pair index space, so the tile
@@ -1692,6 +1717,10 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64
     }
     __syncthreads();
     mbar_wait(&S.bar[0], 0);
+#if PBSM_DIAG == 5
+    if (tid == 0 && S.recs[0][0].id == -12345) atomicAdd(A.total, 1ull);
+    return;
+#endif
     nested_chunk<EMIT>(S, A, 0, c);
     return;
   }
@@ -1955,7 +1984,7 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
   const i64 nm = nested_max < 0 ? (i64)kNestedMax : (i64)nested_max;
   k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles, nm,
                                                               w.partials, w.hdr);
-  k_plan_partials<<<1, kNV * 32, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je[0], w.je[1], w.lpre);
+  k_plan_partials<<<kNV, kPartThreads, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je[0], w.je[1], w.lpre);
   PlanOut P;
   P.cur_r = w.cur_r;
   P.cur_s = w.cur_s;
