@@ -1480,147 +1480,134 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
 // however small and lopsided the tiles are, and the hits of a warp-step are
 // compacted with a ballot + popcount into consecutive output slots (one
 // coalesced 16-byte store per hit).
+//
+// Staging: per-thread 16-byte async copies (cp.async) land each 64-byte list
+// record directly in the layout the pair tests read — {xl|label, xu} and
+// {yl, yu} in two 16-byte arrays, the id in a third — so there is no
+// transpose pass, and 32 lanes reading 32 consecutive entries hit 512
+// contiguous bytes (4 wavefronts).  The pad words are never fetched.
 constexpr int kHitSteps = 32;  // warp-steps per warp whose hit ballots are kept
 
-#ifndef PBSM_NESTED_BUFS
-#define PBSM_NESTED_BUFS 1   // 2 = persistent CTAs with a double-buffered chunk pipeline
-#endif
-constexpr int kNestedBufs = PBSM_NESTED_BUFS;
+struct TileInfo {  // one 16-byte shared-memory read per pair test
+  u32 p0;          // first pair index of the tile
+  u32 rs0;         // chunk-local position of the tile's first R | first S << 16
+  u32 ns;          // |S_T|
+  float inv_ns;    // 1 / |S_T|
+};
 
 struct NestedSmem {
-  Rec recs[kNestedBufs][kCap];   // TMA: the chunk's R range, then its S range
-  uint4 jr[kNestedBufs][kMaxTiles];  // TMA: the chunk's tile records
-  u64 f[4][kCap + kPad];         // SoA copy of the MBR words (padded rows)
-  u32 tP[kMaxTiles + 1];         // pair-index prefix per tile
-  u16 tR0[kMaxTiles], tS0[kMaxTiles], tNS[kMaxTiles];
-  float tInvS[kMaxTiles];        // 1 / |S_T|
+  ulonglong2 ax[kCap];           // {xl | label, xu} per staged entry (R range, then S range)
+  double2 ay[kCap];              // {yl, yu}
+  longlong2 aid[kCap];           // {id, pad}
+  TileInfo ti[kMaxTiles];
+  u32 tb[kMaxTiles + 1];         // tile pair-prefix boundaries (tb[nt] = pair total)
   u64 wtot[kJoinThreads / 32 + 1];
   u64 scan[kJoinThreads / 32 + 1];
   u32 hits[kJoinThreads / 32][kHitSteps];  // pass-1 ballots, replayed by pass 2
-  u64 bar[kNestedBufs];
   u64 base;
-  int nt[kNestedBufs], NR[kNestedBufs], NS[kNestedBufs];
 };
 
-__device__ __forceinline__ void mbar_arrive(u64* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-// thread 0 only: start loading chunk c into buffer b; always completes one
-// phase of bar[b] (with or without data)
-__device__ __forceinline__ void nested_prefetch(NestedSmem& S, const JoinArgs& A, int b, i64 c,
-                                                i64 n_chunks) {
-  b = kNestedBufs == 1 ? 0 : b;
-  int nt = 0, NR = 0, NS = 0;
-  uint4 d0 = make_uint4(0, 0, 0, 0);
-  if (c < n_chunks) {
-    d0 = A.cdesc[0][c];
-    const uint4 d1 = A.cdesc[0][c + 1];
-    nt = (int)(d1.x - d0.x);
-    NR = (int)(d1.y - d0.y);
-    NS = (int)(d1.z - d0.z);
-    if (!(nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles)) {
-      atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);  // never by construction
-      nt = NR = NS = 0;
-    }
-  }
-  S.nt[b] = nt;
-  S.NR[b] = NR;
-  S.NS[b] = NS;
-  if (nt == 0) {
-    mbar_arrive(&S.bar[b]);
-    return;
-  }
-  // the buffer was last read through the generic proxy: order those reads
-  // before the async-proxy (TMA) writes
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  mbar_expect_tx(&S.bar[b], (u32)nt * 16u + (u32)(NR + NS) * (u32)sizeof(Rec));
-  bulk_g2s(&S.jr[b][0], A.jrec[0] + d0.x, (u32)nt * 16u, &S.bar[b]);
-  bulk_g2s(&S.recs[b][0], A.rl + d0.y, (u32)NR * (u32)sizeof(Rec), &S.bar[b]);
-  bulk_g2s(&S.recs[b][NR], A.sl + d0.z, (u32)NS * (u32)sizeof(Rec), &S.bar[b]);
-}
-
-// first tile of warp-step q0: binary search over the pair prefix (the same
+// first tile of pair q0: binary search over the boundaries (the same
 // addresses in every lane: broadcast reads)
 __device__ __forceinline__ int nested_tile_of(const NestedSmem& S, int nt, u32 q0) {
-  int lo = 0, hi = nt;  // last lt with tP[lt] <= q0
+  int lo = 0, hi = nt;  // last lt with tb[lt] <= q0
   while (hi - lo > 1) {
     const int m = (lo + hi) >> 1;
-    if (S.tP[m] <= q0) lo = m; else hi = m;
+    if (S.tb[m] <= q0) lo = m; else hi = m;
   }
   return lo;
 }
 
-// pair q of the chunk → (position of r, position of s), or false past the end;
-// lt enters as the tile of the warp-step's first pair
-__device__ __forceinline__ bool nested_pair(const NestedSmem& S, int nt, u32 q, int lt, int& pr,
-                                            int& ps) {
-  if (q >= S.tP[nt]) return false;
-  while (q >= S.tP[lt + 1]) ++lt;  // within a warp-step: a few tiles at most
-  const u32 local = q - S.tP[lt];
-  const u32 nS = S.tNS[lt];
-  // local / nS: local < 2^16 and |local/nS - integer| >= 0.5/nS, so the
-  // float estimate of (local + 0.5) / nS truncates to the exact quotient
-  const u32 r = (u32)__float2int_rz(((float)local + 0.5f) * S.tInvS[lt]);
-  pr = S.tR0[lt] + (int)r;
-  ps = S.tS0[lt] + (int)(local - r * nS);
-  return true;
+// Tiles of one warp-step: lane j reads boundary tb[lt + 1 + j]; the in-step
+// boundaries (at most 31: tiles hold >= 1 pair and tb[lt] <= q0) become a
+// position bitmask, and lane L's tile is lt + (boundaries at positions <= L).
+// Returns lane's tile; advances lt to the tile of the step's last pair.
+__device__ __forceinline__ int nested_step_tile(const NestedSmem& S, int nt, u32 q0, int& lt,
+                                                int lane) {
+  const int j = lt + 1 + lane;
+  const u32 d = (j <= nt ? S.tb[j] : 0xffffffffu) - q0;
+  const unsigned bits = __reduce_or_sync(0xffffffffu, d < 32u ? (1u << d) : 0u);
+  const int mine = lt + __popc(bits & (0xffffffffu >> (31 - lane)));
+  lt += __popc(bits);
+  return mine;
+}
+
+// pair q (in tile t) → chunk-local positions of its r and s entries
+__device__ __forceinline__ void nested_pair(const NestedSmem& S, int t, u32 q, int& pr, int& ps) {
+  const TileInfo ti = S.ti[t];
+  const u32 local = q - ti.p0;
+  // local / ns: local < 2^16 and |local/ns - integer| >= 0.5/ns, so the
+  // float estimate of (local + 0.5) / ns truncates to the exact quotient
+  const u32 r = (u32)__float2int_rz(((float)local + 0.5f) * ti.inv_ns);
+  pr = (int)(ti.rs0 & 0xffffu) + (int)r;
+  ps = (int)(ti.rs0 >> 16) + (int)(local - r * ti.ns);
 }
 
 __device__ __forceinline__ bool nested_hit(const NestedSmem& S, int pr, int ps) {
-  const double rxu = __longlong_as_double((long long)S.f[1][pr]);
-  const double ryl = __longlong_as_double((long long)S.f[2][pr]);
-  const double ryu = __longlong_as_double((long long)S.f[3][pr]);
-  const double sxu = __longlong_as_double((long long)S.f[1][ps]);
-  const double syl = __longlong_as_double((long long)S.f[2][ps]);
-  const double syu = __longlong_as_double((long long)S.f[3][ps]);
-  return pair_ok(S.f[0][pr], rxu, ryl, ryu, S.f[0][ps], sxu, syl, syu);
+  const ulonglong2 rx = S.ax[pr], sx = S.ax[ps];
+  const double2 ry = S.ay[pr], sy = S.ay[ps];
+  return pair_ok(rx.x, __longlong_as_double((long long)rx.y), ry.x, ry.y, sx.x,
+                 __longlong_as_double((long long)sx.y), sy.x, sy.y);
 }
 
-// One chunk from buffer b (staged and waited for by the caller).
+// One CTA per chunk.  (A persistent double-buffered form was measured slower
+// on B200: more resident CTAs beat a deeper load pipeline here.)
 template <bool EMIT>
-__device__ __forceinline__ void nested_chunk(NestedSmem& S, const JoinArgs& A, int b, i64 c) {
+__global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64 n_chunks) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nt = S.nt[b], NR = S.NR[b], N = S.NR[b] + S.NS[b];
-  // tile table + pair prefix (nt <= kMaxTiles <= 2 * kJoinThreads)
-  static_assert(kMaxTiles <= 2 * kJoinThreads, "two tiles per thread");
-  u32 np = 0;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int lt = 2 * tid + h;
-    if (lt < nt) {
-      const uint4 r = S.jr[b][lt], r0 = S.jr[b][0];
-      S.tR0[lt] = (u16)(r.x - r0.x);
-      S.tS0[lt] = (u16)(NR + (int)(r.y - r0.y));
-      S.tNS[lt] = (u16)r.w;
-      S.tInvS[lt] = 1.0f / (float)r.w;
-      np += r.z * r.w;
-    }
+  __shared__ int s_unit;
+  if (A.ordered) {  // the look-back needs units handed out in launch order
+    if (tid == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
+    __syncthreads();
   }
+  const i64 c = A.ordered ? s_unit : blockIdx.x;
+  // chunk descriptor (broadcast loads): tiles [d0.x, d1.x), R entries
+  // [d0.y, d1.y), S entries [d0.z, d1.z)
+  const uint4 d0 = A.cdesc[0][c], d1 = A.cdesc[0][c + 1];
+  int nt = (int)(d1.x - d0.x), NR = (int)(d1.y - d0.y), NS = (int)(d1.z - d0.z);
+  if (!(nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles)) {
+    // never by construction (k_chunks); flag it and contribute 0 pairs (no
+    // early return: the ordered look-back chain must still be fed)
+    if (tid == 0) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
+    nt = NR = NS = 0;
+  }
+  const int N = NR + NS;
+  // async staging of the chunk's entries (coords + id; the pad is skipped)
+  for (int e = tid; e < N; e += kJoinThreads) {
+    const Rec* src = e < NR ? A.rl + d0.y + e : A.sl + d0.z + (e - NR);
+    const unsigned char* g = reinterpret_cast<const unsigned char*>(src);
+    cp_async16(&S.ax[e], g);
+    cp_async16(&S.ay[e], g + 16);
+    cp_async16(&S.aid[e], g + 32);
+  }
+  // meanwhile: the tile table from the tile records (one tile per thread)
+  static_assert(kMaxTiles <= kJoinThreads, "one tile per thread");
+  uint4 tr = make_uint4(0, 0, 0, 0);
+  if (tid < nt) tr = A.jrec[0][d0.x + tid];
   u64 tot;
-  u32 pre = (u32)block_excl_scan<kJoinThreads>((u64)np, &tot, S.scan);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int lt = 2 * tid + h;
-    if (lt < nt) {
-      S.tP[lt] = pre;
-      pre += S.jr[b][lt].z * S.jr[b][lt].w;
-    }
+  const u32 pre = (u32)block_excl_scan<kJoinThreads>((u64)tr.z * tr.w, &tot, S.scan);
+  if (tid < nt) {
+    TileInfo t;
+    t.p0 = pre;
+    t.rs0 = (tr.x - d0.y) | ((u32)(NR + (int)(tr.y - d0.z)) << 16);
+    t.ns = tr.w;
+    t.inv_ns = 1.0f / (float)tr.w;
+    S.ti[tid] = t;
+    S.tb[tid] = pre;
   }
-  if (tid == 0) S.tP[nt] = (u32)tot;
-  // SoA transpose, conflict-free: a warp reads 4 whole records per step
-  {
-    const u64* words = reinterpret_cast<const u64*>(S.recs[b]);
-    for (int r0 = warp * 4; r0 < N; r0 += 4 * (kJoinThreads / 32)) {
-      const int r = r0 + (lane >> 3), word = lane & 7;
-      if (r < N && word < 4) S.f[word][r] = words[r * 8 + word];
-    }
-  }
+  if (tid == 0) S.tb[nt] = (u32)tot;
+  cp_async_wait_all();
   __syncthreads();
-#if PBSM_DIAG == 6
-  if (tid == 0 && S.f[0][N - 1] == 12345ull) atomicAdd(A.total, 1ull);
-  return;
-#endif
   const u32 NP = (u32)tot;
   const unsigned lt_mask = (1u << lane) - 1u;
   // each warp owns one contiguous slice of the pair index space, so the tile
@@ -1634,10 +1621,14 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const JoinArgs& A, i
   int lt = lt_beg;
   int step = 0;
   for (u32 q0 = q_beg; q0 < q_end; q0 += 32u, ++step) {
-    while (q0 >= S.tP[lt + 1]) ++lt;  // warp-uniform
-    int pr, ps;
-    const bool hit = q0 + lane < q_end && nested_pair(S, nt, q0 + lane, lt, pr, ps) &&
-                     nested_hit(S, pr, ps);
+    const u32 q = q0 + lane;
+    const int t = nested_step_tile(S, nt, q0, lt, lane);
+    bool hit = false;
+    if (q < q_end) {
+      int pr, ps;
+      nested_pair(S, t, q, pr, ps);
+      hit = nested_hit(S, pr, ps);
+    }
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (step < kHitSteps && lane == 0) S.hits[warp][step] = m;
     wcnt += __popc(m);
@@ -1671,72 +1662,28 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const JoinArgs& A, i
   lt = lt_beg;
   step = 0;
   for (u32 q0 = q_beg; q0 < q_end; q0 += 32u, ++step) {
-    while (q0 >= S.tP[lt + 1]) ++lt;
+    const u32 q = q0 + lane;
+    const int t = nested_step_tile(S, nt, q0, lt, lane);
     int pr = 0, ps = 0;
     unsigned m;
     bool hit;
     if (step < kHitSteps) {
       m = S.hits[warp][step];
-      if (m == 0u) continue;
       hit = (m >> lane) & 1u;
-      if (hit) nested_pair(S, nt, q0 + lane, lt, pr, ps);
+      if (hit) nested_pair(S, t, q, pr, ps);
     } else {
-      hit = q0 + lane < q_end && nested_pair(S, nt, q0 + lane, lt, pr, ps) &&
-            nested_hit(S, pr, ps);
+      hit = false;
+      if (q < q_end) {
+        nested_pair(S, t, q, pr, ps);
+        hit = nested_hit(S, pr, ps);
+      }
       m = __ballot_sync(0xffffffffu, hit);
     }
     if (hit) {
       const i64 o = __popc(m & lt_mask);
-      *reinterpret_cast<longlong2*>(out + 2 * o) =
-          make_longlong2(S.recs[b][pr].id, S.recs[b][ps].id);
+      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(S.aid[pr].x, S.aid[ps].x);
     }
     out += 2 * (i64)__popc(m);
-  }
-}
-
-// One CTA per chunk (default), or with PBSM_NESTED_BUFS=2 persistent CTAs
-// walking chunks c = blockIdx.x + i * gridDim.x while the TMA engine fills the
-// other buffer with chunk i+1.  Measured on B200 the single-buffer form wins:
-// the per-chunk cost is dominated by the in-CTA barriers and scans, so more
-// resident CTAs beat a deeper load pipeline.
-template <bool EMIT>
-__global__ void __launch_bounds__(kJoinThreads, 4) k_join_nested(JoinArgs A, i64 n_chunks) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
-  const int tid = threadIdx.x;
-  if (kNestedBufs == 1) {
-    __shared__ int s_unit;
-    if (A.ordered) {  // the look-back needs units handed out in launch order
-      if (tid == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
-      __syncthreads();
-    }
-    const i64 c = A.ordered ? s_unit : blockIdx.x;
-    if (tid == 0) {
-      mbar_init(&S.bar[0], 1);
-      nested_prefetch(S, A, 0, c, n_chunks);
-    }
-    __syncthreads();
-    mbar_wait(&S.bar[0], 0);
-#if PBSM_DIAG == 5
-    if (tid == 0 && S.recs[0][0].id == -12345) atomicAdd(A.total, 1ull);
-    return;
-#endif
-    nested_chunk<EMIT>(S, A, 0, c);
-    return;
-  }
-  if (tid == 0) {
-    for (int b = 0; b < kNestedBufs; ++b) mbar_init(&S.bar[b], 1);
-    nested_prefetch(S, A, 0, blockIdx.x, n_chunks);
-  }
-  for (i64 i = 0;; ++i) {
-    const i64 c = blockIdx.x + i * gridDim.x;
-    if (c >= n_chunks) break;
-    const int b = (int)(i & 1);
-    if (tid == 0) nested_prefetch(S, A, b ^ 1, c + gridDim.x, n_chunks);
-    __syncthreads();  // S.nt[b] & co (written by thread 0 an iteration ago) visible
-    mbar_wait(&S.bar[b], (u32)((i >> 1) & 1));
-    nested_chunk<EMIT>(S, A, b, c);
-    __syncthreads();  // buffer b and the chunk scratch free for reuse
   }
 }
 
@@ -1901,15 +1848,8 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.total = (unsigned long long*)&w.hdr->pairs;
   A.ordered = ordered ? 1 : 0;
   if (cn > 0) {
-    // persistent grid: at most the resident CTAs (the ordered look-back waits
-    // on chunks of other CTAs, so every CTA must be resident)
-    const void* fn = emit ? (const void*)k_join_nested<true> : (const void*)k_join_nested<false>;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads,
-                                                      sizeof(NestedSmem)) != cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-    const i64 grid = kNestedBufs == 1 ? cn : std::min<i64>(cn, (i64)per_sm * num_sms());
+    // one CTA per chunk (the ordered look-back takes tickets in launch order)
+    const i64 grid = cn;
     if (emit)
       k_join_nested<true><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
     else
