@@ -79,30 +79,28 @@ constexpr int kLmax = PBSM_LMAX;        // largest tile (|R_T|+|S_T|) staged by 
 constexpr int kNestedMax = PBSM_NESTED_MAX;  // nested strategy iff |R_T|*|S_T| <= this
 constexpr int kCap = kChunkB + kLmax;   // max entries staged per chunk CTA
 constexpr int kMaxTiles = kCap / 2;     // a join tile holds >= 2 entries
+#ifndef PBSM_CHUNK_BN
+#define PBSM_CHUNK_BN 384
+#endif
+constexpr int kChunkBN = PBSM_CHUNK_BN;  // bucket width of the nested chunks
+constexpr int kCapN = kChunkBN + kLmax;  // max entries of a nested chunk
+constexpr int kMaxTilesN = kCapN / 2;
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
 constexpr int kLargeOther = 2048;         // other-side entries per large work item
-constexpr int kPad = 4;                 // SoA row padding (words): bank spread
 
 constexpr int kScanThreads = 256;
 constexpr int kScanPer = 16;
 constexpr int kScanTile = kScanThreads * kScanPer;
 
-#ifndef PBSM_RPT
-#define PBSM_RPT 1
-#endif
 #ifndef PBSM_BIN_DIRECT
 #define PBSM_BIN_DIRECT 0
 #endif
 #ifndef PBSM_EF_STORE
 #define PBSM_EF_STORE 0
 #endif
-#ifndef PBSM_DIAG
-#define PBSM_DIAG 0
-#endif
 #ifndef PBSM_PART_MINB
 #define PBSM_PART_MINB 4
 #endif
-constexpr int kRectsPerThread = PBSM_RPT;  // ILP in the count / scatter passes
 constexpr int kBins = 256;                  // row bands of the binned scatter
 constexpr int kBinSlots = kBins + 1;        // + one slot for rectangles outside the strip
 constexpr int kMaxPartBlocks = 4096;        // grid cap of the count / bin passes
@@ -394,6 +392,20 @@ __device__ __forceinline__ void part_range(i64 n, i64& beg, i64& end) {
   end = min(n, beg + per);
 }
 
+
+// ---- cp.async (16/8-byte async global → shared copies)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __restrict__ xl,
                                                const double* __restrict__ xu,
                                                const double* __restrict__ yl,
@@ -435,17 +447,10 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
     const int c1 = tile_of(b, kx, bx);
     const int r0 = max(tile_of(c, ky, by), row_lo);
     const int r1 = min(tile_of(d, ky, by), row_hi - 1);
-#if PBSM_DIAG != 2 && PBSM_DIAG != 3
     atomicAdd_block(&hist[band_of(r0, r1, row_lo, row_hi)], 1u);
-#endif
-#if PBSM_DIAG == 1 || PBSM_DIAG == 3
-    bad |= (u32)(c0 + c1 + r0 + r1) & 0x40000000u;
-    if (false) {
-#else
     if (c0 == c1 && r0 == r1) {
       atomicAdd(cnt + (size_t)(r0 - row_lo) * kx + c0, 1u);
     } else {
-#endif
       for (int row = r0; row <= r1; ++row) {
         u32* rowp = cnt + (size_t)(row - row_lo) * kx;
         for (int col = c0; col <= c1; ++col) atomicAdd(rowp + col, 1u);
@@ -1016,10 +1021,11 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ c
 __global__ void k_chunks(const u32* __restrict__ je, const uint4* __restrict__ jrec,
                          uint4* __restrict__ cdesc, pbsm_header* hdr, int which) {
   const i64 nj = which ? hdr->n_sorted : hdr->n_nested;
+  const u32 B = which ? (u32)kChunkB : (u32)kChunkBN;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nj;
        j += (i64)gridDim.x * blockDim.x) {
-    const i64 c = je[j] / kChunkB;
-    const i64 cp = j == 0 ? -1 : (i64)(je[j - 1] / kChunkB);
+    const i64 c = je[j] / B;
+    const i64 cp = j == 0 ? -1 : (i64)(je[j - 1] / B);
     if (cp < c) {
       const uint4 r = jrec[j];
       for (i64 cc = cp + 1; cc <= c; ++cc) cdesc[cc] = make_uint4((u32)j, r.x, r.y, 0u);
@@ -1496,24 +1502,16 @@ struct TileInfo {  // one 16-byte shared-memory read per pair test
 };
 
 struct NestedSmem {
-  ulonglong2 ax[kCap];           // {xl | label, xu} per staged entry (R range, then S range)
-  double2 ay[kCap];              // {yl, yu}
-  longlong2 aid[kCap];           // {id, pad}
-  TileInfo ti[kMaxTiles];
-  u32 tb[kMaxTiles + 1];         // tile pair-prefix boundaries (tb[nt] = pair total)
+  ulonglong2 ax[kCapN];          // {xl | label, xu} per staged entry (R range, then S range)
+  double2 ay[kCapN];             // {yl, yu}
+  i64 aid[kCapN];                // id
+  TileInfo ti[kMaxTilesN];
+  u32 tb[kMaxTilesN + 1];        // tile pair-prefix boundaries (tb[nt] = pair total)
   u64 wtot[kJoinThreads / 32 + 1];
   u64 scan[kJoinThreads / 32 + 1];
   u32 hits[kJoinThreads / 32][kHitSteps];  // pass-1 ballots, replayed by pass 2
   u64 base;
 };
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
 
 // first tile of pair q0: binary search over the boundaries (the same
 // addresses in every lane: broadcast reads)
@@ -1575,7 +1573,7 @@ __global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64
   // [d0.y, d1.y), S entries [d0.z, d1.z)
   const uint4 d0 = A.cdesc[0][c], d1 = A.cdesc[0][c + 1];
   int nt = (int)(d1.x - d0.x), NR = (int)(d1.y - d0.y), NS = (int)(d1.z - d0.z);
-  if (!(nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles)) {
+  if (!(nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCapN && nt <= kMaxTilesN)) {
     // never by construction (k_chunks); flag it and contribute 0 pairs (no
     // early return: the ordered look-back chain must still be fed)
     if (tid == 0) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
@@ -1588,22 +1586,34 @@ __global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64
     const unsigned char* g = reinterpret_cast<const unsigned char*>(src);
     cp_async16(&S.ax[e], g);
     cp_async16(&S.ay[e], g + 16);
-    cp_async16(&S.aid[e], g + 32);
+    cp_async8(&S.aid[e], g + 32);
   }
-  // meanwhile: the tile table from the tile records (one tile per thread)
-  static_assert(kMaxTiles <= kJoinThreads, "one tile per thread");
-  uint4 tr = make_uint4(0, 0, 0, 0);
-  if (tid < nt) tr = A.jrec[0][d0.x + tid];
+  // meanwhile: the tile table from the tile records (kTPT consecutive tiles
+  // per thread)
+  constexpr int kTPT = (kMaxTilesN + kJoinThreads - 1) / kJoinThreads;
+  uint4 tr[kTPT];
+  u32 np = 0;
+#pragma unroll
+  for (int h = 0; h < kTPT; ++h) {
+    const int t = kTPT * tid + h;
+    tr[h] = t < nt ? A.jrec[0][d0.x + t] : make_uint4(0, 0, 0, 0);
+    np += tr[h].z * tr[h].w;
+  }
   u64 tot;
-  const u32 pre = (u32)block_excl_scan<kJoinThreads>((u64)tr.z * tr.w, &tot, S.scan);
-  if (tid < nt) {
-    TileInfo t;
-    t.p0 = pre;
-    t.rs0 = (tr.x - d0.y) | ((u32)(NR + (int)(tr.y - d0.z)) << 16);
-    t.ns = tr.w;
-    t.inv_ns = 1.0f / (float)tr.w;
-    S.ti[tid] = t;
-    S.tb[tid] = pre;
+  u32 pre = (u32)block_excl_scan<kJoinThreads>((u64)np, &tot, S.scan);
+#pragma unroll
+  for (int h = 0; h < kTPT; ++h) {
+    const int t = kTPT * tid + h;
+    if (t < nt) {
+      TileInfo ti;
+      ti.p0 = pre;
+      ti.rs0 = (tr[h].x - d0.y) | ((u32)(NR + (int)(tr[h].y - d0.z)) << 16);
+      ti.ns = tr[h].w;
+      ti.inv_ns = 1.0f / (float)tr[h].w;
+      S.ti[t] = ti;
+      S.tb[t] = pre;
+      pre += tr[h].z * tr[h].w;
+    }
   }
   if (tid == 0) S.tb[nt] = (u32)tot;
   cp_async_wait_all();
@@ -1681,7 +1691,7 @@ __global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64
     }
     if (hit) {
       const i64 o = __popc(m & lt_mask);
-      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(S.aid[pr].x, S.aid[ps].x);
+      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(S.aid[pr], S.aid[ps]);
     }
     out += 2 * (i64)__popc(m);
   }
@@ -1770,10 +1780,12 @@ int num_sms() {
 }
 
 // grid of the count and bin passes (the same n → the same block ranges)
+// grid of the count and bin passes (the same n → the same block ranges)
 unsigned part_blocks(i64 n) {
   return (unsigned)std::max<i64>(1, std::min<i64>((n + 1023) / 1024,
                                                   std::min<i64>(kMaxPartBlocks, num_sms() * 8)));
 }
+
 
 struct ScanLayout {
   size_t cnt, base, partials, total;
@@ -1880,7 +1892,7 @@ const char* pbsm_build_info(void) {
   return "pbsm sm_100a v3: count+validate / plan / scatter (64B records, join tiles only) / "
          "guard / TMA-staged mini-joins (nested | sort+forward-scan | large) with count->emit; "
          "B=" PBSM_STR(PBSM_CHUNK_B) " Lmax=" PBSM_STR(PBSM_LMAX) " nested<=" PBSM_STR(
-             PBSM_NESTED_MAX) " rpt=" PBSM_STR(PBSM_RPT);
+             PBSM_NESTED_MAX) "";
 }
 
 int64_t pbsm_workspace_bytes(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi) {
@@ -1957,8 +1969,7 @@ static int scatter_impl(const int64_t* ids, const double* xl, const double* xu,
                         int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
                         int32_t row_hi, pbsm_entry* out, int64_t capacity, void* stream) {
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const i64 per_block = 256 * kRectsPerThread;
-  const i64 blocks = std::min<i64>((n + per_block - 1) / per_block, (i64)num_sms() * 8);
+  const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * 8);
   ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band)};
   k_scatter<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       in, n, kx, ky, row_lo, row_hi, w.bx, w.by, side ? w.cur_s : w.cur_r,
