@@ -379,10 +379,14 @@ struct BRec {
 static_assert(sizeof(BRec) == 40, "band record");
 
 // band of a rectangle in the binned scatter: its first tile row inside the
-// strip, in kBins equal row bands; rectangles that miss the strip → kBins
+// strip, in kBins equal row bands; rectangles that miss the strip → kBins.
+// Any monotone map into [0, kBins) works as long as the count and bin passes
+// agree, so a float multiply replaces the 64-bit division (which cost ~10% of
+// k_count's instructions).
 __device__ __forceinline__ int band_of(int r0, int r1, int row_lo, int row_hi) {
   if (r0 > r1) return kBins;
-  return (int)(((i64)(r0 - row_lo) * kBins) / (row_hi - row_lo));
+  const float scale = (float)kBins / (float)(row_hi - row_lo);
+  return min((int)((float)(r0 - row_lo) * scale), kBins - 1);
 }
 
 // the contiguous input range of block b in the count and bin passes
@@ -448,8 +452,15 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
     const int r0 = max(tile_of(c, ky, by), row_lo);
     const int r1 = min(tile_of(d, ky, by), row_hi - 1);
     atomicAdd_block(&hist[band_of(r0, r1, row_lo, row_hi)], 1u);
-    if (c0 == c1 && r0 == r1) {
-      atomicAdd(cnt + (size_t)(r0 - row_lo) * kx + c0, 1u);
+    u32* t00 = cnt + (size_t)(r0 - row_lo) * kx + c0;
+    const int ec = c1 - c0, er = r1 - r0;  // extents - 1 (er < 0: outside the strip)
+    if ((ec | er) == 0) {
+      atomicAdd(t00, 1u);
+    } else if (ec <= 1 && er <= 1 && er >= 0) {  // 2 or 4 tiles, no loop
+      atomicAdd(t00, 1u);
+      if (ec) atomicAdd(t00 + 1, 1u);
+      if (er) atomicAdd(t00 + kx, 1u);
+      if (ec & er) atomicAdd(t00 + kx + 1, 1u);
     } else {
       for (int row = r0; row <= r1; ++row) {
         u32* rowp = cnt + (size_t)(row - row_lo) * kx;
