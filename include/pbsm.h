@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 3
+#define PBSM_ABI_VERSION 4
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -195,6 +195,15 @@ int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
  * pbsm_refine_result_offset(n_cand) of scratch. */
 int64_t pbsm_refine_scratch_bytes(int64_t n_cand);
 int64_t pbsm_refine_result_offset(int64_t n_cand);
+/* SJB1 dataset body (load_mbr_binary, io.py:113-141): n packed 40-byte
+ * little-endian records {id u64, x_l, y_l, x_u, y_u f64} at an 8-byte aligned
+ * device address → the RectBatch SoA columns (ids reinterpreted as int64,
+ * like .astype(np.int64)).  *bad (device u32) = 1 if any record has a lower
+ * bound above its upper bound (or a NaN), the check load_mbr_binary raises
+ * DatasetError for. */
+int pbsm_unpack_records(const void* records, int64_t n, int64_t* ids, double* xl, double* xu,
+                        double* yl, double* yu, uint32_t* bad, void* stream);
+
 int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const double* py,
                 const double* qx, const double* qy, const int64_t* p_ids, const int64_t* q_ids,
                 double eps_sq, void* scratch, int64_t* out, void* stream);

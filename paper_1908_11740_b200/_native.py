@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
@@ -29,7 +29,8 @@ EXPORTED = (
     "pbsm_count", "pbsm_plan", "pbsm_read_header", "pbsm_scatter", "pbsm_bin",
     "pbsm_scatter_banded",
     "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit",
-    "pbsm_refine_scratch_bytes", "pbsm_refine_result_offset", "pbsm_refine",
+    "pbsm_unpack_records", "pbsm_refine_scratch_bytes", "pbsm_refine_result_offset",
+    "pbsm_refine",
 )
 
 
@@ -79,6 +80,7 @@ _SIGNATURES = {
                                   _P]),
     "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P, _P,
                                  _I64, _I32, _P]),
+    "pbsm_unpack_records": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "pbsm_refine_scratch_bytes": (_I64, [_I64]),
     "pbsm_refine_result_offset": (_I64, [_I64]),
     "pbsm_refine": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),

@@ -406,6 +406,12 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem)
                : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -1512,10 +1518,20 @@ struct TileInfo {  // one 16-byte shared-memory read per pair test
   float inv_ns;    // 1 / |S_T|
 };
 
-struct NestedSmem {
+#ifndef PBSM_NESTED_PERSIST
+#define PBSM_NESTED_PERSIST 0  // 1: persistent CTAs staging chunk i+1 during chunk i (measured slower)
+#endif
+constexpr int kNestedBufs = PBSM_NESTED_PERSIST ? 2 : 1;
+
+struct NestedBuf {               // one staged chunk
   ulonglong2 ax[kCapN];          // {xl | label, xu} per staged entry (R range, then S range)
   double2 ay[kCapN];             // {yl, yu}
   i64 aid[kCapN];                // id
+  uint4 jr[kMaxTilesN];          // tile records {r_start, s_start, |R_T|, |S_T|}
+};
+
+struct NestedSmem {
+  NestedBuf buf[kNestedBufs];
   TileInfo ti[kMaxTilesN];
   u32 tb[kMaxTilesN + 1];        // tile pair-prefix boundaries (tb[nt] = pair total)
   u64 wtot[kJoinThreads / 32 + 1];
@@ -1560,54 +1576,65 @@ __device__ __forceinline__ void nested_pair(const NestedSmem& S, int t, u32 q, i
   ps = (int)(ti.rs0 >> 16) + (int)(local - r * ti.ns);
 }
 
-__device__ __forceinline__ bool nested_hit(const NestedSmem& S, int pr, int ps) {
-  const ulonglong2 rx = S.ax[pr], sx = S.ax[ps];
-  const double2 ry = S.ay[pr], sy = S.ay[ps];
+__device__ __forceinline__ bool nested_hit(const NestedBuf& B, int pr, int ps) {
+  const ulonglong2 rx = B.ax[pr], sx = B.ax[ps];
+  const double2 ry = B.ay[pr], sy = B.ay[ps];
   return pair_ok(rx.x, __longlong_as_double((long long)rx.y), ry.x, ry.y, sx.x,
                  __longlong_as_double((long long)sx.y), sy.x, sy.y);
 }
 
-// One CTA per chunk.  (A persistent double-buffered form was measured slower
-// on B200: more resident CTAs beat a deeper load pipeline here.)
-template <bool EMIT>
-__global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64 n_chunks) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ int s_unit;
-  if (A.ordered) {  // the look-back needs units handed out in launch order
-    if (tid == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
-    __syncthreads();
-  }
-  const i64 c = A.ordered ? s_unit : blockIdx.x;
-  // chunk descriptor (broadcast loads): tiles [d0.x, d1.x), R entries
-  // [d0.y, d1.y), S entries [d0.z, d1.z)
-  const uint4 d0 = A.cdesc[0][c], d1 = A.cdesc[0][c + 1];
-  int nt = (int)(d1.x - d0.x), NR = (int)(d1.y - d0.y), NS = (int)(d1.z - d0.z);
-  if (!(nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCapN && nt <= kMaxTilesN)) {
+// chunk c's ranges: tiles [d0.x, d0.x + nt), R entries from d0.y, S from d0.z
+struct NestedChunk {
+  uint4 d0;
+  int nt, NR, NS;
+};
+
+// all threads: the chunk descriptor (broadcast loads) and its plan check
+__device__ __forceinline__ NestedChunk nested_desc(const JoinArgs& A, i64 c) {
+  NestedChunk k;
+  k.d0 = A.cdesc[0][c];
+  const uint4 d1 = A.cdesc[0][c + 1];
+  k.nt = (int)(d1.x - k.d0.x);
+  k.NR = (int)(d1.y - k.d0.y);
+  k.NS = (int)(d1.z - k.d0.z);
+  if (!(k.nt > 0 && k.NR > 0 && k.NS > 0 && k.NR + k.NS <= kCapN && k.nt <= kMaxTilesN)) {
     // never by construction (k_chunks); flag it and contribute 0 pairs (no
     // early return: the ordered look-back chain must still be fed)
-    if (tid == 0) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
-    nt = NR = NS = 0;
+    if (threadIdx.x == 0) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
+    k.nt = k.NR = k.NS = 0;
   }
-  const int N = NR + NS;
-  // async staging of the chunk's entries (coords + id; the pad is skipped)
-  for (int e = tid; e < N; e += kJoinThreads) {
-    const Rec* src = e < NR ? A.rl + d0.y + e : A.sl + d0.z + (e - NR);
+  return k;
+}
+
+// all threads: async copies of the chunk's entries (coords + id; the pad is
+// skipped) and tile records into B
+__device__ __forceinline__ void nested_stage(NestedBuf& B, const JoinArgs& A,
+                                             const NestedChunk& k) {
+  const int N = k.NR + k.NS;
+  for (int e = threadIdx.x; e < N; e += kJoinThreads) {
+    const Rec* src = e < k.NR ? A.rl + k.d0.y + e : A.sl + k.d0.z + (e - k.NR);
     const unsigned char* g = reinterpret_cast<const unsigned char*>(src);
-    cp_async16(&S.ax[e], g);
-    cp_async16(&S.ay[e], g + 16);
-    cp_async8(&S.aid[e], g + 32);
+    cp_async16(&B.ax[e], g);
+    cp_async16(&B.ay[e], g + 16);
+    cp_async8(&B.aid[e], g + 32);
   }
-  // meanwhile: the tile table from the tile records (kTPT consecutive tiles
-  // per thread)
+  for (int t = threadIdx.x; t < k.nt; t += kJoinThreads) cp_async16(&B.jr[t], A.jrec[0] + k.d0.x + t);
+}
+
+// One staged chunk (B landed and visible): tile table, count, reserve, emit.
+template <bool EMIT>
+__device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
+                                             const JoinArgs& A, const NestedChunk& k, i64 c) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nt = k.nt, NR = k.NR;
+  // tile table (kTPT consecutive tiles per thread)
   constexpr int kTPT = (kMaxTilesN + kJoinThreads - 1) / kJoinThreads;
   uint4 tr[kTPT];
   u32 np = 0;
 #pragma unroll
   for (int h = 0; h < kTPT; ++h) {
     const int t = kTPT * tid + h;
-    tr[h] = t < nt ? A.jrec[0][d0.x + t] : make_uint4(0, 0, 0, 0);
+    tr[h] = t < nt ? B.jr[t] : make_uint4(0, 0, 0, 0);
     np += tr[h].z * tr[h].w;
   }
   u64 tot;
@@ -1618,7 +1645,7 @@ __global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64
     if (t < nt) {
       TileInfo ti;
       ti.p0 = pre;
-      ti.rs0 = (tr[h].x - d0.y) | ((u32)(NR + (int)(tr[h].y - d0.z)) << 16);
+      ti.rs0 = (tr[h].x - k.d0.y) | ((u32)(NR + (int)(tr[h].y - k.d0.z)) << 16);
       ti.ns = tr[h].w;
       ti.inv_ns = 1.0f / (float)tr[h].w;
       S.ti[t] = ti;
@@ -1627,7 +1654,6 @@ __global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64
     }
   }
   if (tid == 0) S.tb[nt] = (u32)tot;
-  cp_async_wait_all();
   __syncthreads();
   const u32 NP = (u32)tot;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -1648,7 +1674,7 @@ __global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64
     if (q < q_end) {
       int pr, ps;
       nested_pair(S, t, q, pr, ps);
-      hit = nested_hit(S, pr, ps);
+      hit = nested_hit(B, pr, ps);
     }
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (step < kHitSteps && lane == 0) S.hits[warp][step] = m;
@@ -1696,15 +1722,59 @@ __global__ void __launch_bounds__(kJoinThreads, 6) k_join_nested(JoinArgs A, i64
       hit = false;
       if (q < q_end) {
         nested_pair(S, t, q, pr, ps);
-        hit = nested_hit(S, pr, ps);
+        hit = nested_hit(B, pr, ps);
       }
       m = __ballot_sync(0xffffffffu, hit);
     }
     if (hit) {
       const i64 o = __popc(m & lt_mask);
-      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(S.aid[pr], S.aid[ps]);
+      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(B.aid[pr], B.aid[ps]);
     }
     out += 2 * (i64)__popc(m);
+  }
+}
+
+// PERSIST = false: one CTA per chunk (chunks handed out by ticket in the
+// ordered mode, whose look-back needs launch order).  PERSIST = true
+// (unordered): a resident grid walks chunks c = blockIdx.x + i * gridDim.x,
+// staging chunk i+1 with cp.async while chunk i is joined.
+template <bool EMIT, bool PERSIST>
+__global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(JoinArgs A,
+                                                                             i64 n_chunks) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
+  if (!PERSIST) {
+    __shared__ int s_unit;
+    if (A.ordered) {
+      if (threadIdx.x == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
+      __syncthreads();
+    }
+    const i64 c = A.ordered ? s_unit : blockIdx.x;
+    const NestedChunk k = nested_desc(A, c);
+    nested_stage(S.buf[0], A, k);
+    cp_async_wait_all();
+    __syncthreads();
+    nested_chunk<EMIT>(S, S.buf[0], A, k, c);
+    return;
+  }
+  i64 c = blockIdx.x;
+  if (c >= n_chunks) return;
+  NestedChunk k = nested_desc(A, c);
+  nested_stage(S.buf[0], A, k);
+  cp_async_commit();
+  for (int it = 0; c < n_chunks; c += gridDim.x, ++it) {
+    const i64 cn = c + gridDim.x;
+    NestedChunk kn = k;
+    if (cn < n_chunks) {
+      kn = nested_desc(A, cn);
+      nested_stage(S.buf[(it + 1) & (kNestedBufs - 1)], A, kn);
+    }
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();  // chunk c landed for every thread
+    nested_chunk<EMIT>(S, S.buf[it & (kNestedBufs - 1)], A, k, c);
+    __syncthreads();  // buffer and tables free for reuse
+    k = kn;
   }
 }
 
@@ -1741,6 +1811,33 @@ __device__ __forceinline__ bool within_eps(const i64* __restrict__ cand, i64 i,
   const double dx = __dsub_rn(px[a], qx[b]);
   const double dy = __dsub_rn(py[a], qy[b]);
   return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= eps_sq;
+}
+
+// ---------------------------------------------------------------- input formats
+// SJB1 body (io.py:113-141 in the reference): packed little-endian records
+// {id u64, x_l f64, y_l f64, x_u f64, y_u f64} (40 bytes) → the SoA columns
+// of RectBatch, with load_mbr_binary's check (lower <= upper on both axes;
+// NaN fails it) as an error flag.
+__global__ void k_unpack_records(const u64* __restrict__ rec, i64 n, i64* __restrict__ ids,
+                                 double* __restrict__ xl, double* __restrict__ xu,
+                                 double* __restrict__ yl, double* __restrict__ yu,
+                                 u32* __restrict__ bad) {
+  bool b = false;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const u64* r = rec + 5 * i;
+    const double a = __longlong_as_double((long long)__ldcs(r + 1));
+    const double c = __longlong_as_double((long long)__ldcs(r + 2));
+    const double bb = __longlong_as_double((long long)__ldcs(r + 3));
+    const double d = __longlong_as_double((long long)__ldcs(r + 4));
+    ids[i] = (i64)__ldcs(r);
+    xl[i] = a;
+    yl[i] = c;
+    xu[i] = bb;
+    yu[i] = d;
+    b |= !(a <= bb) || !(c <= d);
+  }
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1u);
 }
 
 __global__ void k_refine_flag(const i64* __restrict__ cand, i64 n, const double* __restrict__ px,
@@ -1827,12 +1924,15 @@ int set_smem_attrs() {
   e = cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(JoinSmem));
   if (e != cudaSuccess) return (int)e;
-  e = cudaFuncSetAttribute(k_join_nested<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(NestedSmem));
-  if (e != cudaSuccess) return (int)e;
-  e = cudaFuncSetAttribute(k_join_nested<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(NestedSmem));
-  if (e != cudaSuccess) return (int)e;
+  const void* nested_fns[] = {(const void*)k_join_nested<false, false>,
+                              (const void*)k_join_nested<true, false>,
+                              (const void*)k_join_nested<false, true>,
+                              (const void*)k_join_nested<true, true>};
+  for (const void* fn : nested_fns) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(NestedSmem));
+    if (e != cudaSuccess) return (int)e;
+  }
   done = true;
   return 0;
 }
@@ -1871,12 +1971,26 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.total = (unsigned long long*)&w.hdr->pairs;
   A.ordered = ordered ? 1 : 0;
   if (cn > 0) {
-    // one CTA per chunk (the ordered look-back takes tickets in launch order)
-    const i64 grid = cn;
-    if (emit)
-      k_join_nested<true><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
-    else
-      k_join_nested<false><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+    if (ordered || !PBSM_NESTED_PERSIST) {
+      // one CTA per chunk (the ordered look-back takes tickets in launch order)
+      if (emit)
+        k_join_nested<true, false><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+      else
+        k_join_nested<false, false><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+    } else {
+      const void* fn = emit ? (const void*)k_join_nested<true, true>
+                            : (const void*)k_join_nested<false, true>;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads,
+                                                        sizeof(NestedSmem)) != cudaSuccess ||
+          per_sm < 1)
+        per_sm = 1;
+      const i64 grid = std::min<i64>(cn, (i64)per_sm * num_sms());
+      if (emit)
+        k_join_nested<true, true><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+      else
+        k_join_nested<false, true><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+    }
   }
   if (rest > 0) {
     // the sorted/large launch keeps its own ticket (the look-back ids follow
@@ -1900,10 +2014,10 @@ int32_t pbsm_abi_version(void) { return PBSM_ABI_VERSION; }
 #define PBSM_STR2(x) #x
 #define PBSM_STR(x) PBSM_STR2(x)
 const char* pbsm_build_info(void) {
-  return "pbsm sm_100a v3: count+validate / plan / scatter (64B records, join tiles only) / "
-         "guard / TMA-staged mini-joins (nested | sort+forward-scan | large) with count->emit; "
-         "B=" PBSM_STR(PBSM_CHUNK_B) " Lmax=" PBSM_STR(PBSM_LMAX) " nested<=" PBSM_STR(
-             PBSM_NESTED_MAX) "";
+  return "pbsm sm_100a abi4: count+validate / plan / scatter (64B records, join tiles only) / "
+         "guard / mini-joins: nested (cp.async-staged) | sort+forward-scan, large (TMA-staged), "
+         "count->emit; B=" PBSM_STR(PBSM_CHUNK_B) " Bn=" PBSM_STR(PBSM_CHUNK_BN) " Lmax=" PBSM_STR(
+             PBSM_LMAX) " nested<=" PBSM_STR(PBSM_NESTED_MAX);
 }
 
 int64_t pbsm_workspace_bytes(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi) {
@@ -2066,6 +2180,18 @@ int64_t pbsm_refine_result_offset(int64_t n_cand) {
   if (n_cand < 0) return PBSM_E_ARG;
   const ScanLayout SL = scan_layout(n_cand);
   return (int64_t)(SL.base + 8 * SL.n);
+}
+
+int pbsm_unpack_records(const void* records, int64_t n, int64_t* ids, double* xl, double* xu,
+                        double* yl, double* yu, uint32_t* bad, void* stream) {
+  if (n < 0 || !bad) return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(bad, 0, sizeof(uint32_t), s);
+  if (n == 0) return launch_status();
+  if (!records || !ids || !xl || !xu || !yl || !yu || ((uintptr_t)records & 7u)) return PBSM_E_ARG;
+  const unsigned blocks = (unsigned)std::min<i64>((n + 255) / 256, (i64)num_sms() * 8);
+  k_unpack_records<<<blocks, 256, 0, s>>>((const u64*)records, n, (i64*)ids, xl, xu, yl, yu, bad);
+  return launch_status();
 }
 
 int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const double* py,

@@ -340,3 +340,28 @@ def test_slice_distribution_nccl_single_rank(golden):
         assert np.array_equal(got, g["cfg2_pairs"])
     finally:
         dist.destroy_process_group()
+
+
+def test_sjb1_device_loader_matches_host(tmp_path, golden):
+    """load_dataset_device: one H2D copy + pbsm_unpack_records == the host
+    loader's columns; an inverted record raises the loader's DatasetError; the
+    joined result through device-loaded inputs is the reference list."""
+    from paper_1908_11740_b200 import io as pio
+
+    g = golden["configs"]
+    r, s, k = make_config(1, float(g["cfg1_scale"]))
+    pio.save_mbr_binary(pb.RectBatch(*r), tmp_path / "r.bin")
+    pio.save_mbr_binary(pb.RectBatch(*s), tmp_path / "s.bin")
+    rd = pio.load_dataset_device(tmp_path / "r.bin")
+    host, _ = pio.load_mbr_binary(tmp_path / "r.bin")
+    for col in ("ids", "xl", "xu", "yl", "yu"):
+        assert np.array_equal(getattr(rd, col).cpu().numpy(), getattr(host, col)), col
+    sd = pio.load_dataset_device(tmp_path / "s.bin")
+    res = dev.run_join(rd, sd, k, k)
+    assert res.count == int(g["cfg1_count"])
+    assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), g["cfg1_pairs"])
+    bad = pb.RectBatch(*(a.copy() for a in r))
+    bad.yl[5] = bad.yu[5] + 0.25
+    pio.save_mbr_binary(bad, tmp_path / "bad.bin")
+    with pytest.raises(pb.DatasetError, match="lower bound above upper bound"):
+        pio.load_dataset_device(tmp_path / "bad.bin")
