@@ -195,6 +195,19 @@ int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
  * pbsm_refine_result_offset(n_cand) of scratch. */
 int64_t pbsm_refine_scratch_bytes(int64_t n_cand);
 int64_t pbsm_refine_result_offset(int64_t n_cand);
+/* pbsm_join_emit without the host copy of the plan: the kernels read the
+ * unit counts from the device header and the grids are the caller's upper
+ * bounds (e.g. the previous join's counts), so the pipeline needs no host
+ * sync between pbsm_plan and the emit.  Unordered placement only.  After the
+ * final pbsm_read_header the caller checks header.chunks_nested <=
+ * max_nested_chunks and chunks_sorted + n_items <= max_other_units (and the
+ * list capacities it gave pbsm_scatter): otherwise some units were not run
+ * and the join must be repeated with pbsm_join_emit. */
+int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                           const pbsm_entry* r_list, const pbsm_entry* s_list,
+                           int64_t max_nested_chunks, int64_t max_other_units, void* scratch,
+                           int64_t* pairs, int64_t capacity, void* stream);
+
 /* SJB1 dataset body (load_mbr_binary, io.py:113-141): n packed 40-byte
  * little-endian records {id u64, x_l, y_l, x_u, y_u f64} at an 8-byte aligned
  * device address → the RectBatch SoA columns (ids reinterpreted as int64,

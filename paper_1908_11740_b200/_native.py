@@ -28,7 +28,7 @@ EXPORTED = (
     "pbsm_abi_version", "pbsm_build_info", "pbsm_workspace_bytes", "pbsm_init",
     "pbsm_count", "pbsm_plan", "pbsm_read_header", "pbsm_scatter", "pbsm_bin",
     "pbsm_scatter_banded",
-    "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit",
+    "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit", "pbsm_join_emit_bounded",
     "pbsm_unpack_records", "pbsm_refine_scratch_bytes", "pbsm_refine_result_offset",
     "pbsm_refine",
 )
@@ -80,6 +80,8 @@ _SIGNATURES = {
                                   _P]),
     "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P, _P,
                                  _I64, _I32, _P]),
+    "pbsm_join_emit_bounded": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I64, _I64, _P,
+                                         _P, _I64, _P]),
     "pbsm_unpack_records": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "pbsm_refine_scratch_bytes": (_I64, [_I64]),
     "pbsm_refine_result_offset": (_I64, [_I64]),

@@ -1134,6 +1134,7 @@ struct JoinArgs {
   i64 capacity;    // pairs the buffer holds
   i64 n_units;
   pbsm_header* hdr;
+  int bounded;     // grids are upper bounds: units past the plan's counts exit
 };
 
 struct ChunkSmem {
@@ -1750,6 +1751,7 @@ __global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(J
       __syncthreads();
     }
     const i64 c = A.ordered ? s_unit : blockIdx.x;
+    if (A.bounded && c >= A.hdr->chunks_nested) return;
     const NestedChunk k = nested_desc(A, c);
     nested_stage(S.buf[0], A, k);
     cp_async_wait_all();
@@ -1757,6 +1759,7 @@ __global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(J
     nested_chunk<EMIT>(S, S.buf[0], A, k, c);
     return;
   }
+  if (A.bounded) n_chunks = min(n_chunks, (i64)A.hdr->chunks_nested);
   i64 c = blockIdx.x;
   if (c >= n_chunks) return;
   NestedChunk k = nested_desc(A, c);
@@ -1793,6 +1796,7 @@ __global__ void __launch_bounds__(kJoinThreads, 2) k_join(JoinArgs A) {
   // units of this launch: [sorted chunks | large items]; the look-back ids
   // continue after the nested chunks (k_join_nested)
   const i64 cn = A.hdr->chunks_nested, cs = A.hdr->chunks_sorted;
+  if (A.bounded && local >= cs + A.hdr->n_items) return;
   const i64 unit = cn + local;
   if (local < cs) join_sorted<EMIT>(U.c, A, unit, local);
   else join_large<EMIT>(U.l, A, unit, local - cs);
@@ -1939,12 +1943,15 @@ int set_smem_attrs() {
 
 int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, int row_hi,
                 const pbsm_entry* r_list, const pbsm_entry* s_list, const pbsm_header* plan,
-                void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s) {
+                void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s,
+                i64 max_nested = -1, i64 max_other = -1) {
   int rc = set_smem_attrs();
   if (rc) return rc;
   const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
   Ws w = ws_bind(ws, L);
-  const i64 cn = plan->chunks_nested, rest = plan->chunks_sorted + plan->n_items;
+  const bool bounded = plan == nullptr;  // sizes from the device header, grids = bounds
+  const i64 cn = bounded ? max_nested : plan->chunks_nested;
+  const i64 rest = bounded ? max_other : plan->chunks_sorted + plan->n_items;
   const i64 n_units = cn + rest;
   // write guard first (reads the cursors the scatter left behind)
   const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
@@ -1970,6 +1977,7 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.hdr = w.hdr;
   A.total = (unsigned long long*)&w.hdr->pairs;
   A.ordered = ordered ? 1 : 0;
+  A.bounded = bounded ? 1 : 0;
   if (cn > 0) {
     if (ordered || !PBSM_NESTED_PERSIST) {
       // one CTA per chunk (the ordered look-back takes tickets in launch order)
@@ -2169,6 +2177,18 @@ int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
     return PBSM_E_ARG;
   return launch_join(true, ordered != 0, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan,
                      scratch, pairs, capacity, as_stream(stream));
+}
+
+int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                           const pbsm_entry* r_list, const pbsm_entry* s_list,
+                           int64_t max_nested_chunks, int64_t max_other_units, void* scratch,
+                           int64_t* pairs, int64_t capacity, void* stream) {
+  if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || capacity < 0 ||
+      (capacity > 0 && !pairs) || max_nested_chunks < 0 || max_other_units < 0 ||
+      max_nested_chunks > 0x7fffffff || max_other_units > 0x7fffffff)
+    return PBSM_E_ARG;
+  return launch_join(true, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, nullptr, scratch,
+                     pairs, capacity, as_stream(stream), max_nested_chunks, max_other_units);
 }
 
 int64_t pbsm_refine_scratch_bytes(int64_t n_cand) {

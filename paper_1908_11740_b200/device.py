@@ -155,6 +155,15 @@ def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream) -> torch.Ten
     return band
 
 
+# Sizes of the last synchronous plan per join shape (grid, strip, input
+# sizes, cost model): with a hit, run_join skips the host read of the plan
+# header — lists, unit grids and the pair buffer use these sizes and the emit
+# runs bounded (pbsm_join_emit_bounded); the final header read checks every
+# size and a miss re-runs the join synchronously.
+_plan_cache: dict = {}
+SPECULATE = os.environ.get("PBSM_SPECULATE", "1") != "0"
+
+
 def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool = True,
              row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
              keep_counts: bool = False, probe: PhaseProbe | None = None,
@@ -196,12 +205,20 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         counts = tuple(v.clone() for v in _tile_count_views(ws, kx, ky, kx * (row_hi - row_lo)))
     _native.check(lib.pbsm_plan(wsp, *grid, nested_max, stream), "pbsm_plan")
     mark("plan")
-    h = _read_header(lib, ws, stream)
-    mark("header")
+    key = (str(device), kx, ky, row_lo, row_hi, len(r), len(s), s is r, nested_max, bin_bytes)
+    guess = _plan_cache.get(key) if (SPECULATE and collect and not ordered
+                                     and not keep_counts) else None
+    if guess is None:
+        h = _read_header(lib, ws, stream)
+        mark("header")
+        list_r, list_s = h.list_r, h.list_s
+    else:
+        h = None
+        list_r, list_s = guess["list_r"], guess["list_s"]
 
     lists = []
     thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
-    for side, b, total in ((0, r, h.list_r), (1, s, h.list_s)):
+    for side, b, total in ((0, r, list_r), (1, s, list_s)):
         ent = torch.empty((max(total, 1), 8), dtype=torch.int64, device=device)  # 64 B records
         # the copy costs ~80 B per rectangle; it pays where the random record
         # writes dominate: large lists and heavy replication (cfg4: 1.7
@@ -222,10 +239,41 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     if ev:
         ev[1].record()
 
+    rl, sl = lists
+    if guess is not None:
+        cap, cn, rest = guess["pairs"], guess["nested"], guess["other"]
+        scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(cn + rest)), dtype=torch.uint8,
+                              device=device)
+        pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
+        _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), sl.data_ptr(), cn,
+                                                 rest, scratch.data_ptr(), pairs.data_ptr(), cap,
+                                                 stream), "pbsm_join_emit_bounded")
+        mark("join")
+        h2 = _read_header(lib, ws, stream,
+                          allow=_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW)
+        mark("header2")
+        if (h2.list_r > list_r or h2.list_s > list_s or h2.chunks_nested > cn
+                or h2.chunks_sorted + h2.n_items > rest or h2.pairs > cap
+                or h2.error & (_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW)):
+            # another input behind the same shape: redo it with the exact plan
+            _plan_cache.pop(key, None)
+            return run_join(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
+                            timing=timing, keep_counts=keep_counts, probe=probe,
+                            ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes)
+        count = int(h2.pairs)
+        if ev:
+            ev[2].record()
+            ev[2].synchronize()
+        res = DeviceJoinResult(count, pairs[:count], header=h2.as_dict())
+        if ev:
+            res.times = {"partition": ev[0].elapsed_time(ev[1]) / 1e3,
+                         "join": ev[1].elapsed_time(ev[2]) / 1e3,
+                         "total": ev[0].elapsed_time(ev[2]) / 1e3}
+        return res
+
     n_units = h.n_units
     scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(n_units)), dtype=torch.uint8,
                           device=device)
-    rl, sl = lists
     pairs = None
     if not collect:
         _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), C.byref(h),
@@ -249,6 +297,11 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                 break
             cap = count  # rare: the estimate was short, emit again into an exact buffer
         pairs = pairs[:count]
+        if not ordered and not keep_counts:
+            _plan_cache.clear()  # one shape at a time
+            _plan_cache[key] = {"list_r": h.list_r, "list_s": h.list_s, "pairs": cap,
+                                "nested": h.chunks_nested,
+                                "other": h.chunks_sorted + h.n_items}
     if ev:
         ev[2].record()
         ev[2].synchronize()

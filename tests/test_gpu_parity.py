@@ -365,3 +365,32 @@ def test_sjb1_device_loader_matches_host(tmp_path, golden):
     pio.save_mbr_binary(bad, tmp_path / "bad.bin")
     with pytest.raises(pb.DatasetError, match="lower bound above upper bound"):
         pio.load_dataset_device(tmp_path / "bad.bin")
+
+
+def test_speculative_plan_reuse(golden):
+    """A second join of the same shape skips the plan-header read (sizes from
+    the previous plan, bounded emit); different data behind the same shape —
+    bigger lists, more chunks, more pairs, or fewer — is detected by the final
+    header read and re-run, always bit-exact."""
+    g = golden["configs"]
+    r, s, k = make_config(2, float(g["cfg2_scale"]))
+    R, S = dev.to_device(r), dev.to_device(s)
+    want = g["cfg2_pairs"]
+    dev._plan_cache.clear()
+    for _ in range(2):  # synchronous, then speculative with an exact guess
+        res = dev.run_join(R, S, k, k)
+        assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+    assert dev._plan_cache
+    # same sizes, denser S: everything grows → mismatch → exact re-run
+    s2 = tuple(a.copy() for a in s)
+    s2[1][:] = s2[1] * 0.5
+    s2[2][:] = s2[2] * 0.5 + 0.01
+    S2 = dev.to_device(s2)
+    got = dev.run_join(R, S2, k, k)
+    ref = oracle.join(r, s2, "2d", k)
+    assert got.count == ref["count"]
+    assert np.array_equal(oracle.sorted_pairs(got.pairs.cpu().numpy()),
+                          oracle.sorted_pairs(ref["pairs"]))
+    # and back to the original data (smaller than the cached guess)
+    res = dev.run_join(R, S, k, k)
+    assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
