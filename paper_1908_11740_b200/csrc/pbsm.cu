@@ -322,6 +322,25 @@ __device__ __forceinline__ void block_excl_scan_multi(T v[NV], T tot[NV],
   __syncthreads();
 }
 
+// 32-bit variant (one shuffle per step instead of two)
+template <int NT>
+__device__ __forceinline__ u32 block_excl_scan32(u32 v, u32* total, u32* sh /* >= NT/32+1 */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const u32 inc = warp_incl_scan<u32>(v);
+  if (lane == 31) sh[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const u32 s = lane < NT / 32 ? sh[lane] : 0u;
+    const u32 si = warp_incl_scan<u32>(s);
+    if (lane < NT / 32) sh[lane] = si - s;
+    if (lane == NT / 32 - 1) sh[NT / 32] = si;
+  }
+  __syncthreads();
+  const u32 r = inc - v + sh[wid];
+  *total = sh[NT / 32];
+  return r;  // (callers sync before sh is reused)
+}
+
 // ---- TMA bulk copy (cp.async.bulk) + mbarrier, one elected thread issues
 __device__ __forceinline__ u32 smem_u32(const void* p) {
   return (u32)__cvta_generic_to_shared(p);
@@ -1510,7 +1529,7 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
 // {yl, yu} in two 16-byte arrays, the id in a third — so there is no
 // transpose pass, and 32 lanes reading 32 consecutive entries hit 512
 // contiguous bytes (4 wavefronts).  The pad words are never fetched.
-constexpr int kHitSteps = 32;  // warp-steps per warp whose hit ballots are kept
+constexpr int kHitCap = 128;  // hits per warp kept (packed entry positions) for the emit
 
 struct TileInfo {  // one 16-byte shared-memory read per pair test
   u32 p0;          // first pair index of the tile
@@ -1536,8 +1555,8 @@ struct NestedSmem {
   TileInfo ti[kMaxTilesN];
   u32 tb[kMaxTilesN + 1];        // tile pair-prefix boundaries (tb[nt] = pair total)
   u64 wtot[kJoinThreads / 32 + 1];
-  u64 scan[kJoinThreads / 32 + 1];
-  u32 hits[kJoinThreads / 32][kHitSteps];  // pass-1 ballots, replayed by pass 2
+  u32 scan32[kJoinThreads / 32 + 1];
+  u32 hits[kJoinThreads / 32][kHitCap];  // pass-1 hits: r position | s position << 16
   u64 base;
 };
 
@@ -1588,6 +1607,7 @@ __device__ __forceinline__ bool nested_hit(const NestedBuf& B, int pr, int ps) {
 struct NestedChunk {
   uint4 d0;
   int nt, NR, NS;
+  bool ok;
 };
 
 // all threads: the chunk descriptor (broadcast loads) and its plan check
@@ -1598,13 +1618,18 @@ __device__ __forceinline__ NestedChunk nested_desc(const JoinArgs& A, i64 c) {
   k.nt = (int)(d1.x - k.d0.x);
   k.NR = (int)(d1.y - k.d0.y);
   k.NS = (int)(d1.z - k.d0.z);
-  if (!(k.nt > 0 && k.NR > 0 && k.NS > 0 && k.NR + k.NS <= kCapN && k.nt <= kMaxTilesN)) {
-    // never by construction (k_chunks); flag it and contribute 0 pairs (no
-    // early return: the ordered look-back chain must still be fed)
+  k.ok = k.nt > 0 && k.NR > 0 && k.NS > 0 && k.NR + k.NS <= kCapN && k.nt <= kMaxTilesN;
+  return k;
+}
+
+// a chunk that breaks the plan invariants (never, by construction of
+// k_chunks): flag it and contribute 0 pairs (no early return: the ordered
+// look-back chain must still be fed)
+__device__ __forceinline__ void nested_check(const JoinArgs& A, NestedChunk& k) {
+  if (!k.ok) {
     if (threadIdx.x == 0) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
     k.nt = k.NR = k.NS = 0;
   }
-  return k;
 }
 
 // all threads: async copies of the chunk's entries (coords + id; the pad is
@@ -1638,8 +1663,8 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     tr[h] = t < nt ? B.jr[t] : make_uint4(0, 0, 0, 0);
     np += tr[h].z * tr[h].w;
   }
-  u64 tot;
-  u32 pre = (u32)block_excl_scan<kJoinThreads>((u64)np, &tot, S.scan);
+  u32 tot;
+  u32 pre = block_excl_scan32<kJoinThreads>(np, &tot, S.scan32);
 #pragma unroll
   for (int h = 0; h < kTPT; ++h) {
     const int t = kTPT * tid + h;
@@ -1667,18 +1692,20 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
   // pass 1: count (and keep each warp-step's hit ballot for pass 2)
   u32 wcnt = 0;
   int lt = lt_beg;
-  int step = 0;
-  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u, ++step) {
+  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
     const u32 q = q0 + lane;
     const int t = nested_step_tile(S, nt, q0, lt, lane);
     bool hit = false;
+    int pr = 0, ps = 0;
     if (q < q_end) {
-      int pr, ps;
       nested_pair(S, t, q, pr, ps);
       hit = nested_hit(B, pr, ps);
     }
     const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (step < kHitSteps && lane == 0) S.hits[warp][step] = m;
+    if (EMIT && hit) {  // ballot-compacted into the warp's hit list
+      const u32 o = wcnt + __popc(m & lt_mask);
+      if (o < kHitCap) S.hits[warp][o] = (u32)pr | ((u32)ps << 16);
+    }
     wcnt += __popc(m);
   }
   if (lane == 0) S.wtot[warp] = wcnt;
@@ -1703,30 +1730,29 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
   if (!EMIT) return;
   __syncthreads();
   if (S.base == ~0ull) return;
-  // pass 2: emit, ballot-compacted (same slices, same order); for the first
-  // kHitSteps steps the recorded ballot says which lanes hit, so only those
-  // map their pair and nothing is tested twice
+  // pass 2: emit the warp's hits at its offset — from the hit list (one
+  // coalesced 16-byte store per hit, nothing re-tested), or, for a warp whose
+  // hits overflowed the list, by re-testing its slice (same order)
   i64* out = A.pairs + 2 * (i64)(S.base + S.wtot[warp]);
+  if (wcnt <= (u32)kHitCap) {
+    for (u32 i = lane; i < wcnt; i += 32u) {
+      const u32 v = S.hits[warp][i];
+      *reinterpret_cast<longlong2*>(out + 2 * (i64)i) =
+          make_longlong2(B.aid[v & 0xffffu], B.aid[v >> 16]);
+    }
+    return;
+  }
   lt = lt_beg;
-  step = 0;
-  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u, ++step) {
+  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
     const u32 q = q0 + lane;
     const int t = nested_step_tile(S, nt, q0, lt, lane);
     int pr = 0, ps = 0;
-    unsigned m;
-    bool hit;
-    if (step < kHitSteps) {
-      m = S.hits[warp][step];
-      hit = (m >> lane) & 1u;
-      if (hit) nested_pair(S, t, q, pr, ps);
-    } else {
-      hit = false;
-      if (q < q_end) {
-        nested_pair(S, t, q, pr, ps);
-        hit = nested_hit(B, pr, ps);
-      }
-      m = __ballot_sync(0xffffffffu, hit);
+    bool hit = false;
+    if (q < q_end) {
+      nested_pair(S, t, q, pr, ps);
+      hit = nested_hit(B, pr, ps);
     }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (hit) {
       const i64 o = __popc(m & lt_mask);
       *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(B.aid[pr], B.aid[ps]);
@@ -1751,8 +1777,12 @@ __global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(J
       __syncthreads();
     }
     const i64 c = A.ordered ? s_unit : blockIdx.x;
-    if (A.bounded && c >= A.hdr->chunks_nested) return;
-    const NestedChunk k = nested_desc(A, c);
+    // (cdesc holds tiles + 2 entries, so the descriptor load is in bounds
+    // even for a unit past the plan's count: load it alongside the count)
+    const i64 n_plan = A.bounded ? (i64)A.hdr->chunks_nested : n_chunks;
+    NestedChunk k = nested_desc(A, c);
+    if (c >= n_plan) return;
+    nested_check(A, k);
     nested_stage(S.buf[0], A, k);
     cp_async_wait_all();
     __syncthreads();
@@ -1763,6 +1793,7 @@ __global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(J
   i64 c = blockIdx.x;
   if (c >= n_chunks) return;
   NestedChunk k = nested_desc(A, c);
+  nested_check(A, k);
   nested_stage(S.buf[0], A, k);
   cp_async_commit();
   for (int it = 0; c < n_chunks; c += gridDim.x, ++it) {
@@ -1770,6 +1801,7 @@ __global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(J
     NestedChunk kn = k;
     if (cn < n_chunks) {
       kn = nested_desc(A, cn);
+      nested_check(A, kn);
       nested_stage(S.buf[(it + 1) & (kNestedBufs - 1)], A, kn);
     }
     cp_async_commit();

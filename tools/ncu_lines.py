@@ -36,7 +36,8 @@ tmp = Path(tempfile.mkdtemp())
 subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
 cubins = list(tmp.glob("*.cubin"))
 dis = subprocess.run(["nvdisasm", "-g", "-c", str(cubins[0])], capture_output=True, text=True).stdout
-want = "ILb1E" if "(bool)1" in kname else ("ILb0E" if "(bool)0" in kname else "")
+bools = re.findall(r"\(bool\)([01])", kname)
+want = ("I" + "".join(f"Lb{b}E" for b in bools) + "E") if bools else ""
 short = kname.split("(")[0].split("::")[-1].split("<")[0]
 line_of = {}
 cur_fn = None
