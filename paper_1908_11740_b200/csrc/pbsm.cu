@@ -1553,7 +1553,8 @@ struct NestedBuf {               // one staged chunk
 struct NestedSmem {
   NestedBuf buf[kNestedBufs];
   TileInfo ti[kMaxTilesN];
-  u32 tb[kMaxTilesN + 1];        // tile pair-prefix boundaries (tb[nt] = pair total)
+  u32 tb[kMaxTilesN + 33];       // tile pair-prefix boundaries (tb[nt] = pair total),
+                                 // then 32 sentinels (no bounds check per warp-step)
   u64 wtot[kJoinThreads / 32 + 1];
   u32 scan32[kJoinThreads / 32 + 1];
   u32 hits[kJoinThreads / 32][kHitCap];  // pass-1 hits: r position | s position << 16
@@ -1578,7 +1579,8 @@ __device__ __forceinline__ int nested_tile_of(const NestedSmem& S, int nt, u32 q
 __device__ __forceinline__ int nested_step_tile(const NestedSmem& S, int nt, u32 q0, int& lt,
                                                 int lane) {
   const int j = lt + 1 + lane;
-  const u32 d = (j <= nt ? S.tb[j] : 0xffffffffu) - q0;
+  const u32 d = S.tb[j] - q0;  // tb[nt + 1 ..] = ~0
+  if (__shfl_sync(0xffffffffu, d, 0) >= 32u) return lt;  // the whole step in tile lt
   const unsigned bits = __reduce_or_sync(0xffffffffu, d < 32u ? (1u << d) : 0u);
   const int mine = lt + __popc(bits & (0xffffffffu >> (31 - lane)));
   lt += __popc(bits);
@@ -1679,7 +1681,7 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
       pre += tr[h].z * tr[h].w;
     }
   }
-  if (tid == 0) S.tb[nt] = (u32)tot;
+  if (tid <= 32) S.tb[nt + tid] = tid == 0 ? (u32)tot : 0xffffffffu;
   __syncthreads();
   const u32 NP = (u32)tot;
   const unsigned lt_mask = (1u << lane) - 1u;
