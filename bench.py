@@ -198,7 +198,7 @@ def reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "pairs_per_s": pairs / dt,
         "config": {"workload": f"cfg{args.config}", "sample_fraction": frac},
@@ -383,7 +383,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": step_s * 1e3,
-        "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SURVEY.md §8(d) generators; TIGER/OSM data unavailable)",
         "config": {"workload": f"cfg{args.config}", "n_r": n_r, "n_s": n_s, "grid": f"{k}x{k}",

@@ -101,10 +101,16 @@ constexpr int kScanTile = kScanThreads * kScanPer;
 #ifndef PBSM_PART_MINB
 #define PBSM_PART_MINB 4
 #endif
-constexpr int kBins = 256;                  // row bands of the binned scatter
+#ifndef PBSM_BINS
+#define PBSM_BINS 256
+#endif
+constexpr int kBins = PBSM_BINS;                  // row bands of the binned scatter
 constexpr int kBinSlots = kBins + 1;        // + one slot for rectangles outside the strip
 constexpr int kMaxPartBlocks = 4096;        // grid cap of the count / bin passes
-constexpr int kBinTile = 1024;              // rectangles staged per bin-copy step
+#ifndef PBSM_BIN_TILE
+#define PBSM_BIN_TILE 1024
+#endif
+constexpr int kBinTile = PBSM_BIN_TILE;              // rectangles staged per bin-copy step
 
 constexpr u64 kXOut = 1ull << 63;
 constexpr u64 kYOut = 1ull << 62;
@@ -653,9 +659,10 @@ struct ScatterIn {
   const i64* ids;
   const double *xl, *xu, *yl, *yu;
   const BRec* band;  // non-null: read the row-band copy instead
+  template <bool BANDED>
   __device__ __forceinline__ void load(i64 i, double& a, double& b, double& c, double& d,
                                        i64& id) const {
-    if (band) {
+    if (BANDED) {
       const BRec* r = band + i;
       id = __ldcs(&r->id);
       a = __ldcs(&r->xl);
@@ -672,7 +679,10 @@ struct ScatterIn {
   }
 };
 
-__global__ void __launch_bounds__(256, PBSM_PART_MINB) k_scatter(ScatterIn in, i64 n,
+// 5 resident CTAs per SM measured best for the SoA input (cfg3: 4.77 vs 4.91
+// ms at 4), 4 for the 40-byte band records (cfg4: 6.65 vs 7.02 ms at 5)
+template <bool BANDED>
+__global__ void __launch_bounds__(256, BANDED ? 4 : 5) k_scatter(ScatterIn in, i64 n,
                                                  int kx, int ky, int row_lo, int row_hi,
                                                  const double* __restrict__ bx,
                                                  const double* __restrict__ by,
@@ -684,11 +694,11 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_scatter(ScatterIn in, i
   i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   double pa = 0, pb = 0, pc = 0, pd = 0;
   i64 pid = 0;
-  if (i < n) in.load(i, pa, pb, pc, pd, pid);  // software pipeline: next rectangle in flight
+  if (i < n) in.load<BANDED>(i, pa, pb, pc, pd, pid);  // software pipeline: next one in flight
   for (; i < n; i += stride) {
     const double a = pa, b = pb, c = pc, d = pd;
     const i64 id = pid;
-    if (i + stride < n) in.load(i + stride, pa, pb, pc, pd, pid);
+    if (i + stride < n) in.load<BANDED>(i + stride, pa, pb, pc, pd, pid);
     const int c0 = tile_of(a, kx, bx);
     const int c1 = tile_of(b, kx, bx);
     const int rr0 = tile_of(c, ky, by);
@@ -1154,6 +1164,10 @@ struct JoinArgs {
   i64 n_units;
   pbsm_header* hdr;
   int bounded;     // grids are upper bounds: units past the plan's counts exit
+  // write guard folded into the nested join (g_tiles > 0): cursor ends vs
+  // the counted ends, every tile (partition.py:229-233)
+  const u32 *g_cur_r, *g_end_r, *g_cur_s, *g_end_s;
+  u64 g_tiles;
 };
 
 struct ChunkSmem {
@@ -1173,11 +1187,15 @@ struct ChunkSmem {
   int unit, nt, NR, NS;
 };
 
+constexpr int kLargeHitCap = 4096;  // hits of a large work item kept for the emit
 struct LargeSmem {
   Rec other[kCap];
+  u32 hit[kLargeHitCap];        // lead thread | other index (in the item) << 8
+  i64 lead_id[kJoinThreads];
   u64 bar;
   u64 scan[kJoinThreads / 32 + 1];
   u64 base;
+  u32 nhit;
   int unit;
 };
 
@@ -1424,9 +1442,11 @@ __device__ void join_sorted(ChunkSmem& S, const JoinArgs& A, i64 unit, int c) {
 // which stream through shared memory.  Every (lead, other) pair is tested with the full
 // closed-interval predicate (intersects, geometry.py:59-61) and the class rule
 // (>= 1 x-in and >= 1 y-in ⇔ Eq. 1 owner tile).
-template <bool EMIT>
-__device__ __forceinline__ u32 large_pass(const LargeSmem& S, int n, bool have, const Half& me,
-                                          bool lead_r, i64 my_id, i64* out) {
+// LIST: also record each hit (lead thread, other index k0 + k) in the block's
+// hit list while it has room
+template <bool EMIT, bool LIST>
+__device__ __forceinline__ u32 large_pass(LargeSmem& S, int n, bool have, const Half& me,
+                                          bool lead_r, i64 my_id, i64* out, u32 k0) {
   u32 c = 0;
   if (!have) return 0;
   const double mxl = key_x(me.xl_key);
@@ -1440,6 +1460,10 @@ __device__ __forceinline__ u32 large_pass(const LargeSmem& S, int n, bool have, 
       if (EMIT) {
         *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
             lead_r ? make_longlong2(my_id, o.id) : make_longlong2(o.id, my_id);
+      }
+      if (LIST) {
+        const u32 h = atomicAdd_block(&S.nhit, 1u);
+        if (h < (u32)kLargeHitCap) S.hit[h] = threadIdx.x | ((k0 + (u32)k) << 8);
       }
       ++c;
     }
@@ -1477,7 +1501,11 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
     me = *reinterpret_cast<const Half*>(L + a);
     my_id = L[a].id;
   }
-  if (tid == 0) mbar_init(&S.bar, 1);
+  if (tid == 0) {
+    mbar_init(&S.bar, 1);
+    S.nhit = 0;
+  }
+  S.lead_id[tid] = my_id;
   __syncthreads();
   u32 phase = 0;
   u32 cnt = 0;
@@ -1495,9 +1523,9 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
       mbar_wait(&S.bar, phase);
       phase ^= 1u;
       if (pass == 0) {
-        cnt += large_pass<false>(S, n, have, me, lead_r, my_id, nullptr);
+        cnt += large_pass<false, EMIT>(S, n, have, me, lead_r, my_id, nullptr, ob - o_beg);
       } else if (ok) {
-        out += 2 * (i64)large_pass<true>(S, n, have, me, lead_r, my_id, out);
+        out += 2 * (i64)large_pass<true, false>(S, n, have, me, lead_r, my_id, out, 0);
       }
     }
     if (pass == 0) {
@@ -1509,6 +1537,23 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
       }
       if (tid == 0) S.base = reserve(A, unit, total);
       __syncthreads();
+      if (total <= (u64)kLargeHitCap) {
+        // every hit is in the list: emit from it (no second pass over the
+        // other side), one coalesced 16-byte store per hit
+        if ((i64)(S.base + total) > A.capacity) {
+          if (tid == 0 && total) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
+          return;
+        }
+        i64* o = A.pairs + 2 * (i64)S.base;
+        for (u32 h = tid; h < (u32)total; h += kJoinThreads) {
+          const u32 v = S.hit[h];
+          const i64 lid = S.lead_id[v & 0xffu];
+          const i64 oid = O[o_beg + (v >> 8)].id;
+          *reinterpret_cast<longlong2*>(o + 2 * (i64)h) =
+              lead_r ? make_longlong2(lid, oid) : make_longlong2(oid, lid);
+        }
+        return;
+      }
       const i64 start = (i64)(S.base + excl);
       ok = start + (i64)cnt <= A.capacity;
       if (!ok && cnt) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
@@ -1773,6 +1818,13 @@ __global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(J
   extern __shared__ __align__(128) unsigned char smem_raw[];
   NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
   if (!PERSIST) {
+    if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
+      bool bad = false;
+      for (u64 t = blockIdx.x * (u64)kJoinThreads + threadIdx.x; t < A.g_tiles;
+           t += (u64)gridDim.x * kJoinThreads)
+        bad |= (A.g_cur_r[t] != A.g_end_r[t]) || (A.g_cur_s[t] != A.g_end_s[t]);
+      if (bad) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
+    }
     __shared__ int s_unit;
     if (A.ordered) {
       if (threadIdx.x == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
@@ -1987,10 +2039,14 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   const i64 cn = bounded ? max_nested : plan->chunks_nested;
   const i64 rest = bounded ? max_other : plan->chunks_sorted + plan->n_items;
   const i64 n_units = cn + rest;
-  // write guard first (reads the cursors the scatter left behind)
-  const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
-                                                                (i64)num_sms() * 8));
-  k_guard<<<gb, 256, 0, s>>>(w.cur_r, w.cnt_r, w.cur_s, w.cnt_s, L.tiles, w.hdr);
+  // the write guard (reads the cursors the scatter left behind) runs inside
+  // the nested join when there is one, else as its own kernel
+  const bool fused_guard = cn > 0 && (ordered || !PBSM_NESTED_PERSIST);
+  if (!fused_guard) {
+    const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
+                                                                  (i64)num_sms() * 8));
+    k_guard<<<gb, 256, 0, s>>>(w.cur_r, w.cnt_r, w.cur_s, w.cnt_s, L.tiles, w.hdr);
+  }
   cudaMemsetAsync(&w.hdr->pairs, 0, sizeof(int64_t), s);
   if (n_units == 0) return launch_status();
   if (ordered) cudaMemsetAsync(scratch, 0, join_scratch(n_units), s);
@@ -2012,6 +2068,11 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.total = (unsigned long long*)&w.hdr->pairs;
   A.ordered = ordered ? 1 : 0;
   A.bounded = bounded ? 1 : 0;
+  A.g_cur_r = w.cur_r;
+  A.g_end_r = w.cnt_r;
+  A.g_cur_s = w.cur_s;
+  A.g_end_s = w.cnt_s;
+  A.g_tiles = fused_guard ? L.tiles : 0;
   if (cn > 0) {
     if (ordered || !PBSM_NESTED_PERSIST) {
       // one CTA per chunk (the ordered look-back takes tickets in launch order)
@@ -2136,11 +2197,19 @@ static int scatter_impl(const int64_t* ids, const double* xl, const double* xu,
                         int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
                         int32_t row_hi, pbsm_entry* out, int64_t capacity, void* stream) {
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * 8);
+#ifndef PBSM_SCAT_GRID
+#define PBSM_SCAT_GRID 16
+#endif
+  const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * PBSM_SCAT_GRID);
   ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band)};
-  k_scatter<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
-      in, n, kx, ky, row_lo, row_hi, w.bx, w.by, side ? w.cur_s : w.cur_r,
-      reinterpret_cast<Rec*>(out), capacity, w.hdr);
+  if (band)
+    k_scatter<true><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+        in, n, kx, ky, row_lo, row_hi, w.bx, w.by, side ? w.cur_s : w.cur_r,
+        reinterpret_cast<Rec*>(out), capacity, w.hdr);
+  else
+    k_scatter<false><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+        in, n, kx, ky, row_lo, row_hi, w.bx, w.by, side ? w.cur_s : w.cur_r,
+        reinterpret_cast<Rec*>(out), capacity, w.hdr);
   return launch_status();
 }
 

@@ -394,3 +394,42 @@ def test_speculative_plan_reuse(golden):
     # and back to the original data (smaller than the cached guess)
     res = dev.run_join(R, S, k, k)
     assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+
+
+def test_write_guard_detects_a_skipped_scatter(golden):
+    """The partition write guard (partition.py:229-233): if a scatter did not
+    run, the cursor ends disagree with the counted ends and the join reports
+    PBSM_ERR_OFFSET_MISMATCH (the guard runs inside the nested join kernel
+    when there is one, else on its own)."""
+    import ctypes as C
+
+    from paper_1908_11740_b200 import _native
+
+    lib = _native.load()
+    g = golden["configs"]
+    r, s, k = make_config(2, float(g["cfg2_scale"]))
+    R, S = dev.to_device(r), dev.to_device(s)
+    for nested_max in (-1, 0):  # with nested chunks (fused guard) / all sorted (own kernel)
+        ws = dev._workspace(lib, R.device, k, k, 0, k)
+        wsp, st = ws.data_ptr(), torch.cuda.current_stream().cuda_stream
+        lib.pbsm_init(wsp, k, k, 0, k, st)
+        for side, b in ((0, R), (1, S)):
+            lib.pbsm_count(b.xl.data_ptr(), b.xu.data_ptr(), b.yl.data_ptr(), b.yu.data_ptr(),
+                           len(b), side, wsp, k, k, 0, k, st)
+        lib.pbsm_plan(wsp, k, k, 0, k, nested_max, st)
+        h = _native.Header()
+        lib.pbsm_read_header(wsp, C.byref(h), st)
+        rl = torch.empty((h.list_r, 8), dtype=torch.int64, device="cuda")
+        sl = torch.empty((h.list_s, 8), dtype=torch.int64, device="cuda")
+        lib.pbsm_scatter(R.ids.data_ptr(), R.xl.data_ptr(), R.xu.data_ptr(), R.yl.data_ptr(),
+                         R.yu.data_ptr(), len(R), 0, wsp, k, k, 0, k, rl.data_ptr(), h.list_r, st)
+        # S's scatter deliberately skipped
+        scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(h.n_units)), dtype=torch.uint8,
+                              device="cuda")
+        pairs = torch.empty((max(h.pair_bound, 1), 2), dtype=torch.int64, device="cuda")
+        assert lib.pbsm_join_emit(wsp, k, k, 0, k, rl.data_ptr(), sl.data_ptr(), C.byref(h),
+                                  scratch.data_ptr(), pairs.data_ptr(), max(h.pair_bound, 1), 0,
+                                  st) == 0
+        h2 = _native.Header()
+        lib.pbsm_read_header(wsp, C.byref(h2), st)
+        assert h2.error & _native.ERR_OFFSET_MISMATCH, nested_max
