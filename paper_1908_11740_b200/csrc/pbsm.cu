@@ -84,6 +84,10 @@ constexpr int kMaxTiles = kCap / 2;     // a join tile holds >= 2 entries
 #endif
 constexpr int kChunkBN = PBSM_CHUNK_BN;  // bucket width of the nested chunks
 constexpr int kCapN = kChunkBN + kLmax;  // max entries of a nested chunk
+#ifndef PBSM_NESTED_THREADS
+#define PBSM_NESTED_THREADS 256
+#endif
+constexpr int kNT = PBSM_NESTED_THREADS;  // threads of a nested-join CTA
 constexpr int kMaxTilesN = kCapN / 2;
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
 constexpr int kLargeOther = 2048;         // other-side entries per large work item
@@ -1600,9 +1604,9 @@ struct NestedSmem {
   TileInfo ti[kMaxTilesN];
   u32 tb[kMaxTilesN + 33];       // tile pair-prefix boundaries (tb[nt] = pair total),
                                  // then 32 sentinels (no bounds check per warp-step)
-  u64 wtot[kJoinThreads / 32 + 1];
-  u32 scan32[kJoinThreads / 32 + 1];
-  u32 hits[kJoinThreads / 32][kHitCap];  // pass-1 hits: r position | s position << 16
+  u64 wtot[kNT / 32 + 1];
+  u32 scan32[kNT / 32 + 1];
+  u32 hits[kNT / 32][kHitCap];  // pass-1 hits: r position | s position << 16
   u64 base;
 };
 
@@ -1684,14 +1688,14 @@ __device__ __forceinline__ void nested_check(const JoinArgs& A, NestedChunk& k) 
 __device__ __forceinline__ void nested_stage(NestedBuf& B, const JoinArgs& A,
                                              const NestedChunk& k) {
   const int N = k.NR + k.NS;
-  for (int e = threadIdx.x; e < N; e += kJoinThreads) {
+  for (int e = threadIdx.x; e < N; e += kNT) {
     const Rec* src = e < k.NR ? A.rl + k.d0.y + e : A.sl + k.d0.z + (e - k.NR);
     const unsigned char* g = reinterpret_cast<const unsigned char*>(src);
     cp_async16(&B.ax[e], g);
     cp_async16(&B.ay[e], g + 16);
     cp_async8(&B.aid[e], g + 32);
   }
-  for (int t = threadIdx.x; t < k.nt; t += kJoinThreads) cp_async16(&B.jr[t], A.jrec[0] + k.d0.x + t);
+  for (int t = threadIdx.x; t < k.nt; t += kNT) cp_async16(&B.jr[t], A.jrec[0] + k.d0.x + t);
 }
 
 // One staged chunk (B landed and visible): tile table, count, reserve, emit.
@@ -1701,7 +1705,7 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = k.nt, NR = k.NR;
   // tile table (kTPT consecutive tiles per thread)
-  constexpr int kTPT = (kMaxTilesN + kJoinThreads - 1) / kJoinThreads;
+  constexpr int kTPT = (kMaxTilesN + kNT - 1) / kNT;
   uint4 tr[kTPT];
   u32 np = 0;
 #pragma unroll
@@ -1711,7 +1715,7 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     np += tr[h].z * tr[h].w;
   }
   u32 tot;
-  u32 pre = block_excl_scan32<kJoinThreads>(np, &tot, S.scan32);
+  u32 pre = block_excl_scan32<kNT>(np, &tot, S.scan32);
 #pragma unroll
   for (int h = 0; h < kTPT; ++h) {
     const int t = kTPT * tid + h;
@@ -1732,7 +1736,7 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
   const unsigned lt_mask = (1u << lane) - 1u;
   // each warp owns one contiguous slice of the pair index space, so the tile
   // of its current step only moves forward: one binary search per warp
-  constexpr int kW = kJoinThreads / 32;
+  constexpr int kW = kNT / 32;
   const u32 per = ((NP + kW - 1) / kW + 31u) & ~31u;
   const u32 q_beg = min(NP, (u32)warp * per), q_end = min(NP, q_beg + per);
   const int lt_beg = q_beg < NP ? nested_tile_of(S, nt, q_beg) : 0;
@@ -1813,15 +1817,15 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
 // (unordered): a resident grid walks chunks c = blockIdx.x + i * gridDim.x,
 // staging chunk i+1 with cp.async while chunk i is joined.
 template <bool EMIT, bool PERSIST>
-__global__ void __launch_bounds__(kJoinThreads, PERSIST ? 4 : 6) k_join_nested(JoinArgs A,
+__global__ void __launch_bounds__(kNT, PERSIST ? 4 : 1536 / kNT) k_join_nested(JoinArgs A,
                                                                              i64 n_chunks) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
   if (!PERSIST) {
     if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
       bool bad = false;
-      for (u64 t = blockIdx.x * (u64)kJoinThreads + threadIdx.x; t < A.g_tiles;
-           t += (u64)gridDim.x * kJoinThreads)
+      for (u64 t = blockIdx.x * (u64)kNT + threadIdx.x; t < A.g_tiles;
+           t += (u64)gridDim.x * kNT)
         bad |= (A.g_cur_r[t] != A.g_end_r[t]) || (A.g_cur_s[t] != A.g_end_s[t]);
       if (bad) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
     }
@@ -2077,22 +2081,22 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
     if (ordered || !PBSM_NESTED_PERSIST) {
       // one CTA per chunk (the ordered look-back takes tickets in launch order)
       if (emit)
-        k_join_nested<true, false><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+        k_join_nested<true, false><<<(unsigned)cn, kNT, sizeof(NestedSmem), s>>>(A, cn);
       else
-        k_join_nested<false, false><<<(unsigned)cn, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+        k_join_nested<false, false><<<(unsigned)cn, kNT, sizeof(NestedSmem), s>>>(A, cn);
     } else {
       const void* fn = emit ? (const void*)k_join_nested<true, true>
                             : (const void*)k_join_nested<false, true>;
       int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinThreads,
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT,
                                                         sizeof(NestedSmem)) != cudaSuccess ||
           per_sm < 1)
         per_sm = 1;
       const i64 grid = std::min<i64>(cn, (i64)per_sm * num_sms());
       if (emit)
-        k_join_nested<true, true><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+        k_join_nested<true, true><<<(unsigned)grid, kNT, sizeof(NestedSmem), s>>>(A, cn);
       else
-        k_join_nested<false, true><<<(unsigned)grid, kJoinThreads, sizeof(NestedSmem), s>>>(A, cn);
+        k_join_nested<false, true><<<(unsigned)grid, kNT, sizeof(NestedSmem), s>>>(A, cn);
     }
   }
   if (rest > 0) {
