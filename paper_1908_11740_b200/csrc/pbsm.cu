@@ -1587,11 +1587,6 @@ struct TileInfo {  // one 16-byte shared-memory read per pair test
   float inv_ns;    // 1 / |S_T|
 };
 
-#ifndef PBSM_NESTED_PERSIST
-#define PBSM_NESTED_PERSIST 0  // 1: persistent CTAs staging chunk i+1 during chunk i (measured slower)
-#endif
-constexpr int kNestedBufs = PBSM_NESTED_PERSIST ? 2 : 1;
-
 struct NestedBuf {               // one staged chunk
   ulonglong2 ax[kCapN];          // {xl | label, xu} per staged entry (R range, then S range)
   double2 ay[kCapN];             // {yl, yu}
@@ -1600,7 +1595,7 @@ struct NestedBuf {               // one staged chunk
 };
 
 struct NestedSmem {
-  NestedBuf buf[kNestedBufs];
+  NestedBuf buf;
   TileInfo ti[kMaxTilesN];
   u32 tb[kMaxTilesN + 33];       // tile pair-prefix boundaries (tb[nt] = pair total),
                                  // then 32 sentinels (no bounds check per warp-step)
@@ -1812,63 +1807,36 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
   }
 }
 
-// PERSIST = false: one CTA per chunk (chunks handed out by ticket in the
-// ordered mode, whose look-back needs launch order).  PERSIST = true
-// (unordered): a resident grid walks chunks c = blockIdx.x + i * gridDim.x,
-// staging chunk i+1 with cp.async while chunk i is joined.
-template <bool EMIT, bool PERSIST>
-__global__ void __launch_bounds__(kNT, PERSIST ? 4 : 1536 / kNT) k_join_nested(JoinArgs A,
-                                                                             i64 n_chunks) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  NestedSmem& S = *reinterpret_cast<NestedSmem*>(smem_raw);
-  if (!PERSIST) {
-    if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
-      bool bad = false;
-      for (u64 t = blockIdx.x * (u64)kNT + threadIdx.x; t < A.g_tiles;
-           t += (u64)gridDim.x * kNT)
-        bad |= (A.g_cur_r[t] != A.g_end_r[t]) || (A.g_cur_s[t] != A.g_end_s[t]);
-      if (bad) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
-    }
-    __shared__ int s_unit;
-    if (A.ordered) {
-      if (threadIdx.x == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
-      __syncthreads();
-    }
-    const i64 c = A.ordered ? s_unit : blockIdx.x;
-    // (cdesc holds tiles + 2 entries, so the descriptor load is in bounds
-    // even for a unit past the plan's count: load it alongside the count)
-    const i64 n_plan = A.bounded ? (i64)A.hdr->chunks_nested : n_chunks;
-    NestedChunk k = nested_desc(A, c);
-    if (c >= n_plan) return;
-    nested_check(A, k);
-    nested_stage(S.buf[0], A, k);
-    cp_async_wait_all();
+// One CTA per chunk (chunks handed out by ticket in the ordered mode, whose
+// look-back needs launch order).  Static shared memory: the compiler then
+// addresses it with constant offsets.  (A persistent variant that staged chunk
+// i+1 with cp.async while joining chunk i was measured slower twice: more
+// resident CTAs beat the deeper pipeline.)
+template <bool EMIT>
+__global__ void __launch_bounds__(kNT, 1536 / kNT) k_join_nested(JoinArgs A, i64 n_chunks) {
+  __shared__ __align__(128) NestedSmem S;
+  if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
+    bool bad = false;
+    for (u64 t = blockIdx.x * (u64)kNT + threadIdx.x; t < A.g_tiles; t += (u64)gridDim.x * kNT)
+      bad |= (A.g_cur_r[t] != A.g_end_r[t]) || (A.g_cur_s[t] != A.g_end_s[t]);
+    if (bad) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
+  }
+  __shared__ int s_unit;
+  if (A.ordered) {
+    if (threadIdx.x == 0) s_unit = (int)atomicAdd(A.ticket, 1u);
     __syncthreads();
-    nested_chunk<EMIT>(S, S.buf[0], A, k, c);
-    return;
   }
-  if (A.bounded) n_chunks = min(n_chunks, (i64)A.hdr->chunks_nested);
-  i64 c = blockIdx.x;
-  if (c >= n_chunks) return;
+  const i64 c = A.ordered ? s_unit : blockIdx.x;
+  // (cdesc holds tiles + 2 entries, so the descriptor load is in bounds
+  // even for a unit past the plan's count: load it alongside the count)
+  const i64 n_plan = A.bounded ? (i64)A.hdr->chunks_nested : n_chunks;
   NestedChunk k = nested_desc(A, c);
+  if (c >= n_plan) return;
   nested_check(A, k);
-  nested_stage(S.buf[0], A, k);
-  cp_async_commit();
-  for (int it = 0; c < n_chunks; c += gridDim.x, ++it) {
-    const i64 cn = c + gridDim.x;
-    NestedChunk kn = k;
-    if (cn < n_chunks) {
-      kn = nested_desc(A, cn);
-      nested_check(A, kn);
-      nested_stage(S.buf[(it + 1) & (kNestedBufs - 1)], A, kn);
-    }
-    cp_async_commit();
-    cp_async_wait1();
-    __syncthreads();  // chunk c landed for every thread
-    nested_chunk<EMIT>(S, S.buf[it & (kNestedBufs - 1)], A, k, c);
-    __syncthreads();  // buffer and tables free for reuse
-    k = kn;
-  }
+  nested_stage(S.buf, A, k);
+  cp_async_wait_all();
+  __syncthreads();
+  nested_chunk<EMIT>(S, S.buf, A, k, c);
 }
 
 template <bool EMIT>
@@ -2018,15 +1986,7 @@ int set_smem_attrs() {
   e = cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(JoinSmem));
   if (e != cudaSuccess) return (int)e;
-  const void* nested_fns[] = {(const void*)k_join_nested<false, false>,
-                              (const void*)k_join_nested<true, false>,
-                              (const void*)k_join_nested<false, true>,
-                              (const void*)k_join_nested<true, true>};
-  for (const void* fn : nested_fns) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(NestedSmem));
-    if (e != cudaSuccess) return (int)e;
-  }
+
   done = true;
   return 0;
 }
@@ -2045,7 +2005,7 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   const i64 n_units = cn + rest;
   // the write guard (reads the cursors the scatter left behind) runs inside
   // the nested join when there is one, else as its own kernel
-  const bool fused_guard = cn > 0 && (ordered || !PBSM_NESTED_PERSIST);
+  const bool fused_guard = cn > 0;
   if (!fused_guard) {
     const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
                                                                   (i64)num_sms() * 8));
@@ -2078,26 +2038,11 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.g_end_s = w.cnt_s;
   A.g_tiles = fused_guard ? L.tiles : 0;
   if (cn > 0) {
-    if (ordered || !PBSM_NESTED_PERSIST) {
-      // one CTA per chunk (the ordered look-back takes tickets in launch order)
-      if (emit)
-        k_join_nested<true, false><<<(unsigned)cn, kNT, sizeof(NestedSmem), s>>>(A, cn);
-      else
-        k_join_nested<false, false><<<(unsigned)cn, kNT, sizeof(NestedSmem), s>>>(A, cn);
-    } else {
-      const void* fn = emit ? (const void*)k_join_nested<true, true>
-                            : (const void*)k_join_nested<false, true>;
-      int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kNT,
-                                                        sizeof(NestedSmem)) != cudaSuccess ||
-          per_sm < 1)
-        per_sm = 1;
-      const i64 grid = std::min<i64>(cn, (i64)per_sm * num_sms());
-      if (emit)
-        k_join_nested<true, true><<<(unsigned)grid, kNT, sizeof(NestedSmem), s>>>(A, cn);
-      else
-        k_join_nested<false, true><<<(unsigned)grid, kNT, sizeof(NestedSmem), s>>>(A, cn);
-    }
+    // one CTA per chunk (the ordered look-back takes tickets in launch order)
+    if (emit)
+      k_join_nested<true><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+    else
+      k_join_nested<false><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
   }
   if (rest > 0) {
     // the sorted/large launch keeps its own ticket (the look-back ids follow
