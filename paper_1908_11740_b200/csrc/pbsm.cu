@@ -59,7 +59,13 @@ namespace {
 
 // ---------------------------------------------------------------- constants
 constexpr int kPlanThreads = 256;
-constexpr int kPlanPer = 4;                          // tiles per thread
+#ifndef PBSM_PLAN_PER
+#define PBSM_PLAN_PER 4
+#endif
+#ifndef PBSM_PLAN_MINB
+#define PBSM_PLAN_MINB 4
+#endif
+constexpr int kPlanPer = PBSM_PLAN_PER;               // tiles per thread
 constexpr int kPlanTile = kPlanThreads * kPlanPer;   // 1024 tiles per CTA
 constexpr int kNV = 12;                              // plan scan lanes (see tile_vals)
 constexpr int kNTot = kNV;                           // partials row stride
@@ -964,7 +970,7 @@ struct PlanOut {
   u32* lpre;
 };
 
-__global__ void __launch_bounds__(kPlanThreads) k_plan_apply(u32* __restrict__ cr,
+__global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32* __restrict__ cr,
                                                              u32* __restrict__ cs, u64 T, u64 nb,
                                                              i64 nm,
                                                              const u64* __restrict__ partials,

@@ -28,7 +28,7 @@ import numpy as np
 
 __all__ = ["canonical_pairs", "combine_counts", "distribute", "distributed_join",
            "distributed_join_slices", "exchange_counts", "gather_pairs", "plan_strips",
-           "plan_strips_distributed", "row_range", "strip_inputs"]
+           "plan_strips_distributed", "row_range", "strip_inputs", "strip_join"]
 
 
 def _tile_index(p: np.ndarray, k: int) -> np.ndarray:
@@ -141,9 +141,19 @@ def distributed_join(r, s, k: int, device=None, collect: bool = True):
     lo, hi = cuts[rank], cuts[rank + 1]
     rr = strip_inputs(r, k, lo, hi)
     ss = rr if s is r else strip_inputs(s, k, lo, hi)
+    return strip_join(rr, ss, k, lo, hi, device, collect=collect)
+
+
+def strip_join(rr, ss, k: int, row_lo: int, row_hi: int, device=None, collect: bool = True):
+    """One rank's join of its strip from host arrays already split
+    (``strip_inputs``; pinned arrays copy without staging): host→device,
+    the strip pipeline, the count exchange.  Returns (DeviceJoinResult,
+    exchange dict)."""
+    from . import device as dev
+
     rd = dev.to_device(rr, device)
-    sd = rd if s is r else dev.to_device(ss, device)
-    res = dev.run_join(rd, sd, k, k, collect=collect, row_lo=lo, row_hi=hi)
+    sd = rd if ss is rr else dev.to_device(ss, device)
+    res = dev.run_join(rd, sd, k, k, collect=collect, row_lo=row_lo, row_hi=row_hi)
     ex = exchange_counts(res.count, res.header["a_r"], res.header["a_s"], device=device)
     return res, ex
 

@@ -433,3 +433,22 @@ def test_write_guard_detects_a_skipped_scatter(golden):
         h2 = _native.Header()
         lib.pbsm_read_header(wsp, C.byref(h2), st)
         assert h2.error & _native.ERR_OFFSET_MISMATCH, nested_max
+
+
+def test_strip_join_api_reassembles(golden):
+    """parallel.strip_join (the per-rank public call the multi-GPU bench's
+    end-to-end leg uses) on every strip of a 3-way plan, one after another:
+    the union of the strips' pairs is the reference list."""
+    from paper_1908_11740_b200 import parallel
+
+    g = golden["configs"]
+    r, s, k = make_config(2, float(g["cfg2_scale"]))
+    cuts = parallel.plan_strips(r, s, k, 3)
+    parts = []
+    for lo, hi in zip(cuts, cuts[1:]):
+        res, ex = parallel.strip_join(parallel.strip_inputs(r, k, lo, hi),
+                                      parallel.strip_inputs(s, k, lo, hi), k, lo, hi, "cuda")
+        assert ex["pairs"] == res.count
+        parts.append(res.pairs.cpu().numpy())
+    got = oracle.sorted_pairs(np.concatenate(parts))
+    assert np.array_equal(got, g["cfg2_pairs"])
