@@ -94,7 +94,11 @@ constexpr int kCapN = kChunkBN + kLmax;  // max entries of a nested chunk
 #define PBSM_NESTED_THREADS 256
 #endif
 constexpr int kNT = PBSM_NESTED_THREADS;  // threads of a nested-join CTA
+#ifndef PBSM_NESTED_ROWS
+#define PBSM_NESTED_ROWS 1  // 1: lane per lead entry; 0: pair-flattened lanes
+#endif
 constexpr int kMaxTilesN = kCapN / 2;
+static_assert(kCapN <= 512 && kLmax <= 128, "nested row descriptors: 9-bit positions, 7-bit counts");
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
 constexpr int kLargeOther = 2048;         // other-side entries per large work item
 
@@ -1602,9 +1606,14 @@ struct NestedBuf {               // one staged chunk
 
 struct NestedSmem {
   NestedBuf buf;
-  TileInfo ti[kMaxTilesN];
-  u32 tb[kMaxTilesN + 33];       // tile pair-prefix boundaries (tb[nt] = pair total),
-                                 // then 32 sentinels (no bounds check per warp-step)
+  // row form: per lead entry pos | o0 << 9 | |other| << 18 | R-leads << 25
+  // (positions < kCapN = 512; |other| <= 64: the smaller side of a tile of
+  // <= kLmax = 128 entries)
+  u32 lead[PBSM_NESTED_ROWS ? kCapN : 1];
+  // flat form: tile table, pair-prefix boundaries (tb[nt] = pair total) and
+  // 32 sentinels (no bounds check per warp-step)
+  TileInfo ti[PBSM_NESTED_ROWS ? 1 : kMaxTilesN];
+  u32 tb[PBSM_NESTED_ROWS ? 1 : kMaxTilesN + 33];
   u64 wtot[kNT / 32 + 1];
   u32 scan32[kNT / 32 + 1];
   u32 hits[kNT / 32][kHitCap];  // pass-1 hits: r position | s position << 16
@@ -1699,51 +1708,44 @@ __device__ __forceinline__ void nested_stage(NestedBuf& B, const JoinArgs& A,
   for (int t = threadIdx.x; t < k.nt; t += kNT) cp_async16(&B.jr[t], A.jrec[0] + k.d0.x + t);
 }
 
-// One staged chunk (B landed and visible): tile table, count, reserve, emit.
-template <bool EMIT>
-__device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
-                                             const JoinArgs& A, const NestedChunk& k, i64 c) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nt = k.nt, NR = k.NR;
-  // tile table (kTPT consecutive tiles per thread)
-  constexpr int kTPT = (kMaxTilesN + kNT - 1) / kNT;
-  uint4 tr[kTPT];
-  u32 np = 0;
-#pragma unroll
-  for (int h = 0; h < kTPT; ++h) {
-    const int t = kTPT * tid + h;
-    tr[h] = t < nt ? B.jr[t] : make_uint4(0, 0, 0, 0);
-    np += tr[h].z * tr[h].w;
-  }
-  u32 tot;
-  u32 pre = block_excl_scan32<kNT>(np, &tot, S.scan32);
-#pragma unroll
-  for (int h = 0; h < kTPT; ++h) {
-    const int t = kTPT * tid + h;
-    if (t < nt) {
-      TileInfo ti;
-      ti.p0 = pre;
-      ti.rs0 = (tr[h].x - k.d0.y) | ((u32)(NR + (int)(tr[h].y - k.d0.z)) << 16);
-      ti.ns = tr[h].w;
-      ti.inv_ns = 1.0f / (float)tr[h].w;
-      S.ti[t] = ti;
-      S.tb[t] = pre;
-      pre += tr[h].z * tr[h].w;
+// Row form: one lane per entry of each tile's larger ("lead") side, looping
+// over the tile's other side (<= 32 entries with the default cost model,
+// |R_T|*|S_T| <= 1024; <= 64 for any nested tile, |R_T|+|S_T| <= 128).  No per-pair index arithmetic; a warp runs max(|other|)
+// steps over its 32 lead entries.  body(hit, pr, ps, ballot) is called by
+// every lane of every step.
+template <typename Body>
+__device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf& B, u32 e_beg,
+                                            u32 e_end, int lane, Body&& body) {
+  for (u32 g = e_beg; g < e_end; g += 32u) {
+    const u32 ei = g + lane;
+    const bool valid = ei < e_end;
+    const u32 d = valid ? S.lead[ei] : 0u;
+    const u32 pos = d & 511u, o0 = (d >> 9) & 511u, nO = valid ? (d >> 18) & 127u : 0u;
+    const bool lr = (d >> 25) & 1u;
+    const ulonglong2 mx = B.ax[pos];
+    const double2 my = B.ay[pos];
+    const double mxu = __longlong_as_double((long long)mx.y);
+    const u32 steps = __reduce_max_sync(0xffffffffu, nO);
+    for (u32 j = 0; j < steps; ++j) {
+      bool hit = false;
+      if (j < nO) {
+        const ulonglong2 ox = B.ax[o0 + j];
+        const double2 oy = B.ay[o0 + j];
+        hit = pair_ok(mx.x, mxu, my.x, my.y, ox.x, __longlong_as_double((long long)ox.y), oy.x,
+                      oy.y);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      body(hit, lr ? pos : o0 + j, lr ? o0 + j : pos, m);
     }
   }
-  if (tid <= 32) S.tb[nt + tid] = tid == 0 ? (u32)tot : 0xffffffffu;
-  __syncthreads();
-  const u32 NP = (u32)tot;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  // each warp owns one contiguous slice of the pair index space, so the tile
-  // of its current step only moves forward: one binary search per warp
-  constexpr int kW = kNT / 32;
-  const u32 per = ((NP + kW - 1) / kW + 31u) & ~31u;
-  const u32 q_beg = min(NP, (u32)warp * per), q_end = min(NP, q_beg + per);
-  const int lt_beg = q_beg < NP ? nested_tile_of(S, nt, q_beg) : 0;
-  // pass 1: count (and keep each warp-step's hit ballot for pass 2)
-  u32 wcnt = 0;
-  int lt = lt_beg;
+}
+
+// Pair-flattened form (PBSM_NESTED_ROWS=0): every (r, s) pair of every tile
+// gets an index (tile-major, then r, then s); lane q of a warp-step tests pair q.
+template <typename Body>
+__device__ __forceinline__ void nested_flat(const NestedSmem& S, const NestedBuf& B, int nt,
+                                            u32 q_beg, u32 q_end, int lt, int lane,
+                                            Body&& body) {
   for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
     const u32 q = q0 + lane;
     const int t = nested_step_tile(S, nt, q0, lt, lane);
@@ -1753,21 +1755,78 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
       nested_pair(S, t, q, pr, ps);
       hit = nested_hit(B, pr, ps);
     }
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (EMIT && hit) {  // ballot-compacted into the warp's hit list
+    body(hit, (u32)pr, (u32)ps, __ballot_sync(0xffffffffu, hit));
+  }
+}
+
+// One staged chunk (B landed and visible): tables, count, reserve, emit.
+template <bool EMIT>
+__device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
+                                             const JoinArgs& A, const NestedChunk& k, i64 c) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nt = k.nt, NR = k.NR;
+  constexpr int kTPT = (kMaxTilesN + kNT - 1) / kNT;
+  constexpr int kW = kNT / 32;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // per-tile table (kTPT consecutive tiles per thread)
+  uint4 tr[kTPT];
+  u32 w = 0;
+#pragma unroll
+  for (int h = 0; h < kTPT; ++h) {
+    const int t = kTPT * tid + h;
+    tr[h] = t < nt ? B.jr[t] : make_uint4(0, 0, 0, 0);
+    w += PBSM_NESTED_ROWS ? max(tr[h].z, tr[h].w) : tr[h].z * tr[h].w;
+  }
+  u32 W;  // rows: lead entries of the chunk; flat: pairs of the chunk
+  u32 pre = block_excl_scan32<kNT>(w, &W, S.scan32);
+#pragma unroll
+  for (int h = 0; h < kTPT; ++h) {
+    const int t = kTPT * tid + h;
+    if (t >= nt) continue;
+    const u32 r0 = tr[h].x - k.d0.y, s0 = (u32)NR + (tr[h].y - k.d0.z);
+    if (PBSM_NESTED_ROWS) {
+      const bool lr = tr[h].z >= tr[h].w;
+      const u32 nL = lr ? tr[h].z : tr[h].w, nO = lr ? tr[h].w : tr[h].z;
+      const u32 l0 = lr ? r0 : s0, o0 = lr ? s0 : r0;
+      const u32 d = (o0 << 9) | (nO << 18) | ((u32)lr << 25);
+      for (u32 i = 0; i < nL; ++i) S.lead[pre + i] = (l0 + i) | d;
+      pre += nL;
+    } else {
+      TileInfo ti;
+      ti.p0 = pre;
+      ti.rs0 = r0 | (s0 << 16);
+      ti.ns = tr[h].w;
+      ti.inv_ns = 1.0f / (float)tr[h].w;
+      S.ti[t] = ti;
+      S.tb[t] = pre;
+      pre += tr[h].z * tr[h].w;
+    }
+  }
+  if (!PBSM_NESTED_ROWS && tid <= 32) S.tb[nt + tid] = tid == 0 ? W : 0xffffffffu;
+  __syncthreads();
+  // each warp owns one contiguous, 32-aligned slice of the work index space
+  const u32 per = ((W + kW - 1) / kW + 31u) & ~31u;
+  const u32 w_beg = min(W, (u32)warp * per), w_end = min(W, w_beg + per);
+  const int lt_beg = (!PBSM_NESTED_ROWS && w_beg < W) ? nested_tile_of(S, nt, w_beg) : 0;
+  // pass 1: count, keeping the warp's hits (ballot-compacted) in its list
+  u32 wcnt = 0;
+  auto count = [&](bool hit, u32 pr, u32 ps, unsigned m) {
+    if (EMIT && hit) {
       const u32 o = wcnt + __popc(m & lt_mask);
-      if (o < kHitCap) S.hits[warp][o] = (u32)pr | ((u32)ps << 16);
+      if (o < kHitCap) S.hits[warp][o] = pr | (ps << 16);
     }
     wcnt += __popc(m);
-  }
+  };
+  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, lane, count);
+  else nested_flat(S, B, nt, w_beg, w_end, lt_beg, lane, count);
   if (lane == 0) S.wtot[warp] = wcnt;
   __syncthreads();
   if (tid == 0) {
     u64 t = 0;
-    for (int w = 0; w < kW; ++w) {
-      const u64 v = S.wtot[w];
-      S.wtot[w] = t;
-      t += v;
+    for (int v = 0; v < kW; ++v) {
+      const u64 x = S.wtot[v];
+      S.wtot[v] = t;
+      t += x;
     }
     if (!EMIT) {
       if (t) atomicAdd(A.total, t);
@@ -1794,23 +1853,15 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     }
     return;
   }
-  lt = lt_beg;
-  for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
-    const u32 q = q0 + lane;
-    const int t = nested_step_tile(S, nt, q0, lt, lane);
-    int pr = 0, ps = 0;
-    bool hit = false;
-    if (q < q_end) {
-      nested_pair(S, t, q, pr, ps);
-      hit = nested_hit(B, pr, ps);
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
+  auto emit = [&](bool hit, u32 pr, u32 ps, unsigned m) {
     if (hit) {
       const i64 o = __popc(m & lt_mask);
       *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(B.aid[pr], B.aid[ps]);
     }
     out += 2 * (i64)__popc(m);
-  }
+  };
+  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, lane, emit);
+  else nested_flat(S, B, nt, w_beg, w_end, lt_beg, lane, emit);
 }
 
 // One CTA per chunk (chunks handed out by ticket in the ordered mode, whose
