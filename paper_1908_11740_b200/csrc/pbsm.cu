@@ -1715,8 +1715,8 @@ __device__ __forceinline__ void nested_stage(NestedBuf& B, const JoinArgs& A,
 // every lane of every step.
 template <typename Body>
 __device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf& B, u32 e_beg,
-                                            u32 e_end, int lane, Body&& body) {
-  for (u32 g = e_beg; g < e_end; g += 32u) {
+                                            u32 e_end, u32 e_step, int lane, Body&& body) {
+  for (u32 g = e_beg; g < e_end; g += e_step) {
     const u32 ei = g + lane;
     const bool valid = ei < e_end;
     const u32 d = valid ? S.lead[ei] : 0u;
@@ -1804,9 +1804,13 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
   }
   if (!PBSM_NESTED_ROWS && tid <= 32) S.tb[nt + tid] = tid == 0 ? W : 0xffffffffu;
   __syncthreads();
-  // each warp owns one contiguous, 32-aligned slice of the work index space
+  // flat form: each warp owns one contiguous, 32-aligned slice of the pair
+  // index space (its tile only moves forward); row form: warps take groups
+  // of 32 lead entries round-robin (the groups' step counts differ, so
+  // interleaving balances the warps before the barrier)
   const u32 per = ((W + kW - 1) / kW + 31u) & ~31u;
-  const u32 w_beg = min(W, (u32)warp * per), w_end = min(W, w_beg + per);
+  const u32 w_beg = PBSM_NESTED_ROWS ? 32u * warp : min(W, (u32)warp * per);
+  const u32 w_end = PBSM_NESTED_ROWS ? W : min(W, w_beg + per);
   const int lt_beg = (!PBSM_NESTED_ROWS && w_beg < W) ? nested_tile_of(S, nt, w_beg) : 0;
   // pass 1: count, keeping the warp's hits (ballot-compacted) in its list
   u32 wcnt = 0;
@@ -1817,7 +1821,7 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     }
     wcnt += __popc(m);
   };
-  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, lane, count);
+  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, 32u * kW, lane, count);
   else nested_flat(S, B, nt, w_beg, w_end, lt_beg, lane, count);
   if (lane == 0) S.wtot[warp] = wcnt;
   __syncthreads();
@@ -1860,7 +1864,7 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     }
     out += 2 * (i64)__popc(m);
   };
-  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, lane, emit);
+  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, 32u * kW, lane, emit);
   else nested_flat(S, B, nt, w_beg, w_end, lt_beg, lane, emit);
 }
 
@@ -1870,7 +1874,10 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
 // i+1 with cp.async while joining chunk i was measured slower twice: more
 // resident CTAs beat the deeper pipeline.)
 template <bool EMIT>
-__global__ void __launch_bounds__(kNT, 1536 / kNT) k_join_nested(JoinArgs A, i64 n_chunks) {
+#ifndef PBSM_NESTED_MINB
+#define PBSM_NESTED_MINB (1536 / kNT)
+#endif
+__global__ void __launch_bounds__(kNT, PBSM_NESTED_MINB) k_join_nested(JoinArgs A, i64 n_chunks) {
   __shared__ __align__(128) NestedSmem S;
   if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
     bool bad = false;
