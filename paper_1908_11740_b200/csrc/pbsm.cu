@@ -155,7 +155,7 @@ struct __align__(32) Half {  // the MBR half of a record: one sector
 
 // ---------------------------------------------------------------- workspace
 struct WsLayout {
-  size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec[2], je[2], cdesc[2], lrec, lpre,
+  size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec[2], cdesc[2], lrec, lpre,
       partials, bc[2], bo, bscan, total;
   u64 tiles;
   u64 nblocks;
@@ -178,7 +178,6 @@ inline WsLayout ws_layout(int kx, int ky, int row_lo, int row_hi) {
   L.cur_s = o; o = align_up(o + 4 * T, 256);
   for (int q = 0; q < 2; ++q) {  // 0 = nested tiles, 1 = sorted tiles
     L.jrec[q] = o; o = align_up(o + 16 * T, 256);
-    L.je[q] = o; o = align_up(o + 4 * (T + 1), 256);
     L.cdesc[q] = o; o = align_up(o + 16 * (T + 2), 256);
   }
   L.lrec = o; o = align_up(o + 16 * T, 256);
@@ -198,7 +197,6 @@ struct Ws {
   double* bx;
   double* by;
   u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *lpre;
-  u32* je[2];
   uint4* cdesc[2];  // chunk c: {first tile j0, r_start, s_start, -}; [n_chunks] = ends
   uint4* jrec[2];   // {r_start, s_start, nR, nS}
   uint4* lrec;
@@ -221,7 +219,6 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
   w.cur_s = (u32*)(b + L.cur_s);
   for (int q = 0; q < 2; ++q) {
     w.jrec[q] = (uint4*)(b + L.jrec[q]);
-    w.je[q] = (u32*)(b + L.je[q]);
     w.cdesc[q] = (uint4*)(b + L.cdesc[q]);
   }
   w.lrec = (uint4*)(b + L.lrec);
@@ -912,8 +909,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
 // by k_plan_apply); the last CTA to finish writes the header.
 constexpr int kPartThreads = 1024;
 __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict__ partials, u64 nb,
-                                                                 pbsm_header* hdr, u32* je_n,
-                                                                 u32* je_s, u32* lpre) {
+                                                                 pbsm_header* hdr, uint4* cd_n,
+                                                                 uint4* cd_s, u32* lpre) {
   __shared__ u64 sh[kPartThreads / 32 + 1];
   __shared__ bool last;
   u64* row = partials + (u64)blockIdx.x * (nb + 1);
@@ -955,13 +952,16 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
     const u64 lr = c[L_NA] + c[L_SA] + c[L_LA], ls = c[L_NB] + c[L_SB] + c[L_LB];
     hdr->list_r = (i64)lr;
     hdr->list_s = (i64)ls;
-    hdr->chunks_nested = 0;
-    hdr->chunks_sorted = 0;
+    // chunk counts and the closing descriptors (see k_plan_apply)
+    const u64 wn = c[L_NA] + c[L_NB], ws = c[L_SA] + c[L_SB];
+    const u64 chn = wn ? (wn - 1) / kChunkBN + 1 : 0, chs = ws ? (ws - 1) / kChunkB + 1 : 0;
+    hdr->chunks_nested = (i64)chn;
+    hdr->chunks_sorted = (i64)chs;
+    cd_n[chn] = make_uint4((u32)c[L_NF], (u32)c[L_NA], (u32)c[L_NB], 0u);
+    cd_s[chs] = make_uint4((u32)c[L_SF], (u32)(c[L_NA] + c[L_SA]), (u32)(c[L_NB] + c[L_SB]), 0u);
     hdr->pairs = 0;
     if (c[L_A] >= kSkip || c[L_B] >= kSkip || lr >= kSkip || ls >= kSkip || c[L_LI] >= kSkip)
       hdr->error |= PBSM_ERR_TOTAL_RANGE;
-    je_n[c[L_NF]] = (u32)(c[L_NA] + c[L_NB]);   // sentinels: end of the last tile
-    je_s[c[L_SF]] = (u32)(c[L_SA] + c[L_SB]);
     lpre[c[L_LF]] = (u32)c[L_LI];
   }
 }
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
 struct PlanOut {
   u32 *cur_r, *cur_s;
   uint4* jrec[2];
-  u32* je[2];
+  uint4* cdesc[2];
   uint4* lrec;
   u32* lpre;
 };
@@ -1045,12 +1045,20 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
     sa[threadIdx.x * kPlanPer + i] = r0;
     sb[threadIdx.x * kPlanPer + i] = s0;
     if (t < T) {
-      if (kind == kNested) {
-        P.jrec[0][g[L_NF]] = make_uint4(r0, s0, a[i], b[i]);
-        P.je[0][g[L_NF]] = (u32)(g[L_NA] + g[L_NB]);
-      } else if (kind == kSorted) {
-        P.jrec[1][g[L_SF]] = make_uint4(r0, s0, a[i], b[i]);
-        P.je[1][g[L_SF]] = (u32)(g[L_SA] + g[L_SB]);
+      // chunks: consecutive tiles of one strategy whose LAST entry falls in the
+      // same bucket of B entries; a tile starts chunk c when its end is in
+      // bucket c and its start (the previous tile's end) is not.  A tile holds
+      // <= kLmax <= B entries, so it crosses at most one bucket boundary and a
+      // chunk holds < B + kLmax entries.  The plan's last CTA writes the
+      // closing descriptor and the chunk counts (k_plan_partials).
+      if (kind == kNested || kind == kSorted) {
+        const bool q = kind == kSorted;  // (selects, no indexing: keeps P in registers)
+        const u32 jj = (u32)(q ? g[L_SF] : g[L_NF]);
+        (q ? P.jrec[1] : P.jrec[0])[jj] = make_uint4(r0, s0, a[i], b[i]);
+        const i64 st = (i64)(q ? g[L_SA] + g[L_SB] : g[L_NA] + g[L_NB]);
+        const i64 B = q ? kChunkB : kChunkBN;
+        const i64 ce = (st + a[i] + b[i] - 1) / B, cs = st ? (st - 1) / B : -1;
+        if (cs < ce) (q ? P.cdesc[1] : P.cdesc[0])[ce] = make_uint4(jj, r0, s0, 0u);
       } else if (kind == kLarge) {
         P.lrec[g[L_LF]] = make_uint4(r0, s0, a[i], b[i]);
         P.lpre[g[L_LF]] = (u32)g[L_LI];
@@ -1074,30 +1082,6 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
   }
 }
 
-// chunk c = the tiles (of one strategy) whose exclusive entry prefix lies in
-// [c*B, (c+1)*B); a chunk holds < B + kLmax = kCap entries.  Its descriptor
-// {first tile, R list start, S list start} plus the next one's give the
-// chunk's three contiguous ranges (tile records, R entries, S entries).
-__global__ void k_chunks(const u32* __restrict__ je, const uint4* __restrict__ jrec,
-                         uint4* __restrict__ cdesc, pbsm_header* hdr, int which) {
-  const i64 nj = which ? hdr->n_sorted : hdr->n_nested;
-  const u32 B = which ? (u32)kChunkB : (u32)kChunkBN;
-  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nj;
-       j += (i64)gridDim.x * blockDim.x) {
-    const i64 c = je[j] / B;
-    const i64 cp = j == 0 ? -1 : (i64)(je[j - 1] / B);
-    if (cp < c) {
-      const uint4 r = jrec[j];
-      for (i64 cc = cp + 1; cc <= c; ++cc) cdesc[cc] = make_uint4((u32)j, r.x, r.y, 0u);
-    }
-    if (j == nj - 1) {
-      const uint4 r = jrec[j];
-      cdesc[c + 1] = make_uint4((u32)nj, r.x + r.z, r.y + r.w, 0u);
-      if (which) hdr->chunks_sorted = c + 1;
-      else hdr->chunks_nested = c + 1;
-    }
-  }
-}
 
 // ---------------------------------------------------------------- generic scan
 // exclusive scan of u32 counts into u64 bases; base[n] = total (ε refinement)
@@ -1296,7 +1280,7 @@ __device__ __forceinline__ void stage_chunk(Smem& S, const JoinArgs& A, int whic
   if (tid == 0) {
     const int NR = (int)(d1.y - d0.y);
     const int NS = (int)(d1.z - d0.z);
-    // a chunk never exceeds the staging buffer by construction (k_chunks);
+    // a chunk never exceeds the staging buffer by construction (k_plan_apply);
     // if it somehow did, flag it and contribute 0 pairs (no early return:
     // the ordered mode's look-back chain must still be fed)
     const bool fits = nt > 0 && NR > 0 && NS > 0 && NR + NS <= kCap && nt <= kMaxTiles;
@@ -1684,7 +1668,7 @@ __device__ __forceinline__ NestedChunk nested_desc(const JoinArgs& A, i64 c) {
 }
 
 // a chunk that breaks the plan invariants (never, by construction of
-// k_chunks): flag it and contribute 0 pairs (no early return: the ordered
+// k_plan_apply): flag it and contribute 0 pairs (no early return: the ordered
 // look-back chain must still be fed)
 __device__ __forceinline__ void nested_check(const JoinArgs& A, NestedChunk& k) {
   if (!k.ok) {
@@ -2177,22 +2161,19 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
   const i64 nm = nested_max < 0 ? (i64)kNestedMax : (i64)nested_max;
   k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles, nm,
                                                               w.partials, w.hdr);
-  k_plan_partials<<<kNV, kPartThreads, 0, s>>>(w.partials, w.nblocks, w.hdr, w.je[0], w.je[1], w.lpre);
+  k_plan_partials<<<kNV, kPartThreads, 0, s>>>(w.partials, w.nblocks, w.hdr, w.cdesc[0],
+                                                w.cdesc[1], w.lpre);
   PlanOut P;
   P.cur_r = w.cur_r;
   P.cur_s = w.cur_s;
   for (int q = 0; q < 2; ++q) {
     P.jrec[q] = w.jrec[q];
-    P.je[q] = w.je[q];
+    P.cdesc[q] = w.cdesc[q];
   }
   P.lrec = w.lrec;
   P.lpre = w.lpre;
   k_plan_apply<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles,
                                                              w.nblocks, nm, w.partials, P);
-  const unsigned blocks =
-      (unsigned)std::max<i64>(1, std::min<i64>((i64)((w.tiles + 255) / 256), (i64)num_sms() * 8));
-  for (int q = 0; q < 2; ++q)
-    k_chunks<<<blocks, 256, 0, s>>>(w.je[q], w.jrec[q], w.cdesc[q], w.hdr, q);
   return launch_status();
 }
 
