@@ -1185,7 +1185,10 @@ struct ChunkSmem {
   int unit, nt, NR, NS;
 };
 
-constexpr int kLargeHitCap = 4096;  // hits of a large work item kept for the emit
+#ifndef PBSM_LARGE_HITS
+#define PBSM_LARGE_HITS 4096
+#endif
+constexpr int kLargeHitCap = PBSM_LARGE_HITS;  // hits of a large work item kept for the emit
 struct LargeSmem {
   Rec other[kCap];
   u32 hit[kLargeHitCap];        // lead thread | other index (in the item) << 8

@@ -103,9 +103,19 @@ _VALIDATION = (
 _VALIDATION_BITS = sum(b for b, _ in _VALIDATION)
 
 
+_hdr_pinned: dict = {}
+
+
 def _read_header(lib, ws, stream, allow=0) -> _native.Header:
-    h = _native.Header()
-    _native.check(lib.pbsm_read_header(ws.data_ptr(), C.byref(h), stream), "pbsm_read_header")
+    # into page-locked memory: a pageable destination would go through the
+    # driver's staging copy on this (synchronising) path
+    buf = _hdr_pinned.get("buf")
+    if buf is None:
+        buf = _hdr_pinned["buf"] = torch.empty(C.sizeof(_native.Header), dtype=torch.uint8,
+                                               pin_memory=True)
+    dst = C.cast(C.c_void_p(buf.data_ptr()), C.POINTER(_native.Header))
+    _native.check(lib.pbsm_read_header(ws.data_ptr(), dst, stream), "pbsm_read_header")
+    h = _native.Header.from_buffer_copy(C.string_at(buf.data_ptr(), C.sizeof(_native.Header)))
     for bit, msg in _VALIDATION:
         if h.error & bit:
             raise ValueError(msg)
