@@ -16,11 +16,17 @@
 //  4. count → emit pair writer                  ← sweep_count / sweep_collect
 //                                                 (_kernels.pyx:304-341) and the
 //                                                 aggregation (engine.py:293-309)
-//  (2)-(4) are one kernel, k_join: a CTA stages a chunk of join tiles in shared
-//  memory with TMA bulk copies, sorts every (tile, side) segment there, counts
-//  its pairs, learns its output offset by a decoupled look-back over the
-//  preceding chunks, and emits.  Tiles too large for one CTA's shared memory
-//  are split into work items handled by the same kernel (nested loop).
+//  (2)-(4) run as per-tile mini-joins chosen by a cost model in the plan:
+//       k_join_nested  small tiles (the default for the BASELINE configs): a CTA
+//                      stages a chunk of consecutive tiles with cp.async, one
+//                      lane per entry of each tile's larger side tests the
+//                      other side, hits go to per-warp lists, one atomic
+//                      reserves the chunk's output range, then it emits
+//       k_join         medium tiles: TMA-staged chunk, per-(tile, side) rank
+//                      sort by x-lower + the forward scan (Alg. 1); large
+//                      tiles: work items of 256 lead x 2048 other entries
+//  The output range is reserved with one atomic per unit (the reference's pair
+//  list is unordered) or, in ordered mode, by a decoupled look-back.
 //
 // Duplicate avoidance.  The reference keeps a pair in tile T iff
 // max(r.xl,s.xl) >= T.xl and max(r.yl,s.yl) >= T.yl (Eq. 1,
@@ -806,7 +812,7 @@ __global__ void k_guard(const u32* __restrict__ cur_r, const u32* __restrict__ e
 // (compute_segment_offsets, partition.py:151-164): each input's list holds
 // the nested tiles, then the sorted tiles, then the large tiles, each region
 // in tile order — so a chunk of consecutive nested (or sorted) tiles is one
-// contiguous range per input, fetched by one TMA bulk copy.  Within a CTA the
+// contiguous range per input, fetched by one bulk async copy.  Within a CTA the
 // lanes are u32 (a CTA's sums never exceed the u32-checked totals); the
 // per-CTA partial sums are u64.
 enum TileKind { kNone = 0, kNested = 1, kSorted = 2, kLarge = 3 };
@@ -1563,12 +1569,12 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
   }
 }
 
-// ---- nested mini-joins: one CTA per chunk, pairs flattened over lanes
-// Every (r, s) pair of every tile in the chunk gets an index (tile-major,
-// then r, then s); thread q of a warp-step tests pair q.  All lanes stay busy
-// however small and lopsided the tiles are, and the hits of a warp-step are
-// compacted with a ballot + popcount into consecutive output slots (one
-// coalesced 16-byte store per hit).
+// ---- nested mini-joins: one CTA per chunk of small tiles
+// Two lane mappings (PBSM_NESTED_ROWS): the row form (default) gives a lane
+// each entry of a tile's larger side and loops over the smaller side; the
+// flat form numbers every (r, s) pair of the chunk and gives lane q pair q.
+// Hits are ballot-compacted into per-warp lists and emitted after the
+// chunk's single output reservation (one coalesced 16-byte store per hit).
 //
 // Staging: per-thread 16-byte async copies (cp.async) land each 64-byte list
 // record directly in the layout the pair tests read — {xl|label, xu} and
