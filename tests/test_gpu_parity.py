@@ -452,3 +452,23 @@ def test_strip_join_api_reassembles(golden):
         parts.append(res.pairs.cpu().numpy())
     got = oracle.sorted_pairs(np.concatenate(parts))
     assert np.array_equal(got, g["cfg2_pairs"])
+
+
+def test_cli_join_matches_reference(tmp_path, golden, capsys):
+    """`python -m paper_1908_11740_b200 join` (the reference CLI's join
+    subcommand, cli.py:124-158) on SJB1 files: the printed result_count and
+    the saved pair list are the reference's."""
+    from paper_1908_11740_b200 import cli
+    from paper_1908_11740_b200 import io as pio
+
+    g = golden["configs"]
+    r, s, k = make_config(1, float(g["cfg1_scale"]))
+    pio.save_mbr_binary(pb.RectBatch(*r), tmp_path / "r.bin")
+    pio.save_mbr_binary(pb.RectBatch(*s), tmp_path / "s.bin")
+    out = tmp_path / "pairs.npy"
+    rc = cli.main(["join", "--left", str(tmp_path / "r.bin"), "--right", str(tmp_path / "s.bin"),
+                   "--layout", "2d", "--k", str(k), "--collect", "--pairs-out", str(out)])
+    assert rc == 0
+    text = capsys.readouterr().out
+    assert f"result_count={int(g['cfg1_count'])}" in text
+    assert np.array_equal(oracle.sorted_pairs(np.load(out)), g["cfg1_pairs"])
