@@ -152,6 +152,7 @@ struct __align__(64) Rec {
   u64 pad[3];
 };
 static_assert(sizeof(Rec) == 64, "record size");
+static_assert(sizeof(pbsm_header) % 4 == 0 && sizeof(pbsm_header) <= 256 * 4, "header reset");
 static_assert(sizeof(Rec) == sizeof(pbsm_entry), "entry layout");
 
 struct __align__(32) Half {  // the MBR half of a record: one sector
@@ -397,11 +398,29 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
 }
 
 // ---------------------------------------------------------------- init
-__global__ void k_bounds(double* bx, int kx, double* by, int ky) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+// One launch for the whole per-join reset (a memset per buffer cost a host
+// API call each while the GPU sat idle at the start of the join): zero the
+// header and both inputs' per-tile counters, build the boundary tables.
+__global__ void k_init(pbsm_header* hdr, u32* cnt_r, u32* cnt_s, u64 T, double* bx, int kx,
+                       double* by, int ky) {
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  const u64 nt = (u64)gridDim.x * blockDim.x;
+  if (tid < sizeof(pbsm_header) / 4) reinterpret_cast<u32*>(hdr)[tid] = 0u;
   // tile_boundary (geometry.py:82-84): i / k, correctly rounded
-  if (i <= kx) bx[i] = __ddiv_rn((double)i, (double)kx);
-  if (i <= ky) by[i] = __ddiv_rn((double)i, (double)ky);
+  for (u64 i = tid; i <= (u64)max(kx, ky); i += nt) {
+    if (i <= (u64)kx) bx[i] = __ddiv_rn((double)i, (double)kx);
+    if (i <= (u64)ky) by[i] = __ddiv_rn((double)i, (double)ky);
+  }
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  const u64 nv = T / 4;  // the counter arrays are 256-byte aligned
+  for (u64 i = tid; i < nv; i += nt) {
+    reinterpret_cast<uint4*>(cnt_r)[i] = z;
+    reinterpret_cast<uint4*>(cnt_s)[i] = z;
+  }
+  for (u64 i = 4 * nv + tid; i < T; i += nt) {
+    cnt_r[i] = 0u;
+    cnt_s[i] = 0u;
+  }
 }
 
 // ---------------------------------------------------------------- 1a count
@@ -1057,14 +1076,20 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
       // <= kLmax <= B entries, so it crosses at most one bucket boundary and a
       // chunk holds < B + kLmax entries.  The plan's last CTA writes the
       // closing descriptor and the chunk counts (k_plan_partials).
-      if (kind == kNested || kind == kSorted) {
-        const bool q = kind == kSorted;  // (selects, no indexing: keeps P in registers)
-        const u32 jj = (u32)(q ? g[L_SF] : g[L_NF]);
-        (q ? P.jrec[1] : P.jrec[0])[jj] = make_uint4(r0, s0, a[i], b[i]);
-        const i64 st = (i64)(q ? g[L_SA] + g[L_SB] : g[L_NA] + g[L_NB]);
-        const i64 B = q ? kChunkB : kChunkBN;
-        const i64 ce = (st + a[i] + b[i] - 1) / B, cs = st ? (st - 1) / B : -1;
-        if (cs < ce) (q ? P.cdesc[1] : P.cdesc[0])[ce] = make_uint4(jj, r0, s0, 0u);
+      // (one branch per strategy: the bucket widths stay compile-time
+      // constants — a runtime divisor cost a 64-bit division per tile)
+      if (kind == kNested) {
+        const u32 jj = (u32)g[L_NF];
+        P.jrec[0][jj] = make_uint4(r0, s0, a[i], b[i]);
+        const u64 st = g[L_NA] + g[L_NB];
+        const u64 ce = (st + a[i] + b[i] - 1) / kChunkBN;
+        if (st == 0 || (st - 1) / kChunkBN < ce) P.cdesc[0][ce] = make_uint4(jj, r0, s0, 0u);
+      } else if (kind == kSorted) {
+        const u32 jj = (u32)g[L_SF];
+        P.jrec[1][jj] = make_uint4(r0, s0, a[i], b[i]);
+        const u64 st = g[L_SA] + g[L_SB];
+        const u64 ce = (st + a[i] + b[i] - 1) / kChunkB;
+        if (st == 0 || (st - 1) / kChunkB < ce) P.cdesc[1][ce] = make_uint4(jj, r0, s0, 0u);
       } else if (kind == kLarge) {
         P.lrec[g[L_LF]] = make_uint4(r0, s0, a[i], b[i]);
         P.lpre[g[L_LF]] = (u32)g[L_LI];
@@ -2139,11 +2164,9 @@ int pbsm_init(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi, 
   const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
   Ws w = ws_bind(ws, L);
   cudaStream_t s = as_stream(stream);
-  cudaMemsetAsync(w.hdr, 0, sizeof(pbsm_header), s);
-  cudaMemsetAsync(w.cnt_r, 0, 4 * L.tiles, s);
-  cudaMemsetAsync(w.cnt_s, 0, 4 * L.tiles, s);
-  const int m = std::max(kx, ky) + 1;
-  k_bounds<<<(m + 255) / 256, 256, 0, s>>>(w.bx, kx, w.by, ky);
+  const i64 blocks = std::max<i64>(1, std::min<i64>((i64)(L.tiles / 4 + 255) / 256,
+                                                     (i64)num_sms() * 4));
+  k_init<<<(unsigned)blocks, 256, 0, s>>>(w.hdr, w.cnt_r, w.cnt_s, L.tiles, w.bx, kx, w.by, ky);
   return launch_status();
 }
 
