@@ -213,14 +213,15 @@ def reference_arm(args):
 # ---------------------------------------------------------------- GPU arm
 def count_launches(h: dict, dev) -> int:
     """Our kernels per join step (see device.run_join / pbsm.cu host glue)."""
-    n = 1            # k_bounds
+    n = 1            # k_init
     n += 2           # k_count R, S
-    n += 5           # k_plan_reduce, k_plan_partials, k_plan_apply, k_chunks x2
+    n += 3           # k_plan_reduce, k_plan_partials, k_plan_apply
     n += 2           # k_scatter R, S
     for total in (h["list_r"], h["list_s"]):  # binned scatter: 3 scan kernels + k_bin_copy
         n += 4 if 64 * total > dev.BIN_LIST_BYTES else 0
-    n += 1           # k_guard
-    n += 1 if h["n_units"] > 0 else 0   # k_join (all mini-join strategies, count -> emit)
+    # k_join_nested (with the write guard fused in) or a stand-alone k_guard
+    n += 1
+    n += 1 if h["chunks_sorted"] + h["n_items"] > 0 else 0   # k_join (sorted / large units)
     return n
 
 
@@ -281,19 +282,24 @@ def main():
     for _ in range(max(3, args.warmup)):
         res = step()
     barrier()
-    probe = dev.PhaseProbe()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     barrier()
     clocks.t_begin = time.perf_counter()
     start.record()
     for _ in range(args.steps):
-        res = step(probe)
+        res = step()
     end.record()
     barrier()
     clocks.t_end = time.perf_counter()
-    clocks.__exit__(None, None, None)
     t_local = start.elapsed_time(end) / 1e3
+    # per-phase device times: the same K steps again, outside the timed
+    # region (the phase events add host work between the launches)
+    probe = dev.PhaseProbe()
+    for _ in range(args.steps):
+        step(probe)
+    torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
     t = t_local
     local_pairs = res.count
     totals = parallel.combine_counts(res.count, res.header["a_r"], res.header["a_s"], t_local,
