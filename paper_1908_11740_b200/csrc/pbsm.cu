@@ -2007,6 +2007,14 @@ __global__ void k_refine_compact(const i64* __restrict__ cand, i64 n,
   }
 }
 
+// header → page-locked host memory (see pbsm_read_header)
+__global__ void k_publish_header(const pbsm_header* __restrict__ hdr, pbsm_header* out) {
+  static_assert(sizeof(pbsm_header) % 8 == 0, "header words");
+  const int i = threadIdx.x;
+  if (i < (int)(sizeof(pbsm_header) / 8))
+    reinterpret_cast<volatile u64*>(out)[i] = __ldcg(reinterpret_cast<const u64*>(hdr) + i);
+}
+
 // ---------------------------------------------------------------- host glue
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -2212,7 +2220,18 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
 int pbsm_read_header(void* ws, pbsm_header* out, void* stream) {
   if (!ws || !out) return PBSM_E_ARG;
   cudaStream_t s = as_stream(stream);
-  cudaError_t e = cudaMemcpyAsync(out, ws, sizeof(pbsm_header), cudaMemcpyDeviceToHost, s);
+  // page-locked destination (device-accessible under UVA): one tiny kernel
+  // stores the header straight into host memory over PCIe, which returns
+  // sooner than a copy-engine transfer; pageable memory takes the copy
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, out);
+  if (e == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer == (void*)out) {
+    k_publish_header<<<1, 32, 0, s>>>(reinterpret_cast<const pbsm_header*>(ws), out);
+    e = cudaGetLastError();
+  } else {
+    cudaGetLastError();  // (clear a failed attribute query)
+    e = cudaMemcpyAsync(out, ws, sizeof(pbsm_header), cudaMemcpyDeviceToHost, s);
+  }
   if (e != cudaSuccess) return (int)e;
   e = cudaStreamSynchronize(s);
   return e == cudaSuccess ? 0 : (int)e;

@@ -24,7 +24,8 @@ import torch
 from . import _native
 from .errors import KernelError
 
-__all__ = ["DeviceRects", "DeviceJoinResult", "PhaseProbe", "run_join", "to_device"]
+__all__ = ["DeviceRects", "DeviceJoinResult", "PhaseProbe", "release_buffers", "run_join",
+           "to_device"]
 
 
 @dataclass
@@ -86,6 +87,36 @@ def _workspace(lib, device, kx, ky, row_lo, row_hi) -> torch.Tensor:
         _ws_cache.clear()  # keep one grid workspace alive at a time
         _ws_cache[key] = ws
     return ws
+
+
+# Internal buffers of a join (the two tile lists, the join scratch), kept per
+# device and reused by the next join when large enough: a fresh multi-GB
+# allocation per join let the caching allocator fall back to cudaMalloc /
+# cudaFree now and then, stalling the join for milliseconds.  The returned
+# pair arrays are always fresh.  release_buffers() gives the memory back.
+_buf_cache: dict = {}
+
+
+def _buffer(device, name: str, shape: tuple, dtype) -> torch.Tensor:
+    n = 1
+    for d in shape:
+        n *= d
+    # per (device, stream): joins enqueued on different streams never share
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream, name)
+    buf = _buf_cache.get(key)
+    if buf is None or buf.dtype != dtype or buf.numel() < n:
+        _buf_cache.pop(key, None)
+        del buf  # the old block is free before the larger one is requested
+        buf = torch.empty(max(n, 1), dtype=dtype, device=device)
+        _buf_cache[key] = buf
+    return buf[:n].view(shape)
+
+
+def release_buffers() -> None:
+    """Drop the cached tile lists, join scratch and grid workspaces."""
+    _buf_cache.clear()
+    _ws_cache.clear()
+    _plan_cache.clear()
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -229,7 +260,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     lists = []
     thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
-        ent = torch.empty((max(total, 1), 8), dtype=torch.int64, device=device)  # 64 B records
+        ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64)  # 64 B records
         # the copy costs ~80 B per rectangle; it pays where the random record
         # writes dominate: large lists and heavy replication (cfg4: 1.7
         # entries per rectangle; cfg2/cfg3/cfg5: 1.1-1.5, measured slower)
@@ -252,9 +283,10 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     rl, sl = lists
     if guess is not None:
         cap, cn, rest = guess["pairs"], guess["nested"], guess["other"]
-        scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(cn + rest)), dtype=torch.uint8,
-                              device=device)
+        scratch = _buffer(device, "scratch", (int(lib.pbsm_join_scratch_bytes(cn + rest)),),
+                          torch.uint8)
         pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
+        mark("alloc")
         _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), sl.data_ptr(), cn,
                                                  rest, scratch.data_ptr(), pairs.data_ptr(), cap,
                                                  stream), "pbsm_join_emit_bounded")
@@ -282,8 +314,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         return res
 
     n_units = h.n_units
-    scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(n_units)), dtype=torch.uint8,
-                          device=device)
+    scratch = _buffer(device, "scratch", (int(lib.pbsm_join_scratch_bytes(n_units)),),
+                      torch.uint8)
     pairs = None
     if not collect:
         _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), C.byref(h),

@@ -17,12 +17,19 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--bin-bytes", type=int, default=None)
 ap.add_argument("--nested-max", type=int, default=-1)
+ap.add_argument("--per-rep", action="store_true", help="also print each join's device time")
+ap.add_argument("--gc-freeze", action="store_true", help="gc.freeze() after the warm-up")
 a = ap.parse_args()
 r, s, k = make_config(a.config, 1.0)
 R = dev.to_device(r, "cuda")
 S = R if s is r else dev.to_device(s, "cuda")
 for _ in range(3):
     dev.run_join(R, S, k, k, bin_bytes=a.bin_bytes, nested_max=a.nested_max)
+if a.gc_freeze:
+    import gc
+    gc.collect()
+    gc.freeze()
+ms0 = torch.cuda.memory_stats()
 probe = dev.PhaseProbe()
 t0 = torch.cuda.Event(enable_timing=True)
 t1 = torch.cuda.Event(enable_timing=True)
@@ -33,5 +40,19 @@ for _ in range(a.reps):
 t1.record()
 t1.synchronize()
 ph = {n: round(v / a.reps * 1e3, 3) for n, v in probe.durations().items()}
+ms1 = torch.cuda.memory_stats()
+ph["cudaMalloc/free"] = (ms1.get("num_device_alloc", 0) - ms0.get("num_device_alloc", 0),
+                         ms1.get("num_device_free", 0) - ms0.get("num_device_free", 0),
+                         ms1.get("num_alloc_retries", 0) - ms0.get("num_alloc_retries", 0))
+if a.per_rep:
+    reps = []
+    for _ in range(a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dev.run_join(R, S, k, k, bin_bytes=a.bin_bytes, nested_max=a.nested_max)
+        e1.record()
+        e1.synchronize()
+        reps.append(round(e0.elapsed_time(e1), 3))
+    print("per-rep ms", reps)
 print(CONFIGS[a.config].name, f"bin_bytes={a.bin_bytes}", f"{t0.elapsed_time(t1) / a.reps:.3f} ms",
       res.count, ph)
