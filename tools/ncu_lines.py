@@ -48,7 +48,8 @@ for ln in dis.splitlines():
         cur_fn = mf.group(1)
         cur = None
         continue
-    if cur_fn is None or short not in cur_fn or (want and want not in cur_fn):
+    # mangled: <len><name>[template args]: "6k_join" does not match k_join_nested
+    if cur_fn is None or f"{len(short)}{short}{want}" not in cur_fn:
         continue
     mm = re.search(r'//## File ".*?", line (\d+)', ln)
     if mm:
