@@ -25,7 +25,7 @@ from . import _native
 from .errors import KernelError
 
 __all__ = ["DeviceRects", "DeviceJoinResult", "PhaseProbe", "release_buffers", "run_join",
-           "to_device"]
+           "to_device", "to_device_pipelined"]
 
 
 @dataclass
@@ -37,6 +37,11 @@ class DeviceRects:
     xu: torch.Tensor
     yl: torch.Tensor
     yu: torch.Tensor
+    # set by to_device_pipelined: recorded on the copy stream once the four
+    # coordinate columns / the ids have landed; run_join makes its stream
+    # wait on them right before the first kernel that reads them
+    coords_ready: object = None
+    ids_ready: object = None
 
     def __len__(self) -> int:
         return int(self.ids.shape[0])
@@ -62,6 +67,61 @@ def to_device(batch, device="cuda", pinned: bool = True) -> DeviceRects:
             t = t.pin_memory()
         out.append(t.to(device, non_blocking=True))
     return DeviceRects(*out)
+
+
+_copy_streams: dict = {}
+
+
+def _host_tensor(a, dt, pinned: bool) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.dtype != dt:
+        t = t.to(dt)
+    if pinned and t.numel() > 0 and not t.is_pinned():
+        t = t.pin_memory()
+    return t
+
+
+def to_device_pipelined(r, s, device="cuda"):
+    """Copy R and S (``RectBatch`` or 5-tuples) to the GPU on a side stream in
+    the order the join reads them — R's coordinates, S's coordinates, then
+    the ids — with an event after each group, so run_join's count passes
+    start while the rest is still crossing PCIe (the host→device copy is
+    most of an end-to-end join).  Returns (R, S) DeviceRects (S is R when
+    s is r)."""
+    device = torch.device(device)
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    cs = _copy_streams.get(device.index)
+    if cs is None:
+        cs = _copy_streams[device.index] = torch.cuda.Stream(device)
+    batches = [r] if s is r else [r, s]
+    host = []
+    for b in batches:
+        cols = b if isinstance(b, (tuple, list)) else (b.ids, b.xl, b.xu, b.yl, b.yu)
+        host.append([_host_tensor(a, dt, True)
+                     for a, dt in zip(cols, (torch.int64,) + (torch.float64,) * 4)])
+    dev_cols = [[torch.empty(h.shape, dtype=h.dtype, device=device) for h in hb] for hb in host]
+    cs.wait_stream(torch.cuda.current_stream(device))  # the buffers' allocation stream
+    out = []
+    with torch.cuda.stream(cs):
+        coord_ev = []
+        for hb, db in zip(host, dev_cols):
+            for q in range(1, 5):
+                db[q].copy_(hb[q], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            coord_ev.append(ev)
+        for (hb, db), cev in zip(zip(host, dev_cols), coord_ev):
+            db[0].copy_(hb[0], non_blocking=True)
+            iev = torch.cuda.Event()
+            iev.record(cs)
+            out.append(DeviceRects(*db, coords_ready=cev, ids_ready=iev))
+    return (out[0], out[0]) if s is r else (out[0], out[1])
+
+
+def _wait(ev, stream_obj) -> None:
+    if ev is not None:
+        stream_obj.wait_event(ev)
 
 
 @dataclass
@@ -237,7 +297,9 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     mark("start")
     _native.check(lib.pbsm_init(wsp, *grid, stream), "pbsm_init")
     mark("init")
+    cur = torch.cuda.current_stream(device)
     for side, b in ((0, r), (1, s)):
+        _wait(b.coords_ready, cur)
         _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
                                      side, wsp, *grid, stream), "pbsm_count")
     mark("count")
@@ -261,6 +323,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
         ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64)  # 64 B records
+        _wait(b.ids_ready, cur)
         # the copy costs ~80 B per rectangle; it pays where the random record
         # writes dominate: large lists and heavy replication (cfg4: 1.7
         # entries per rectangle; cfg2/cfg3/cfg5: 1.1-1.5, measured slower)

@@ -141,8 +141,9 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
                           0.0, 0.0, 0.0, time.perf_counter() - t0,
                           np.empty(0, dtype=np.int64))
     device = _require_cuda()
-    rd = dev.to_device(r, device)
-    sd = rd if s is r else dev.to_device(s, device)
+    # column copies on a side stream, coordinates first: the count passes
+    # start while the ids are still in flight
+    rd, sd = dev.to_device_pipelined(r, s, device)
     kx, ky = cfg.layout.grid
     res = dev.run_join(rd, sd, kx, ky, collect=collect_user or refine is not None, timing=True)
     count, pairs = res.count, res.pairs
