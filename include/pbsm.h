@@ -137,7 +137,9 @@ int pbsm_read_header(void* ws, pbsm_header* out, void* stream);
  * scatter each rectangle into the list of every JOIN tile it overlaps (tiles
  * where the other input is empty can produce no pair and get no list),
  * labelled with its class there.  `out` holds `capacity` entries
- * (= header.list_r or list_s). */
+ * (= header.list_r or list_s).  ids may be NULL: the entries then carry the
+ * row index, and pbsm_map_ids turns the emitted pairs into ids later (the
+ * host→device copy of the id columns overlaps the join). */
 int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu,
                  const double* yl, const double* yu, int64_t n, int32_t side,
                  void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
@@ -207,6 +209,11 @@ int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int
                            const pbsm_entry* r_list, const pbsm_entry* s_list,
                            int64_t max_nested_chunks, int64_t max_other_units, void* scratch,
                            int64_t* pairs, int64_t capacity, void* stream);
+
+/* pairs[2i], pairs[2i+1] (row indices, i < n) → r_ids[...], s_ids[...] in
+ * place: the pair list of a join whose scatter ran without the id columns. */
+int pbsm_map_ids(int64_t* pairs, int64_t n, const int64_t* r_ids, const int64_t* s_ids,
+                 void* stream);
 
 /* SJB1 dataset body (load_mbr_binary, io.py:113-141): n packed 40-byte
  * little-endian records {id u64, x_l, y_l, x_u, y_u f64} at an 8-byte aligned

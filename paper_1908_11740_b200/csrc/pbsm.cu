@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(256) k_bin_copy(const i64* __restrict__ ids,
       const i64 i = t0 + threadIdx.x + u * 256;
       band[u] = -1;
       if (i < end) {
-        id[u] = __ldcs(ids + i);
+        id[u] = ids ? __ldcs(ids + i) : i;
         a[u] = __ldcs(xl + i);
         b[u] = __ldcs(xu + i);
         c[u] = __ldcs(yl + i);
@@ -706,7 +706,7 @@ struct ScatterIn {
       c = __ldcs(&r->yl);
       d = __ldcs(&r->yu);
     } else {
-      id = __ldcs(ids + i);
+      id = ids ? __ldcs(ids + i) : i;  // no id column: the row index (see pbsm_map_ids)
       a = __ldcs(xl + i);
       b = __ldcs(xu + i);
       c = __ldcs(yl + i);
@@ -2023,6 +2023,16 @@ __global__ void k_publish_header(const pbsm_header* __restrict__ hdr, pbsm_heade
     reinterpret_cast<volatile u64*>(out)[i] = __ldcg(reinterpret_cast<const u64*>(hdr) + i);
 }
 
+// row indices → ids in a pair list (scatter run without the id columns)
+__global__ void k_map_ids(i64* __restrict__ pairs, i64 n, const i64* __restrict__ r_ids,
+                          const i64* __restrict__ s_ids) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const longlong2 p = reinterpret_cast<const longlong2*>(pairs)[i];
+    reinterpret_cast<longlong2*>(pairs)[i] = make_longlong2(__ldg(r_ids + p.x), __ldg(s_ids + p.y));
+  }
+}
+
 // ---------------------------------------------------------------- host glue
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -2274,7 +2284,7 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu, const d
       capacity < 0)
     return PBSM_E_ARG;
   if (n == 0) return 0;
-  if (!ids || !xl || !xu || !yl || !yu || (!out && capacity > 0)) return PBSM_E_ARG;
+  if (!xl || !xu || !yl || !yu || (!out && capacity > 0)) return PBSM_E_ARG;
   return scatter_impl(ids, xl, xu, yl, yu, nullptr, n, side, ws, kx, ky, row_lo, row_hi, out,
                       capacity, stream);
 }
@@ -2297,7 +2307,7 @@ int pbsm_bin(const int64_t* ids, const double* xl, const double* xu, const doubl
   if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1))
     return PBSM_E_ARG;
   if (n == 0) return 0;
-  if (!ids || !xl || !xu || !yl || !yu || !band) return PBSM_E_ARG;
+  if (!xl || !xu || !yl || !yu || !band) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
   cudaStream_t s = as_stream(stream);
   const unsigned nb = part_blocks(n);
@@ -2356,6 +2366,17 @@ int64_t pbsm_refine_result_offset(int64_t n_cand) {
   if (n_cand < 0) return PBSM_E_ARG;
   const ScanLayout SL = scan_layout(n_cand);
   return (int64_t)(SL.base + 8 * SL.n);
+}
+
+int pbsm_map_ids(int64_t* pairs, int64_t n, const int64_t* r_ids, const int64_t* s_ids,
+                 void* stream) {
+  if (n < 0) return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!pairs || !r_ids || !s_ids) return PBSM_E_ARG;
+  const unsigned blocks = (unsigned)std::min<i64>((n + 255) / 256, (i64)num_sms() * 8);
+  k_map_ids<<<blocks, 256, 0, as_stream(stream)>>>((i64*)pairs, n, (const i64*)r_ids,
+                                                    (const i64*)s_ids);
+  return launch_status();
 }
 
 int pbsm_unpack_records(const void* records, int64_t n, int64_t* ids, double* xl, double* xu,

@@ -248,10 +248,10 @@ def pair_capacity(h) -> int:
 BIN_LIST_BYTES = int(os.environ.get("PBSM_BIN_BYTES", 1 << 30))
 
 
-def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream) -> torch.Tensor:
-    """Row-band copy of one input: n 40-byte records {id, xl, xu, yl, yu}."""
+def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream, ids_p) -> torch.Tensor:
+    """Row-band copy of one input: n 40-byte records {id (or row), xl, xu, yl, yu}."""
     band = torch.empty((len(b), 5), dtype=torch.int64, device=b.device)
-    _native.check(lib.pbsm_bin(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu),
+    _native.check(lib.pbsm_bin(ids_p, _ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu),
                                len(b), side, wsp, *grid, band.data_ptr(), stream), "pbsm_bin")
     return band
 
@@ -298,6 +298,10 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     _native.check(lib.pbsm_init(wsp, *grid, stream), "pbsm_init")
     mark("init")
     cur = torch.cuda.current_stream(device)
+    # ids still in flight (to_device_pipelined): the entries carry row
+    # indices and the pair list is mapped to ids at the end (pbsm_map_ids),
+    # so nothing before the final map waits for the id columns
+    late = r.ids_ready is not None and s.ids_ready is not None
     for side, b in ((0, r), (1, s)):
         _wait(b.coords_ready, cur)
         _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
@@ -323,19 +327,19 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
         ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64)  # 64 B records
-        _wait(b.ids_ready, cur)
+        ids_p = None if late else _ptr(b.ids)
         # the copy costs ~80 B per rectangle; it pays where the random record
         # writes dominate: large lists and heavy replication (cfg4: 1.7
         # entries per rectangle; cfg2/cfg3/cfg5: 1.1-1.5, measured slower)
         if 64 * total > thresh and (bin_bytes == 0 or total >= 1.6 * len(b)):
-            band = _banded(lib, b, side, wsp, grid, stream)
+            band = _banded(lib, b, side, wsp, grid, stream, ids_p)
             mark("bin")
             _native.check(lib.pbsm_scatter_banded(band.data_ptr(), len(b), side, wsp, *grid,
                                                   ent.data_ptr(), total, stream),
                           "pbsm_scatter_banded")
             del band
         else:
-            _native.check(lib.pbsm_scatter(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
+            _native.check(lib.pbsm_scatter(ids_p, _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
                                            _ptr(b.yu), len(b), side, wsp, *grid, ent.data_ptr(),
                                            total, stream), "pbsm_scatter")
         mark("scatter")
@@ -366,6 +370,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                             timing=timing, keep_counts=keep_counts, probe=probe,
                             ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes)
         count = int(h2.pairs)
+        if late:
+            _map_ids(lib, pairs, count, r, s, cur, stream)
         if ev:
             ev[2].record()
             ev[2].synchronize()
@@ -402,6 +408,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                 break
             cap = count  # rare: the estimate was short, emit again into an exact buffer
         pairs = pairs[:count]
+        if late:
+            _map_ids(lib, pairs, count, r, s, cur, stream)
         if not ordered and not keep_counts:
             _plan_cache.clear()  # one shape at a time
             _plan_cache[key] = {"list_r": h.list_r, "list_s": h.list_s, "pairs": cap,
@@ -417,6 +425,16 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                      "total": ev[0].elapsed_time(ev[2]) / 1e3}
     res.tile_counts = counts
     return res
+
+
+def _map_ids(lib, pairs, count: int, r: DeviceRects, s: DeviceRects, cur, stream) -> None:
+    """Row-index pairs → id pairs once the id columns have landed."""
+    if count == 0:
+        return
+    _wait(r.ids_ready, cur)
+    _wait(s.ids_ready, cur)
+    _native.check(lib.pbsm_map_ids(pairs.data_ptr(), count, _ptr(r.ids), _ptr(s.ids), stream),
+                  "pbsm_map_ids")
 
 
 def _align(v: int, a: int = 256) -> int:

@@ -58,6 +58,25 @@ def test_reference_configs_bit_exact(golden, cfg):
     assert np.array_equal(oracle.sorted_pairs(rep.pairs), g[f"cfg{cfg}_pairs"])
 
 
+def test_late_ids_mapped_like_direct_ids():
+    """join() copies the id columns last and maps row-index pairs to ids at the
+    end (pbsm_map_ids); device-resident inputs scatter the ids directly.  Both
+    give the oracle's pairs for arbitrary (non-row) ids."""
+    r, s, k = make_config(1, 0.3)
+    rng = np.random.default_rng(7)
+    r = (rng.permutation(len(r[0])).astype(np.int64) * 7 + 3,) + tuple(r[1:])
+    s = (rng.permutation(len(s[0])).astype(np.int64) * 5 - 11,) + tuple(s[1:])
+    want = oracle.sorted_pairs(oracle.join(r, s, "2d", k)["pairs"])
+    rep = pb.join(pb.RectBatch(*r), pb.RectBatch(*s), _collect("2d", k))
+    assert np.array_equal(oracle.sorted_pairs(rep.pairs), want)
+    res = dev.run_join(dev.to_device(r), dev.to_device(s), k, k)
+    assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+    # the row-band (binned) scatter in the late mode too
+    R, S = dev.to_device_pipelined(r, s)
+    res = dev.run_join(R, S, k, k, bin_bytes=0)
+    assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+
+
 def test_count_only_matches_collect():
     r, s, k = make_config(1)
     R, S = pb.RectBatch(*r), pb.RectBatch(*s)
