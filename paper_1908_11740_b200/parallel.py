@@ -87,7 +87,13 @@ def exchange_counts(count: int, a_r: int, a_s: int, device=None, group=None) -> 
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    mine = torch.tensor([count, a_r, a_s], dtype=torch.int64, device=device)
+    mine = torch.tensor([count, a_r, a_s], dtype=torch.int64)
+    if device is not None and torch.device(device).type == "cuda":
+        # staged through page-locked memory: an asynchronous copy, so the
+        # exchange costs one host sync (the read of the gathered counts)
+        mine = mine.pin_memory().to(device, non_blocking=True)
+    elif device is not None:
+        mine = mine.to(device)
     if world == 1:
         allv = mine.view(1, 3)
     else:
