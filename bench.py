@@ -246,10 +246,20 @@ def main():
             print(json.dumps({"error": f"--gpus {args.gpus} needs torchrun with "
                                        f"{args.gpus} processes"}))
             return 1
+    # test hook (tools/multirank_smoke.sh): PBSM_BENCH_SHARED_GPU=1 runs every
+    # rank on cuda:0 with gloo collectives — exercises the multi-rank host
+    # logic on a one-GPU box (no kernel waits on another rank); the numbers of
+    # such a run are not a measurement
+    shared = os.environ.get("PBSM_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
 
     spec = CONFIGS[args.config]
     r, s, k = make_config(args.config)
