@@ -2261,7 +2261,7 @@ static int scatter_impl(const int64_t* ids, const double* xl, const double* xu,
                         int32_t row_hi, pbsm_entry* out, int64_t capacity, void* stream) {
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
 #ifndef PBSM_SCAT_GRID
-#define PBSM_SCAT_GRID 16
+#define PBSM_SCAT_GRID 32  // blocks per SM (swept 8-1000 on cfg2/cfg3: 32 best)
 #endif
   const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * PBSM_SCAT_GRID);
   ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band)};
