@@ -106,7 +106,10 @@ constexpr int kNT = PBSM_NESTED_THREADS;  // threads of a nested-join CTA
 constexpr int kMaxTilesN = kCapN / 2;
 static_assert(kCapN <= 512 && kLmax <= 128, "nested row descriptors: 9-bit positions, 7-bit counts");
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
-constexpr int kLargeOther = 2048;         // other-side entries per large work item
+#ifndef PBSM_LARGE_OTHER
+#define PBSM_LARGE_OTHER 2048
+#endif
+constexpr int kLargeOther = PBSM_LARGE_OTHER;  // other-side entries per large work item
 
 constexpr int kScanThreads = 256;
 constexpr int kScanPer = 16;
@@ -126,7 +129,10 @@ constexpr int kScanTile = kScanThreads * kScanPer;
 #endif
 constexpr int kBins = PBSM_BINS;                  // row bands of the binned scatter
 constexpr int kBinSlots = kBins + 1;        // + one slot for rectangles outside the strip
-constexpr int kMaxPartBlocks = 4096;        // grid cap of the count / bin passes
+#ifndef PBSM_MAX_PART_BLOCKS
+#define PBSM_MAX_PART_BLOCKS 16384
+#endif
+constexpr int kMaxPartBlocks = PBSM_MAX_PART_BLOCKS;  // grid cap of the count / bin passes
 #ifndef PBSM_BIN_TILE
 #define PBSM_BIN_TILE 1024
 #endif
@@ -718,7 +724,10 @@ struct ScatterIn {
 // 5 resident CTAs per SM measured best for the SoA input (cfg3: 4.77 vs 4.91
 // ms at 4), 4 for the 40-byte band records (cfg4: 6.65 vs 7.02 ms at 5)
 template <bool BANDED>
-__global__ void __launch_bounds__(256, BANDED ? 4 : 5) k_scatter(ScatterIn in, i64 n,
+#ifndef PBSM_SCAT_MINB
+#define PBSM_SCAT_MINB 5
+#endif
+__global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(ScatterIn in, i64 n,
                                                  int kx, int ky, int row_lo, int row_hi,
                                                  const double* __restrict__ bx,
                                                  const double* __restrict__ by,
@@ -1930,7 +1939,10 @@ __global__ void __launch_bounds__(kNT, PBSM_NESTED_MINB) k_join_nested(JoinArgs 
 }
 
 template <bool EMIT>
-__global__ void __launch_bounds__(kJoinThreads, 2) k_join(JoinArgs A) {
+#ifndef PBSM_JOIN_MINB
+#define PBSM_JOIN_MINB 2
+#endif
+__global__ void __launch_bounds__(kJoinThreads, PBSM_JOIN_MINB) k_join(JoinArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   JoinSmem& U = *reinterpret_cast<JoinSmem*>(smem_raw);
   // ordered mode hands out units by ticket (launch order, for the look-back);
@@ -2058,10 +2070,14 @@ int num_sms() {
 }
 
 // grid of the count and bin passes (the same n → the same block ranges)
-// grid of the count and bin passes (the same n → the same block ranges)
+// (swept: 32 blocks per SM of >= 2048 rectangles — finer than the 8 per SM
+// before — took the cfg3 count pass from 1.09 to 0.97 ms, cfg2 273 -> 255 µs)
+#ifndef PBSM_PART_GRID
+#define PBSM_PART_GRID 32  // blocks per SM
+#endif
 unsigned part_blocks(i64 n) {
-  return (unsigned)std::max<i64>(1, std::min<i64>((n + 1023) / 1024,
-                                                  std::min<i64>(kMaxPartBlocks, num_sms() * 8)));
+  return (unsigned)std::max<i64>(1, std::min<i64>((n + 2047) / 2048,
+                                                  std::min<i64>(kMaxPartBlocks, num_sms() * PBSM_PART_GRID)));
 }
 
 
