@@ -1047,14 +1047,18 @@ struct PlanOut {
   u32* lpre;
 };
 
+// the lanes k_plan_apply scans: every lane but the two totals (L_A, L_B)
+constexpr int kNA = kNV - 2;
 __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32* __restrict__ cr,
                                                              u32* __restrict__ cs, u64 T, u64 nb,
                                                              i64 nm,
                                                              const u64* __restrict__ partials,
                                                              PlanOut P) {
-  __shared__ u32 sa[kPlanTile];
+  __shared__ u32 sa[kPlanTile];   // counts, then the tiles' list starts
   __shared__ u32 sb[kPlanTile];
-  __shared__ u32 shs[kPlanThreads / 32][kNV];
+  __shared__ u32 ca[kPlanTile];   // counts (for the expected cursor ends)
+  __shared__ u32 cb[kPlanTile];
+  __shared__ u32 shs[kPlanThreads / 32][kNA];
   __shared__ u64 shp[2][kNV];  // this CTA's global prefixes, the totals
   const u64 base = (u64)blockIdx.x * kPlanTile;
   // lane-major partials: lane q of CTA b at q * (nb + 1) + b, totals at q * (nb + 1) + nb;
@@ -1065,14 +1069,17 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
   }
   for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
     const u64 t = base + i;
-    sa[i] = t < T ? cr[t] : 0u;
-    sb[i] = t < T ? cs[t] : 0u;
+    const u32 x = t < T ? cr[t] : 0u, y = t < T ? cs[t] : 0u;
+    sa[i] = x;
+    sb[i] = y;
+    ca[i] = x;
+    cb[i] = y;
   }
   __syncthreads();
   u32 a[kPlanPer], b[kPlanPer];
-  u32 pre[kNV];
+  u32 pre[kNA];  // in-CTA exclusive prefixes of lanes 2..11 (u32: a CTA's sums fit)
 #pragma unroll
-  for (int q = 0; q < kNV; ++q) pre[q] = 0;
+  for (int q = 0; q < kNA; ++q) pre[q] = 0;
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     a[i] = sa[threadIdx.x * kPlanPer + i];
@@ -1080,81 +1087,83 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
     u32 v[kNV];
     tile_vals(a[i], b[i], nm, v);
 #pragma unroll
-    for (int q = 0; q < kNV; ++q) pre[q] += v[q];
+    for (int q = 0; q < kNA; ++q) pre[q] += v[q + 2];
   }
   {
-    u32 tot[kNV];
-    block_excl_scan_multi<kPlanThreads, kNV, u32>(pre, tot, shs);
+    u32 tot[kNA];
+    block_excl_scan_multi<kPlanThreads, kNA, u32>(pre, tot, shs);
   }
-  // global prefixes = this CTA's partial + the u32 in-CTA prefix (the scan's
-  // barriers made shp visible)
-  u64 tot[kNV], g[kNV];
-#pragma unroll
-  for (int q = 0; q < kNV; ++q) {
-    tot[q] = shp[1][q];
-    g[q] = shp[0][q] + pre[q];
-  }
-  // region bases: [nested | sorted | large] in each input's list
-  const u64 rs_base = tot[L_NA], ss_base = tot[L_NB];
-  const u64 rl_base = tot[L_NA] + tot[L_SA], sl_base = tot[L_NB] + tot[L_SB];
+  // global prefix of lane q = this CTA's u64 partial + the u32 running
+  // in-CTA prefix (the scan's barriers made shp visible); only the active
+  // strategy's lanes advance per tile
+  auto g = [&](int q) -> u64 { return shp[0][q] + pre[q - 2]; };
+  const u64 rs_base = shp[1][L_NA], ss_base = shp[1][L_NB];
+  const u64 rl_base = shp[1][L_NA] + shp[1][L_SA], sl_base = shp[1][L_NB] + shp[1][L_SB];
   // (the scan ended with a barrier, so sa/sb may be overwritten now: they
-  // receive the cursor starts; the expected cursor ends go back into cnt[]
-  // for k_guard)
+  // receive the list starts)
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
     const u64 t = base + (u64)threadIdx.x * kPlanPer + i;
     const int kind = tile_kind(a[i], b[i], nm);
     u32 r0 = kSkip, s0 = kSkip;
+    // chunks: consecutive tiles of one strategy whose LAST entry falls in the
+    // same bucket of B entries; a tile starts chunk c when its end is in
+    // bucket c and its start (the previous tile's end) is not.  A tile holds
+    // <= kLmax <= B entries, so it crosses at most one bucket boundary and a
+    // chunk holds < B + kLmax entries.  The plan's last CTA writes the
+    // closing descriptor and the chunk counts (k_plan_partials).
+    // (one branch per strategy: the bucket widths stay compile-time
+    // constants — a runtime divisor cost a 64-bit division per tile)
     if (kind == kNested) {
-      r0 = (u32)g[L_NA];
-      s0 = (u32)g[L_NB];
+      r0 = (u32)g(L_NA);
+      s0 = (u32)g(L_NB);
+      if (t < T) {
+        const u32 jj = (u32)g(L_NF);
+        P.jrec[0][jj] = make_uint4(r0, s0, a[i], b[i]);
+        const u64 st = g(L_NA) + g(L_NB);
+        const u64 ce = (st + a[i] + b[i] - 1) / kChunkBN;
+        if (st == 0 || (st - 1) / kChunkBN < ce) P.cdesc[0][ce] = make_uint4(jj, r0, s0, 0u);
+      }
+      pre[L_NF - 2] += 1u;
+      pre[L_NA - 2] += a[i];
+      pre[L_NB - 2] += b[i];
     } else if (kind == kSorted) {
-      r0 = (u32)(rs_base + g[L_SA]);
-      s0 = (u32)(ss_base + g[L_SB]);
+      r0 = (u32)(rs_base + g(L_SA));
+      s0 = (u32)(ss_base + g(L_SB));
+      if (t < T) {
+        const u32 jj = (u32)g(L_SF);
+        P.jrec[1][jj] = make_uint4(r0, s0, a[i], b[i]);
+        const u64 st = g(L_SA) + g(L_SB);
+        const u64 ce = (st + a[i] + b[i] - 1) / kChunkB;
+        if (st == 0 || (st - 1) / kChunkB < ce) P.cdesc[1][ce] = make_uint4(jj, r0, s0, 0u);
+      }
+      pre[L_SF - 2] += 1u;
+      pre[L_SA - 2] += a[i];
+      pre[L_SB - 2] += b[i];
     } else if (kind == kLarge) {
-      r0 = (u32)(rl_base + g[L_LA]);
-      s0 = (u32)(sl_base + g[L_LB]);
+      r0 = (u32)(rl_base + g(L_LA));
+      s0 = (u32)(sl_base + g(L_LB));
+      if (t < T) {
+        P.lrec[g(L_LF)] = make_uint4(r0, s0, a[i], b[i]);
+        P.lpre[g(L_LF)] = (u32)g(L_LI);
+      }
+      u32 v[kNV];
+      tile_vals(a[i], b[i], nm, v);
+      pre[L_LF - 2] += 1u;
+      pre[L_LI - 2] += v[L_LI];
+      pre[L_LA - 2] += a[i];
+      pre[L_LB - 2] += b[i];
     }
     sa[threadIdx.x * kPlanPer + i] = r0;
     sb[threadIdx.x * kPlanPer + i] = s0;
-    if (t < T) {
-      // chunks: consecutive tiles of one strategy whose LAST entry falls in the
-      // same bucket of B entries; a tile starts chunk c when its end is in
-      // bucket c and its start (the previous tile's end) is not.  A tile holds
-      // <= kLmax <= B entries, so it crosses at most one bucket boundary and a
-      // chunk holds < B + kLmax entries.  The plan's last CTA writes the
-      // closing descriptor and the chunk counts (k_plan_partials).
-      // (one branch per strategy: the bucket widths stay compile-time
-      // constants — a runtime divisor cost a 64-bit division per tile)
-      if (kind == kNested) {
-        const u32 jj = (u32)g[L_NF];
-        P.jrec[0][jj] = make_uint4(r0, s0, a[i], b[i]);
-        const u64 st = g[L_NA] + g[L_NB];
-        const u64 ce = (st + a[i] + b[i] - 1) / kChunkBN;
-        if (st == 0 || (st - 1) / kChunkBN < ce) P.cdesc[0][ce] = make_uint4(jj, r0, s0, 0u);
-      } else if (kind == kSorted) {
-        const u32 jj = (u32)g[L_SF];
-        P.jrec[1][jj] = make_uint4(r0, s0, a[i], b[i]);
-        const u64 st = g[L_SA] + g[L_SB];
-        const u64 ce = (st + a[i] + b[i] - 1) / kChunkB;
-        if (st == 0 || (st - 1) / kChunkB < ce) P.cdesc[1][ce] = make_uint4(jj, r0, s0, 0u);
-      } else if (kind == kLarge) {
-        P.lrec[g[L_LF]] = make_uint4(r0, s0, a[i], b[i]);
-        P.lpre[g[L_LF]] = (u32)g[L_LI];
-      }
-    }
-    u32 v[kNV];
-    tile_vals(a[i], b[i], nm, v);
-#pragma unroll
-    for (int q = 0; q < kNV; ++q) g[q] += v[q];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
     const u64 t = base + i;
     if (t < T) {
       const u32 r0 = sa[i], s0 = sb[i];
-      cr[t] = r0 + cr[t];   // expected end of tile t's R cursor
-      cs[t] = s0 + cs[t];
+      cr[t] = r0 + ca[i];   // expected end of tile t's R cursor (for k_guard)
+      cs[t] = s0 + cb[i];
       P.cur_r[t] = r0;
       P.cur_s[t] = s0;
     }
