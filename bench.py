@@ -222,6 +222,7 @@ def count_launches(h: dict, dev) -> int:
     # k_join_nested (with the write guard fused in) or a stand-alone k_guard
     n += 1
     n += 1 if h["chunks_sorted"] + h["n_items"] > 0 else 0   # k_join (sorted / large units)
+    n += 1           # k_publish_header (the final header read)
     return n
 
 
