@@ -44,7 +44,7 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> Path:
-    deps = SOURCES + HEADERS + [Path(__file__)]
+    deps = SOURCES + sorted(CSRC.glob("*.cuh")) + HEADERS + [Path(__file__)]
     if not force and not _stale(LIB_PATH, deps):
         return LIB_PATH
     LIB_DIR.mkdir(exist_ok=True)

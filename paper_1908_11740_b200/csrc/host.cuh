@@ -1,0 +1,139 @@
+// host.cuh — part of pbsm.cu (one translation unit: included inside its
+// anonymous namespace, after the types and includes at its top).
+// Contents: host glue: launch configuration, smem attributes, join launch.
+#pragma once
+
+// ---------------------------------------------------------------- host glue
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+inline bool grid_ok(int kx, int ky, int row_lo, int row_hi) {
+  return kx >= 1 && ky >= 1 && kx <= 65535 && ky <= 65535 && row_lo >= 0 && row_lo < row_hi &&
+         row_hi <= ky && (u64)kx * (u64)(row_hi - row_lo) < (1ull << 32) - 2;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// grid of the count and bin passes (the same n → the same block ranges)
+// (swept: 32 blocks per SM of >= 2048 rectangles — finer than the 8 per SM
+// before — took the cfg3 count pass from 1.09 to 0.97 ms, cfg2 273 -> 255 µs)
+#ifndef PBSM_PART_GRID
+#define PBSM_PART_GRID 32  // blocks per SM
+#endif
+unsigned part_blocks(i64 n) {
+  return (unsigned)std::max<i64>(1, std::min<i64>((n + 2047) / 2048,
+                                                  std::min<i64>(kMaxPartBlocks, num_sms() * PBSM_PART_GRID)));
+}
+
+
+struct ScanLayout {
+  size_t cnt, base, partials, total;
+  u64 n, nb;
+};
+inline ScanLayout scan_layout(i64 n) {
+  ScanLayout L;
+  L.n = (u64)n;
+  L.nb = (L.n + kScanTile - 1) / kScanTile;
+  size_t o = 0;
+  L.cnt = o; o = align_up(o + 4 * (L.n + 1), 256);
+  L.base = o; o = align_up(o + 8 * (L.n + 1), 256);
+  L.partials = o; o = align_up(o + 8 * (L.nb + 1), 256);
+  L.total = o;
+  return L;
+}
+
+// join scratch: [ticket | status[n_units]]
+inline size_t join_scratch(i64 n_units) { return 256 + align_up(8 * (size_t)(n_units + 1), 256); }
+
+int set_smem_attrs() {
+  static bool done = false;
+  if (done) return 0;
+  cudaError_t e;
+  e = cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(JoinSmem));
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(JoinSmem));
+  if (e != cudaSuccess) return (int)e;
+
+  done = true;
+  return 0;
+}
+
+int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, int row_hi,
+                const pbsm_entry* r_list, const pbsm_entry* s_list, const pbsm_header* plan,
+                void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s,
+                i64 max_nested = -1, i64 max_other = -1) {
+  int rc = set_smem_attrs();
+  if (rc) return rc;
+  const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
+  Ws w = ws_bind(ws, L);
+  const bool bounded = plan == nullptr;  // sizes from the device header, grids = bounds
+  const i64 cn = bounded ? max_nested : plan->chunks_nested;
+  const i64 rest = bounded ? max_other : plan->chunks_sorted + plan->n_items;
+  const i64 n_units = cn + rest;
+  // the write guard (reads the cursors the scatter left behind) runs inside
+  // the nested join when there is one, else as its own kernel
+  const bool fused_guard = cn > 0;
+  if (!fused_guard) {
+    const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
+                                                                  (i64)num_sms() * 8));
+    k_guard<<<gb, 256, 0, s>>>(w.cur_r, w.cnt_r, w.cur_s, w.cnt_s, L.tiles, w.hdr);
+  }
+  cudaMemsetAsync(&w.hdr->pairs, 0, sizeof(int64_t), s);
+  if (n_units == 0) return launch_status();
+  if (ordered) cudaMemsetAsync(scratch, 0, join_scratch(n_units), s);
+  JoinArgs A;
+  for (int q = 0; q < 2; ++q) {
+    A.jrec[q] = w.jrec[q];
+    A.cdesc[q] = w.cdesc[q];
+  }
+  A.lrec = w.lrec;
+  A.lpre = w.lpre;
+  A.rl = reinterpret_cast<const Rec*>(r_list);
+  A.sl = reinterpret_cast<const Rec*>(s_list);
+  A.ticket = (u32*)scratch;
+  A.status = (u64*)((char*)scratch + 256);
+  A.pairs = (i64*)pairs;
+  A.capacity = capacity;
+  A.n_units = n_units;
+  A.hdr = w.hdr;
+  A.total = (unsigned long long*)&w.hdr->pairs;
+  A.ordered = ordered ? 1 : 0;
+  A.bounded = bounded ? 1 : 0;
+  A.g_cur_r = w.cur_r;
+  A.g_end_r = w.cnt_r;
+  A.g_cur_s = w.cur_s;
+  A.g_end_s = w.cnt_s;
+  A.g_tiles = fused_guard ? L.tiles : 0;
+  if (cn > 0) {
+    // one CTA per chunk (the ordered look-back takes tickets in launch order)
+    if (emit)
+      k_join_nested<true><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+    else
+      k_join_nested<false><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+  }
+  if (rest > 0) {
+    // the sorted/large launch keeps its own ticket (the look-back ids follow
+    // the nested chunks', whose kernel has finished by then)
+    if (ordered) cudaMemsetAsync(scratch, 0, 4, s);
+    if (emit)
+      k_join<true><<<(unsigned)rest, kJoinThreads, sizeof(JoinSmem), s>>>(A);
+    else
+      k_join<false><<<(unsigned)rest, kJoinThreads, sizeof(JoinSmem), s>>>(A);
+  }
+  return launch_status();
+}

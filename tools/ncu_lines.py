@@ -51,9 +51,9 @@ for ln in dis.splitlines():
     # mangled: <len><name>[template args]: "6k_join" does not match k_join_nested
     if cur_fn is None or f"{len(short)}{short}{want}" not in cur_fn:
         continue
-    mm = re.search(r'//## File ".*?", line (\d+)', ln)
+    mm = re.search(r'//## File "(.*?)", line (\d+)', ln)
     if mm:
-        cur = int(mm.group(1))
+        cur = (Path(mm.group(1)).name, int(mm.group(2)))
         continue
     mo = re.search(r"/\*([0-9a-f]{4,})\*/", ln)
     if mo and cur is not None:
@@ -66,9 +66,17 @@ for addr, s, i in sass:
     agg[L][1] += i
     ts += s
     ti += i
-src = Path(sys.argv[5] if len(sys.argv) > 5 else
-           "/root/repo/paper_1908_11740_b200/csrc/pbsm.cu").read_text().splitlines()
+csrc = Path(sys.argv[5] if len(sys.argv) > 5 else "/root/repo/paper_1908_11740_b200/csrc")
+texts = {}
 print(kname, f"samples={ts:.0f} inst={ti:.3e}")
 for L, (s, i) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
-    text = src[L - 1].strip()[:70] if 0 < L <= len(src) else "?"
-    print(f"{L:5d} stall {s / ts:6.3f} inst {i / ti:6.3f}  {text}")
+    if L == -1:
+        print(f"{'?':>20} stall {s / ts:6.3f} inst {i / ti:6.3f}")
+        continue
+    fname, line = L
+    if fname not in texts:
+        f = csrc / fname
+        texts[fname] = f.read_text().splitlines() if f.exists() else []
+    src = texts[fname]
+    text = src[line - 1].strip()[:70] if 0 < line <= len(src) else "?"
+    print(f"{fname + ':' + str(line):>20} stall {s / ts:6.3f} inst {i / ti:6.3f}  {text}")
