@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["CONFIGS", "ConfigSpec", "make_config", "make_side"]
+__all__ = ["CONFIGS", "ConfigSpec", "make_config", "make_side", "synthetic"]
 
 
 def _clip(a):
@@ -134,6 +134,36 @@ CONFIGS = {
     5: ConfigSpec("cfg5", 5_000_000, 5_000_000, 1000, True, gen_cfg5, gen_cfg5,
                   5_300_431, 5_300_431, 5_089_522),
 }
+
+
+def synthetic(n: int, x_extent_mean: float = 0.0, y_extent_mean: float = 0.0,
+              distribution: str = "uniform", seed: int = 0, clusters: int = 16,
+              cluster_sigma: float = 0.05):
+    """The reference's own synthetic workload (``SyntheticSpec`` /
+    ``generate_synthetic``, io.py:189-227), restated: uniform or
+    Gaussian-clustered centres, exponentially distributed extents around the
+    per-axis means (0 → points), boxes clipped to the unit square, ids =
+    row indices.  Used for the reference's acceptance anchors."""
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    if n == 0:
+        z = np.empty(0)
+        return np.empty(0, dtype=np.int64), z, z.copy(), z.copy(), z.copy()
+    rng = np.random.default_rng(seed)
+    if distribution == "uniform":
+        cx = rng.random(n)
+        cy = rng.random(n)
+    elif distribution == "gaussian-clustered":
+        centres = rng.random((max(1, clusters), 2))
+        pick = rng.integers(0, len(centres), n)
+        cx = _clip(centres[pick, 0] + rng.normal(0.0, cluster_sigma, n))
+        cy = _clip(centres[pick, 1] + rng.normal(0.0, cluster_sigma, n))
+    else:
+        raise ValueError(f"unknown distribution {distribution!r}")
+    ex = rng.exponential(x_extent_mean, n) if x_extent_mean > 0 else np.zeros(n)
+    ey = rng.exponential(y_extent_mean, n) if y_extent_mean > 0 else np.zeros(n)
+    return (np.arange(n, dtype=np.int64), _clip(cx - ex / 2), _clip(cx + ex / 2),
+            _clip(cy - ey / 2), _clip(cy + ey / 2))
 
 
 def make_side(cfg: int, side: str, n: int | None = None):

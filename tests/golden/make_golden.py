@@ -15,7 +15,9 @@ scratch copy and records the reference's own outputs on seeded inputs:
 * ``configs.npz``    — BASELINE cfg1 at full size and cfg2–5 scaled down:
   result_count, A_R/A_S (PartitionedDataset.total_assigned) and sorted pairs;
 * ``tile_of.npz``    — axis_tile_index known answers at and around i/k;
-* ``epsilon.npz``    — epsilon_distance_join known answers.
+* ``epsilon.npz``    — epsilon_distance_join known answers;
+* ``synthetic.npz``  — generate_synthetic outputs, a join of two of them and
+  the acceptance criterion-3 count (``python make_golden.py synthetic``).
 
 Nothing here runs on the GPU box; the .npz files are committed.
 """
@@ -180,9 +182,43 @@ def make_epsilon(sj):
     np.savez_compressed(HERE / "epsilon.npz", **out)
 
 
+SYNTH_SPECS = [  # (name, SyntheticSpec kwargs); ids are row indices
+    ("u", dict(n=4000, x_extent_mean=2e-3, y_extent_mean=2e-3, seed=11)),
+    ("g", dict(n=3000, x_extent_mean=5e-3, y_extent_mean=1e-3,
+               distribution="gaussian-clustered", seed=12, clusters=8, cluster_sigma=0.03)),
+    ("p", dict(n=2000, seed=13)),  # points
+]
+
+
+def make_synthetic(sj):
+    """The reference's generate_synthetic outputs (pins synth.synthetic), the
+    join of two of them (pairs), and the acceptance criterion-3 instance's
+    count (SyntheticSpec(1_000_000, 1e-3, 1e-3, seed 301 / 302), 1D K=100)."""
+    from sweepjoin.io import SyntheticSpec, generate_synthetic
+    out = {}
+    for name, kw in SYNTH_SPECS:
+        b = generate_synthetic(SyntheticSpec(**kw))
+        for c in ("ids", "xl", "xu", "yl", "yu"):
+            out[f"{name}_{c}"] = getattr(b, c)
+    r = generate_synthetic(SyntheticSpec(**SYNTH_SPECS[0][1]))
+    s = generate_synthetic(SyntheticSpec(**SYNTH_SPECS[1][1]))
+    rep = sj.join(r, s, sj.JoinConfig(sj.PartitionLayout("2d", 32), sink_mode="collect-pairs"))
+    out["ug_k32_pairs"] = sorted_pairs(rep.pairs)
+    r = generate_synthetic(SyntheticSpec(1_000_000, 1e-3, 1e-3, seed=301))
+    s = generate_synthetic(SyntheticSpec(1_000_000, 1e-3, 1e-3, seed=302))
+    rep = sj.join(r, s, sj.JoinConfig(sj.PartitionLayout("1d", 100), threads=os.cpu_count() or 1))
+    out["crit3_count"] = np.int64(rep.result_count)
+    print("criterion-3 count:", rep.result_count)
+    np.savez_compressed(HERE / "synthetic.npz", **out)
+
+
 if __name__ == "__main__":
     sj = import_reference()
+    if sys.argv[1:] == ["synthetic"]:
+        make_synthetic(sj)
+        sys.exit(0)
     make_tile_of(sj)
     make_instances(sj)
     make_epsilon(sj)
     make_configs(sj)
+    make_synthetic(sj)

@@ -77,6 +77,28 @@ def test_late_ids_mapped_like_direct_ids():
     assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
 
 
+def test_reference_synthetic_workloads(golden):
+    """The reference's own generate_synthetic workloads: a uniform x clustered
+    2D join (pairs from the reference) and the acceptance criterion-3 anchor
+    (SyntheticSpec(1_000_000, 1e-3, 1e-3, seed 301 / 302), 1D stripes K=100:
+    100 tiles of ~10^4 entries per side, the large-tile path) — count
+    3,989,612 as the reference reports it."""
+    from paper_1908_11740_b200.synth import synthetic
+    g = golden["synthetic"]
+    u = synthetic(4000, 2e-3, 2e-3, seed=11)
+    c = synthetic(3000, 5e-3, 1e-3, distribution="gaussian-clustered", seed=12, clusters=8,
+                  cluster_sigma=0.03)
+    rep = pb.join(pb.RectBatch(*u), pb.RectBatch(*c), _collect("2d", 32))
+    assert np.array_equal(oracle.sorted_pairs(rep.pairs), g["ug_k32_pairs"])
+    r = pb.RectBatch(*synthetic(1_000_000, 1e-3, 1e-3, seed=301))
+    s = pb.RectBatch(*synthetic(1_000_000, 1e-3, 1e-3, seed=302))
+    rep = pb.join(r, s, pb.JoinConfig(pb.PartitionLayout("1d", 100)))
+    assert rep.result_count == int(g["crit3_count"]) == 3_989_612
+    rep = pb.join(r, s, _collect("1d", 100))
+    assert rep.result_count == 3_989_612 and len(rep.pairs) == 3_989_612
+    assert len(np.unique(rep.pairs[:, 0] * 1_000_000 + rep.pairs[:, 1])) == 3_989_612
+
+
 def test_count_only_matches_collect():
     r, s, k = make_config(1)
     R, S = pb.RectBatch(*r), pb.RectBatch(*s)

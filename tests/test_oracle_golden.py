@@ -73,3 +73,38 @@ def test_generators_reproduce_survey_assignment_counts():
     spec = CONFIGS[1]
     assert int(oracle.count_tiles(r, "2d", k).sum()) == spec.a_r
     assert int(oracle.count_tiles(s, "2d", k).sum()) == spec.a_s
+
+
+def test_synthetic_generator_matches_reference(golden):
+    """synth.synthetic restates the reference's generate_synthetic (io.py:189-227)
+    byte for byte (fixtures from the reference itself)."""
+    from paper_1908_11740_b200.synth import synthetic
+    g = golden["synthetic"]
+    for name, kw in _synth_specs():
+        got = synthetic(**kw)
+        for c, a in zip(("ids", "xl", "xu", "yl", "yu"), got):
+            assert np.array_equal(a, g[f"{name}_{c}"]), (name, c)
+
+
+def _synth_specs():
+    # the specs of tests/golden/make_golden.py SYNTH_SPECS
+    return [
+        ("u", dict(n=4000, x_extent_mean=2e-3, y_extent_mean=2e-3, seed=11)),
+        ("g", dict(n=3000, x_extent_mean=5e-3, y_extent_mean=1e-3,
+                   distribution="gaussian-clustered", seed=12, clusters=8, cluster_sigma=0.03)),
+        ("p", dict(n=2000, seed=13)),
+    ]
+
+
+def test_oracle_synthetic_join_and_criterion3(golden):
+    """The oracle on the reference's synthetic workloads: the u x g join's pairs,
+    and the acceptance criterion-3 instance (1M x 1M, 1D K=100) count."""
+    from paper_1908_11740_b200.synth import synthetic
+    g = golden["synthetic"]
+    specs = dict(_synth_specs())
+    res = oracle.join(synthetic(**specs["u"]), synthetic(**specs["g"]), "2d", 32)
+    assert np.array_equal(oracle.sorted_pairs(res["pairs"]), g["ug_k32_pairs"])
+    r = synthetic(1_000_000, 1e-3, 1e-3, seed=301)
+    s = synthetic(1_000_000, 1e-3, 1e-3, seed=302)
+    res = oracle.join(r, s, "1d", 100, threads=8, collect=False)
+    assert res["count"] == int(g["crit3_count"]) == 3_989_612
