@@ -157,8 +157,9 @@ def strip_join(rr, ss, k: int, row_lo: int, row_hi: int, device=None, collect: b
     exchange dict)."""
     from . import device as dev
 
-    rd = dev.to_device(rr, device)
-    sd = rd if ss is rr else dev.to_device(ss, device)
+    # coordinates first on a side stream, ids last (mapped after the join):
+    # the strip pipeline overlaps the PCIe copy, as in engine.join
+    rd, sd = dev.to_device_pipelined(rr, ss, device if device is not None else "cuda")
     res = dev.run_join(rd, sd, k, k, collect=collect, row_lo=row_lo, row_hi=row_hi)
     ex = exchange_counts(res.count, res.header["a_r"], res.header["a_s"], device=device)
     return res, ex
