@@ -157,19 +157,30 @@ def _workspace(lib, device, kx, ky, row_lo, row_hi) -> torch.Tensor:
 _buf_cache: dict = {}
 
 
-def _buffer(device, name: str, shape: tuple, dtype) -> torch.Tensor:
+def _raw_stream(device) -> int:
+    """cudaStream_t of the current stream on ``device`` (the cheap accessor:
+    torch.cuda.current_stream() builds a Stream object, ~2 µs per call)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(idx)
+
+
+def _buffer(device, name: str, shape: tuple, dtype, stream: int) -> torch.Tensor:
     n = 1
     for d in shape:
         n *= d
     # per (device, stream): joins enqueued on different streams never share
-    key = (str(device), torch.cuda.current_stream(device).cuda_stream, name)
-    buf = _buf_cache.get(key)
+    key = (device, stream, name)
+    ent = _buf_cache.get(key)
+    if ent is not None and ent[1] == shape and ent[0].dtype == dtype:
+        return ent[2]  # the same view as last time
+    buf = ent[0] if ent is not None else None
     if buf is None or buf.dtype != dtype or buf.numel() < n:
         _buf_cache.pop(key, None)
-        del buf  # the old block is free before the larger one is requested
+        del buf, ent  # the old block is free before the larger one is requested
         buf = torch.empty(max(n, 1), dtype=dtype, device=device)
-        _buf_cache[key] = buf
-    return buf[:n].view(shape)
+    view = buf[:n].view(shape)
+    _buf_cache[key] = (buf, shape, view)
+    return view
 
 
 def release_buffers() -> None:
@@ -287,7 +298,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     if len(r) == 0 or len(s) == 0:
         empty = torch.empty((0, 2), dtype=torch.int64, device=device) if collect else None
         return DeviceJoinResult(0, empty)
-    stream = torch.cuda.current_stream(device).cuda_stream
+    stream = _raw_stream(device)
     ws = _workspace(lib, device, kx, ky, row_lo, row_hi)
     wsp = ws.data_ptr()
     grid = (kx, ky, row_lo, row_hi)
@@ -297,7 +308,9 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     mark("start")
     _native.check(lib.pbsm_init(wsp, *grid, stream), "pbsm_init")
     mark("init")
-    cur = torch.cuda.current_stream(device)
+    # (the Stream object only when there are copy events to wait on)
+    cur = (torch.cuda.current_stream(device)
+           if r.coords_ready is not None or s.coords_ready is not None else None)
     # ids still in flight (to_device_pipelined): the entries carry row
     # indices and the pair list is mapped to ids at the end (pbsm_map_ids),
     # so nothing before the final map waits for the id columns
@@ -326,7 +339,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     lists = []
     thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
-        ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64)  # 64 B records
+        ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64,
+                      stream)  # 64 B records
         ids_p = None if late else _ptr(b.ids)
         # the copy costs ~80 B per rectangle; it pays where the random record
         # writes dominate: large lists and heavy replication (cfg4: 1.7
@@ -351,7 +365,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     if guess is not None:
         cap, cn, rest = guess["pairs"], guess["nested"], guess["other"]
         scratch = _buffer(device, "scratch", (int(lib.pbsm_join_scratch_bytes(cn + rest)),),
-                          torch.uint8)
+                          torch.uint8, stream)
         pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
         mark("alloc")
         _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), sl.data_ptr(), cn,
@@ -384,7 +398,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
 
     n_units = h.n_units
     scratch = _buffer(device, "scratch", (int(lib.pbsm_join_scratch_bytes(n_units)),),
-                      torch.uint8)
+                      torch.uint8, stream)
     pairs = None
     if not collect:
         _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), C.byref(h),
