@@ -117,6 +117,51 @@ def test_tile_counts_match_reference(golden):
     assert res.header["a_r"] == CONFIGS[1].a_r and res.header["a_s"] == CONFIGS[1].a_s
 
 
+def _expected_entries(b, k, other_counts, own_counts):
+    """(id, label) of every join-tile assignment of one input, computed on the
+    host: tile ranges by the exact axis_tile_index, label bit 1 = x-out (starts
+    left of the tile), bit 0 = y-out (starts below it)."""
+    from paper_1908_11740_b200 import parallel
+    ids, xl, xu, yl, yu = b
+    c0, c1 = parallel._tile_index(xl, k), parallel._tile_index(xu, k)
+    r0, r1 = parallel._tile_index(yl, k), parallel._tile_index(yu, k)
+    out = []
+    for i in range(len(ids)):
+        for row in range(r0[i], r1[i] + 1):
+            for col in range(c0[i], c1[i] + 1):
+                t = row * k + col
+                if other_counts[t] > 0 and own_counts[t] > 0:
+                    out.append((ids[i], (2 if col != c0[i] else 0) | (1 if row != r0[i] else 0)))
+    return sorted(out)
+
+
+def test_scatter_entries_are_the_join_tile_assignments(golden):
+    """Per-stage parity of the partition: after the scatter, each input's tile
+    lists hold exactly its join-tile assignments (partition.py's tile
+    batches restricted to tiles where both inputs are non-empty), each with
+    the class label of its tile and the rectangle's own coordinates."""
+    r, s, k = make_config(1, 0.2)
+    cnt = dev.run_join(dev.to_device(r), dev.to_device(s), k, k, collect=False,
+                       keep_counts=True).tile_counts
+    cr, cs = (c.cpu().numpy() for c in cnt)
+    res = dev.run_join(dev.to_device(r), dev.to_device(s), k, k)
+    stream = torch.cuda.current_stream().cuda_stream
+    for side, b, own, other, n in ((0, r, cr, cs, res.header["list_r"]),
+                                   (1, s, cs, cr, res.header["list_s"])):
+        lst = dev._buf_cache[(torch.device("cuda", 0), stream, f"list{side}")][2][:n].cpu().numpy()
+        key = lst[:, 0].view(np.uint64)
+        got_ids, got_lab = lst[:, 4], (key >> np.uint64(62)).astype(np.int64)
+        assert sorted(zip(got_ids.tolist(), got_lab.tolist())) == \
+            [(int(a), int(c)) for a, c in _expected_entries(b, k, other, own)]
+        # the record carries the rectangle's own MBR (xl without its label bits)
+        xl = (key & np.uint64((1 << 62) - 1)).view(np.float64)
+        row = {int(i): j for j, i in enumerate(b[0])}
+        idx = np.array([row[int(i)] for i in got_ids])
+        assert np.array_equal(xl, b[1][idx]) and np.array_equal(lst[:, 1].view(np.float64), b[2][idx])
+        assert np.array_equal(lst[:, 2].view(np.float64), b[3][idx])
+        assert np.array_equal(lst[:, 3].view(np.float64), b[4][idx])
+
+
 def _dense_tile_instance(n_dense=900, n_other=700, seed=3):
     """One tile holding > kLmax entries (large-tile path) next to normal tiles."""
     rng = np.random.default_rng(seed)
