@@ -211,14 +211,15 @@ def reference_arm(args):
 
 
 # ---------------------------------------------------------------- GPU arm
-def count_launches(h: dict, dev) -> int:
+def count_launches(h: dict, dev, n_r: int, n_s: int) -> int:
     """Our kernels per join step (see device.run_join / pbsm.cu host glue)."""
     n = 1            # k_init
     n += 2           # k_count R, S
     n += 3           # k_plan_reduce, k_plan_partials, k_plan_apply
     n += 2           # k_scatter R, S
-    for total in (h["list_r"], h["list_s"]):  # binned scatter: 3 scan kernels + k_bin_copy
-        n += 4 if 64 * total > dev.BIN_LIST_BYTES else 0
+    for total, m in ((h["list_r"], n_r), (h["list_s"], n_s)):
+        # binned scatter: 3 scan kernels + k_bin_copy
+        n += 4 if dev._binned(total, m, None) else 0
     # k_join_nested (with the write guard fused in) or a stand-alone k_guard
     n += 1
     n += 1 if h["chunks_sorted"] + h["n_items"] > 0 else 0   # k_join (sorted / large units)
@@ -438,7 +439,7 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return 0
-    launches = count_launches(res.header, dev) * args.steps
+    launches = count_launches(res.header, dev, len(rr[0]), len(ss[0])) * args.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": step_s * 1e3,
