@@ -259,6 +259,16 @@ def pair_capacity(h) -> int:
 BIN_LIST_BYTES = int(os.environ.get("PBSM_BIN_BYTES", 1 << 30))
 
 
+def _binned(total: int, n: int, bin_bytes: int | None) -> bool:
+    """Whether a tile list of ``total`` entries from ``n`` rectangles goes
+    through the row-band copy: the copy costs ~80 B per rectangle, so it pays
+    only where the random record writes dominate — large lists and heavy
+    replication (cfg4: 1.7 entries per rectangle; cfg2/cfg3/cfg5: 1.1-1.5,
+    measured slower).  ``bin_bytes`` None = BIN_LIST_BYTES, 0 = always."""
+    thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
+    return 64 * total > thresh and (bin_bytes == 0 or total >= 1.6 * n)
+
+
 def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream, ids_p) -> torch.Tensor:
     """Row-band copy of one input: n 40-byte records {id (or row), xl, xu, yl, yu}."""
     band = torch.empty((len(b), 5), dtype=torch.int64, device=b.device)
@@ -337,15 +347,11 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         list_r, list_s = guess["list_r"], guess["list_s"]
 
     lists = []
-    thresh = BIN_LIST_BYTES if bin_bytes is None else bin_bytes
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
         ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64,
                       stream)  # 64 B records
         ids_p = None if late else _ptr(b.ids)
-        # the copy costs ~80 B per rectangle; it pays where the random record
-        # writes dominate: large lists and heavy replication (cfg4: 1.7
-        # entries per rectangle; cfg2/cfg3/cfg5: 1.1-1.5, measured slower)
-        if 64 * total > thresh and (bin_bytes == 0 or total >= 1.6 * len(b)):
+        if _binned(total, len(b), bin_bytes):
             band = _banded(lib, b, side, wsp, grid, stream, ids_p)
             mark("bin")
             _native.check(lib.pbsm_scatter_banded(band.data_ptr(), len(b), side, wsp, *grid,
