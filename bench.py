@@ -211,6 +211,34 @@ def reference_arm(args):
 
 
 # ---------------------------------------------------------------- GPU arm
+def h2d_floor(rh, sh, e2e_s: float) -> dict:
+    """The e2e join's floor: the same pinned input columns copied host→device
+    alone (one stream, back to back, CUDA events; best of 3).  ``frac`` =
+    that copy time ÷ the e2e step time (1.0 = the join adds nothing to the
+    PCIe transfer of its inputs)."""
+    import torch
+
+    cols = [c for b in (rh, sh) if b is not None for c in (b.ids, b.xl, b.xu, b.yl, b.yu)]
+    host = [torch.from_numpy(c) for c in cols]
+    dev = [torch.empty_like(h, device="cuda") for h in host]
+    st = torch.cuda.Stream()
+    best = float("inf")
+    for _ in range(3):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            e0.record(st)
+            for d_, h_ in zip(dev, host):
+                d_.copy_(h_, non_blocking=True)
+            e1.record(st)
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    nbytes = sum(h.numel() * h.element_size() for h in host)
+    del dev
+    return {"h2d_GBps": nbytes / best / 1e9, "h2d_ms": best * 1e3, "frac": best / e2e_s,
+            "note": "input columns copied alone from the same pinned buffers"}
+
+
 def count_launches(h: dict, dev, n_r: int, n_s: int) -> int:
     """Our kernels per join step (see device.run_join / pbsm.cu host glue)."""
     n = 1            # k_init
@@ -379,11 +407,13 @@ def main():
             rep = engine.join(Rh, Sh, cfgj)
             ts.append(time.perf_counter() - t0)
         e2e_t = statistics.median(ts)
+        h2d = 40 * (n_r + (0 if self_join else n_s))
         e2e = {"value": (n_r + n_s) / e2e_t, "unit": UNIT,
-               "h2d_bytes_per_step": 40 * (n_r + (0 if self_join else n_s)),
+               "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 16 * rep.result_count, "ms_per_step": e2e_t * 1e3,
                "api": "paper_1908_11740_b200.join(RectBatch, RectBatch, JoinConfig("
-                      "PartitionLayout('2d', K), sink_mode='collect-pairs'))"}
+                      "PartitionLayout('2d', K), sink_mode='collect-pairs'))",
+               "link": h2d_floor(Rh, None if self_join else Sh, e2e_t)}
     elif not args.no_e2e:
         # N ranks: each rank's strip (split on the host beforehand — the
         # distribution step) from pinned host memory through the public strip
