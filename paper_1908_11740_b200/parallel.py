@@ -5,7 +5,8 @@ independent join units, so the grid shards without any
 data-path collective:
 
 * ``plan_strips``  — cut the K tile rows into N contiguous strips whose
-  per-row entry counts (|R|+|S| assignments) are balanced by a prefix sum;
+  per-row cost (|R|+|S| assignments plus capped per-tile pair tests) is
+  balanced by a prefix sum;
 * ``strip_inputs`` — the rectangles a rank needs: those whose tile-row range
   [tile_of(yl), tile_of(yu)] meets the strip (host-side distribution, before
   the timed window) — or, when every rank starts from its own slice of the
@@ -59,15 +60,50 @@ def _row_entries(b, k: int) -> np.ndarray:
     return np.cumsum(d[:k])
 
 
+# Strip cost model (per tile row, integer so the host and the distributed
+# plans agree exactly): KAPPA × entries + Σ_T min(|R_T|·|S_T|, CAP·(|R_T|+|S_T|))
+# with the per-tile counts taken at each rectangle's lower-left tile.  Entries
+# price the count / scatter / staging work (~47 ps each on one B200); the
+# pair term prices the mini-join tests and output, which concentrate where
+# both inputs pile up (cfg2: the clusters clipped onto y = 0 and y = 1 put 40%
+# of all |R_T|·|S_T| in rows 0 and 1999).  Calibrated on the cfg2 strips
+# timed one by one (tools/strip_emulation.py): ~1/2 entry per pair test; the
+# cap stops the brute-forced giant tiles (~0.3 ps per test) from dominating.
+STRIP_KAPPA = 2
+STRIP_CAP = 256
+
+
+def _row_cost(entries: np.ndarray, tr: np.ndarray, ts: np.ndarray) -> np.ndarray:
+    """The cost model on per-row entries and (k, k) per-tile counts (numpy or torch)."""
+    pairs = tr * ts
+    cap = STRIP_CAP * (tr + ts)
+    if isinstance(tr, np.ndarray):
+        tests = np.minimum(pairs, cap)
+    else:
+        import torch
+
+        tests = torch.minimum(pairs, cap)
+    return STRIP_KAPPA * entries + tests.sum(1)
+
+
+def _tile_counts(b, k: int) -> np.ndarray:
+    """Rectangles per tile at their lower-left tile, (k, k) int64."""
+    t = row_range(b, k)[0] * k + _tile_index(b[1], k)
+    return np.bincount(t, minlength=k * k).reshape(k, k).astype(np.int64)
+
+
 def plan_strips(r, s, k: int, world: int) -> list[int]:
-    """Row cut points [0 = c_0 < ... < c_N = k] balancing per-row entries."""
+    """Row cut points [0 = c_0 < ... < c_N = k] balancing the per-row cost
+    (entries and capped pair tests, ``_row_cost``) by a prefix sum."""
     if world <= 1:
         return [0, k]
     if world > k:
         raise ValueError(f"cannot split {k} tile rows over {world} ranks")
     w_r = _row_entries(r, k)
     w = w_r + (w_r if s is r else _row_entries(s, k))
-    return _cut_rows(w, k, world)
+    tr = _tile_counts(r, k)
+    ts = tr if s is r else _tile_counts(s, k)
+    return _cut_rows(_row_cost(w, tr, ts), k, world)
 
 
 def strip_inputs(b, k: int, row_lo: int, row_hi: int):
@@ -242,8 +278,9 @@ def _cut_rows(w, k: int, world: int) -> list[int]:
 
 def plan_strips_distributed(r_cols, s_cols, k: int, group=None) -> list[int]:
     """plan_strips when every rank holds only a slice of R and S: per-row
-    entry counts of the local slices (torch, on the slices' device), one
-    all_reduce, then the same cut rule — every rank gets identical cuts."""
+    entry counts and per-tile counts of the local slices (torch, on the
+    slices' device), one all_reduce, then the same cost model and cut rule —
+    every rank gets identical cuts."""
     import torch
     import torch.distributed as dist
 
@@ -254,6 +291,7 @@ def plan_strips_distributed(r_cols, s_cols, k: int, group=None) -> list[int]:
         raise ValueError(f"cannot split {k} tile rows over {world} ranks")
     dev = r_cols[0].device
     d = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+    tiles = []
     for cols in ((r_cols,) if s_cols is None else (r_cols, s_cols)):
         _, xl, xu, yl, yu = cols
         c0, c1 = tile_rows_torch(xl, xu, k)
@@ -261,10 +299,16 @@ def plan_strips_distributed(r_cols, s_cols, k: int, group=None) -> list[int]:
         span = c1 - c0 + 1
         d.scatter_add_(0, r0, span)
         d.scatter_add_(0, r1 + 1, -span)
+        tiles.append(torch.bincount(r0 * k + c0, minlength=k * k).to(torch.int64))
     if s_cols is None:
         d *= 2
-    dist.all_reduce(d, group=group)
-    w = torch.cumsum(d[:k], 0).cpu().numpy()
+    # one all_reduce: per-row entry deltas and both inputs' per-tile counts
+    buf = torch.cat([d] + tiles)
+    dist.all_reduce(buf, group=group)
+    w = torch.cumsum(buf[:k], 0)
+    tr = buf[k + 1:k + 1 + k * k].view(k, k)
+    ts = tr if s_cols is None else buf[k + 1 + k * k:].view(k, k)
+    w = _row_cost(w, tr, ts).cpu().numpy()
     return _cut_rows(w, k, world)
 
 

@@ -29,12 +29,23 @@ def test_plan_strips_cover_rows(cfg, scale, world):
     assert all(a < b for a, b in zip(cuts, cuts[1:]))
 
 
-def test_plan_strips_balances_entries():
+def test_plan_strips_balances_cost():
     r, s, k = make_config(2, 0.05)
     cuts = parallel.plan_strips(r, s, k, 4)
     w = parallel._row_entries(r, k) + parallel._row_entries(s, k)
-    per = [w[a:b].sum() for a, b in zip(cuts, cuts[1:])]
-    assert max(per) / (sum(per) / 4) < 1.2  # equal-row strips give ~1.4 on cfg2
+    cost = parallel._row_cost(w, parallel._tile_counts(r, k), parallel._tile_counts(s, k))
+    per = [cost[a:b].sum() for a, b in zip(cuts, cuts[1:])]
+    assert max(per) / (sum(per) / 4) < 1.2
+    ent = [w[a:b].sum() for a, b in zip(cuts, cuts[1:])]
+    assert max(ent) / (sum(ent) / 4) < 1.5  # equal-row strips give ~1.4 on cfg2
+
+
+def test_row_cost_caps_giant_tiles():
+    tr = np.array([[1000, 2], [0, 0]], dtype=np.int64)
+    ts = np.array([[3000, 3], [5, 0]], dtype=np.int64)
+    got = parallel._row_cost(np.array([10, 20], dtype=np.int64), tr, ts)
+    cap = parallel.STRIP_CAP * 4000
+    assert got.tolist() == [parallel.STRIP_KAPPA * 10 + cap + 6, parallel.STRIP_KAPPA * 20]
 
 
 def _tile_rows(b, k):
