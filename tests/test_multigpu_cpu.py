@@ -119,6 +119,11 @@ def _dist_worker(rank, world, port, out):
         sl_r = tuple(torch.from_numpy(np.ascontiguousarray(a[rank::world])) for a in r)
         sl_s = tuple(torch.from_numpy(np.ascontiguousarray(a[rank::world])) for a in s)
         assert parallel.plan_strips_distributed(sl_r, sl_s, k) == cuts
+        # self-join (s_cols=None): the same cost model on R alone
+        r5, _, k5 = make_config(5, 0.01)
+        sl5 = tuple(torch.from_numpy(np.ascontiguousarray(a[rank::world])) for a in r5)
+        assert parallel.plan_strips_distributed(sl5, None, k5) == \
+            parallel.plan_strips(r5, r5, k5, world)
         lo, hi = cuts[rank], cuts[rank + 1]
         got = {}
         for name, b in (("r", r), ("s", s)):
