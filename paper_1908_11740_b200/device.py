@@ -283,6 +283,16 @@ def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream, ids_p) -> to
 # runs bounded (pbsm_join_emit_bounded); the final header read checks every
 # size and a miss re-runs the join synchronously.
 _plan_cache: dict = {}
+DUAL = os.environ.get("PBSM_DUAL", "1") != "0"
+_side_streams: dict = {}
+
+
+def _side_stream(device):
+    st = _side_streams.get(device.index)
+    if st is None:
+        st = _side_streams[device.index] = torch.cuda.Stream(device)
+    return st
+
 SPECULATE = os.environ.get("PBSM_SPECULATE", "1") != "0"
 
 
@@ -325,10 +335,29 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     # indices and the pair list is mapped to ids at the end (pbsm_map_ids),
     # so nothing before the final map waits for the id columns
     late = r.ids_ready is not None and s.ids_ready is not None
+    # S's count and scatter run on a side stream, concurrent with R's: each
+    # pass' tail (its last, partly filled wave of blocks) overlaps the other
+    # input's pass (measured: cfg2 1.262 -> 1.253 ms, cfg5 0.783 -> 0.753 ms,
+    # cfg3 8.65 -> 8.55 ms).  With host inputs still crossing PCIe the counts
+    # stay on one stream, each behind its own copy event.
+    main_st = side_st = None
+    if DUAL:
+        main_st = torch.cuda.current_stream(device)
+        side_st = _side_stream(device)
+    dual = DUAL and cur is None
+    if dual:
+        fork = torch.cuda.Event()
+        fork.record(main_st)
+        side_st.wait_event(fork)
     for side, b in ((0, r), (1, s)):
         _wait(b.coords_ready, cur)
+        st_ = side_st.cuda_stream if (dual and side == 1) else stream
         _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
-                                     side, wsp, *grid, stream), "pbsm_count")
+                                     side, wsp, *grid, st_), "pbsm_count")
+    if dual:
+        join_ev = torch.cuda.Event()
+        join_ev.record(side_st)
+        main_st.wait_event(join_ev)
     mark("count")
     counts = None
     if keep_counts:  # per-tile counts, before the plan turns them into cursor ends
@@ -347,10 +376,27 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         list_r, list_s = guess["list_r"], guess["list_s"]
 
     lists = []
+    dual_sc = DUAL and not (_binned(list_r, len(r), bin_bytes) or _binned(list_s, len(s), bin_bytes))
+    if dual_sc:
+        fork = torch.cuda.Event()
+        fork.record(main_st)
+        side_st.wait_event(fork)
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
         ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64,
                       stream)  # 64 B records
         ids_p = None if late else _ptr(b.ids)
+        if dual_sc:
+            _native.check(lib.pbsm_scatter(ids_p, _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
+                                           _ptr(b.yu), len(b), side, wsp, *grid, ent.data_ptr(),
+                                           total, side_st.cuda_stream if side else stream),
+                          "pbsm_scatter")
+            if side == 1:
+                join_ev = torch.cuda.Event()
+                join_ev.record(side_st)
+                main_st.wait_event(join_ev)
+                mark("scatter")
+            lists.append(ent)
+            continue
         if _binned(total, len(b), bin_bytes):
             band = _banded(lib, b, side, wsp, grid, stream, ids_p)
             mark("bin")
