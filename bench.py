@@ -488,7 +488,10 @@ def main():
                      "phase": dom, "achieved": dom_gbs, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_gbs / hbm,
                      "traffic": traffic, "alg_bytes_per_launch": dom_bytes,
-                     "launches_per_step": n_launch, "launch_ms": dom_time * 1e3},
+                     "launches_per_step": n_launch, "launch_ms": dom_time * 1e3,
+                     "timing": "phase span on the launch stream (CUDA events) / launches: "
+                               "R's and S's count/scatter launches run concurrently on two "
+                               "streams, so this is the phase's aggregate rate"},
         "step_roofline": {"alg_bytes": B_alg, "achieved": step_gbs, "peak": hbm * world,
                           "frac": step_gbs / (hbm * world), "unit": "GB/s", "formula": ALG_NOTE},
         "phases_ms": {k_: v * 1e3 for k_, v in phases.items()},
