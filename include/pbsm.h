@@ -215,6 +215,18 @@ int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int
 int pbsm_map_ids(int64_t* pairs, int64_t n, const int64_t* r_ids, const int64_t* s_ids,
                  void* stream);
 
+/* Row-index pairs (pairs[2i], pairs[2i+1], i < n) → out, grouped by the id
+ * chunk of their last-landing id column: group g = min(s_row / chunk_rows,
+ * n_groups - 1) (self_join != 0: max(r_row, s_row)), groups laid out in order,
+ * order inside a group unspecified.  counts (device int64[2 * n_groups]):
+ * [0, n_groups) receives the group sizes, the rest is cursor scratch.
+ * 1 <= n_groups <= 32; out must not alias pairs.  Lets a join over host
+ * inputs map and copy back each group as soon as its ids have landed (the
+ * reference returns the pair list at once, engine.py:293-309; this only
+ * changes when the bytes move). */
+int pbsm_group_pairs(const int64_t* pairs, int64_t n, int64_t chunk_rows, int32_t n_groups,
+                     int32_t self_join, int64_t* out, int64_t* counts, void* stream);
+
 /* SJB1 dataset body (load_mbr_binary, io.py:113-141): n packed 40-byte
  * little-endian records {id u64, x_l, y_l, x_u, y_u f64} at an 8-byte aligned
  * device address → the RectBatch SoA columns (ids reinterpreted as int64,

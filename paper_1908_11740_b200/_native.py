@@ -30,7 +30,7 @@ EXPORTED = (
     "pbsm_scatter_banded",
     "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit", "pbsm_join_emit_bounded",
     "pbsm_unpack_records", "pbsm_refine_scratch_bytes", "pbsm_refine_result_offset",
-    "pbsm_refine", "pbsm_map_ids",
+    "pbsm_refine", "pbsm_map_ids", "pbsm_group_pairs",
 )
 
 
@@ -84,6 +84,7 @@ _SIGNATURES = {
                                          _P, _I64, _P]),
     "pbsm_unpack_records": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "pbsm_map_ids": (C.c_int, [_P, _I64, _P, _P, _P]),
+    "pbsm_group_pairs": (C.c_int, [_P, _I64, _I64, _I32, _I32, _P, _P, _P]),
     "pbsm_refine_scratch_bytes": (_I64, [_I64]),
     "pbsm_refine_result_offset": (_I64, [_I64]),
     "pbsm_refine": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),

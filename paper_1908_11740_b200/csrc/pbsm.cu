@@ -286,6 +286,25 @@ int pbsm_map_ids(int64_t* pairs, int64_t n, const int64_t* r_ids, const int64_t*
   return launch_status();
 }
 
+int pbsm_group_pairs(const int64_t* pairs, int64_t n, int64_t chunk_rows, int32_t n_groups,
+                     int32_t self_join, int64_t* out, int64_t* counts, void* stream) {
+  if (n < 0 || chunk_rows < 1 || n_groups < 1 || n_groups > kMaxGroups || !counts)
+    return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(counts);
+  cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long) * n_groups, s);  // counts | cursors
+  if (n == 0) return launch_status();
+  if (!pairs || !out || pairs == out) return PBSM_E_ARG;
+  // a few thousand pairs per block: the per-block group runs stay long
+  const unsigned blocks = (unsigned)std::max<i64>(1, std::min<i64>((n + 2047) / 2048,
+                                                                   (i64)num_sms() * 8));
+  k_group_count<<<blocks, 256, 0, s>>>((const i64*)pairs, n, chunk_rows, n_groups, self_join,
+                                       cnt);
+  k_group_place<<<blocks, 256, 0, s>>>((const i64*)pairs, n, chunk_rows, n_groups, self_join,
+                                       cnt, cnt + n_groups, (i64*)out);
+  return launch_status();
+}
+
 int pbsm_unpack_records(const void* records, int64_t n, int64_t* ids, double* xl, double* xu,
                         double* yl, double* yu, uint32_t* bad, void* stream) {
   if (n < 0 || !bad) return PBSM_E_ARG;

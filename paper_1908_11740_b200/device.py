@@ -42,6 +42,9 @@ class DeviceRects:
     # wait on them right before the first kernel that reads them
     coords_ready: object = None
     ids_ready: object = None
+    # the last-landing id column is copied in equal row chunks: (chunk_rows,
+    # [event per chunk]) — see staged_pairs_to_host
+    id_chunks: object = None
 
     def __len__(self) -> int:
         return int(self.ids.shape[0])
@@ -70,6 +73,10 @@ def to_device(batch, device="cuda", pinned: bool = True) -> DeviceRects:
 
 
 _copy_streams: dict = {}
+# staged return of host-input joins: the last id column crosses PCIe in
+# ID_GROUPS chunks when it has at least ID_CHUNK_MIN rows
+ID_GROUPS = int(os.environ.get("PBSM_ID_GROUPS", 8))
+ID_CHUNK_MIN = 1 << 20
 
 
 def _host_tensor(a, dt, pinned: bool) -> torch.Tensor:
@@ -111,11 +118,28 @@ def to_device_pipelined(r, s, device="cuda"):
             ev = torch.cuda.Event()
             ev.record(cs)
             coord_ev.append(ev)
-        for (hb, db), cev in zip(zip(host, dev_cols), coord_ev):
-            db[0].copy_(hb[0], non_blocking=True)
-            iev = torch.cuda.Event()
-            iev.record(cs)
-            out.append(DeviceRects(*db, coords_ready=cev, ids_ready=iev))
+        last = len(host) - 1
+        for j, ((hb, db), cev) in enumerate(zip(zip(host, dev_cols), coord_ev)):
+            chunks = None
+            n = hb[0].shape[0]
+            if j == last and n >= ID_CHUNK_MIN:
+                # the last id column in ID_GROUPS row chunks, an event each:
+                # the pairs whose ids are complete go back while the rest
+                # is still in flight (staged_pairs_to_host)
+                rows = -(-n // ID_GROUPS)
+                evs = []
+                for a in range(0, n, rows):
+                    db[0][a:a + rows].copy_(hb[0][a:a + rows], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(cs)
+                    evs.append(e)
+                chunks = (rows, evs)
+                iev = evs[-1]
+            else:
+                db[0].copy_(hb[0], non_blocking=True)
+                iev = torch.cuda.Event()
+                iev.record(cs)
+            out.append(DeviceRects(*db, coords_ready=cev, ids_ready=iev, id_chunks=chunks))
     return (out[0], out[0]) if s is r else (out[0], out[1])
 
 
@@ -131,6 +155,7 @@ class DeviceJoinResult:
     header: dict = field(default_factory=dict)
     times: dict = field(default_factory=dict)  # seconds per phase (CUDA events)
     tile_counts: tuple | None = None      # (cnt_r, cnt_s) device views when kept
+    rows_pending: bool = False            # pairs still hold row indices (defer_map)
 
 
 _ws_cache: dict = {}
@@ -300,7 +325,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
              row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
              keep_counts: bool = False, probe: PhaseProbe | None = None,
              ordered: bool = False, nested_max: int = -1,
-             bin_bytes: int | None = None) -> DeviceJoinResult:
+             bin_bytes: int | None = None, defer_map: bool = False) -> DeviceJoinResult:
     """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
 
     ``probe`` (optional) gets an event after each library call, named after
@@ -309,6 +334,9 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     ``ordered`` selects the look-back (unit-major) output placement;
     ``bin_bytes``: tile lists larger than this go through the row-band copy
     (pbsm_bin) before the scatter (default BIN_LIST_BYTES; 0 = always).
+    ``defer_map``: with id columns still in flight (to_device_pipelined) the
+    pairs are returned as row indices (``rows_pending``) for
+    staged_pairs_to_host instead of being mapped here.
     """
     mark = probe.mark if probe is not None else (lambda name: None)
     lib = _native.load()
@@ -434,14 +462,16 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
             _plan_cache.pop(key, None)
             return run_join(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
                             timing=timing, keep_counts=keep_counts, probe=probe,
-                            ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes)
+                            ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes,
+                            defer_map=defer_map)
         count = int(h2.pairs)
-        if late:
+        if late and not defer_map:
             _map_ids(lib, pairs, count, r, s, cur, stream)
         if ev:
             ev[2].record()
             ev[2].synchronize()
-        res = DeviceJoinResult(count, pairs[:count], header=h2.as_dict())
+        res = DeviceJoinResult(count, pairs[:count], header=h2.as_dict(),
+                               rows_pending=late and defer_map)
         if ev:
             res.times = {"partition": ev[0].elapsed_time(ev[1]) / 1e3,
                          "join": ev[1].elapsed_time(ev[2]) / 1e3,
@@ -474,7 +504,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                 break
             cap = count  # rare: the estimate was short, emit again into an exact buffer
         pairs = pairs[:count]
-        if late:
+        if late and not defer_map:
             _map_ids(lib, pairs, count, r, s, cur, stream)
         if not ordered and not keep_counts:
             _plan_cache.clear()  # one shape at a time
@@ -484,7 +514,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     if ev:
         ev[2].record()
         ev[2].synchronize()
-    res = DeviceJoinResult(count, pairs, header=h2.as_dict())
+    res = DeviceJoinResult(count, pairs, header=h2.as_dict(),
+                           rows_pending=late and defer_map and pairs is not None)
     if ev:
         res.times = {"partition": ev[0].elapsed_time(ev[1]) / 1e3,
                      "join": ev[1].elapsed_time(ev[2]) / 1e3,
@@ -501,6 +532,73 @@ def _map_ids(lib, pairs, count: int, r: DeviceRects, s: DeviceRects, cur, stream
     _wait(s.ids_ready, cur)
     _native.check(lib.pbsm_map_ids(pairs.data_ptr(), count, _ptr(r.ids), _ptr(s.ids), stream),
                   "pbsm_map_ids")
+
+
+_d2h_streams: dict = {}
+STAGED_MIN_PAIRS = 1 << 16
+
+
+def staged_pairs_to_host(pairs: torch.Tensor, count: int, r: DeviceRects,
+                         s: DeviceRects) -> np.ndarray:
+    """Row-index pairs of a join whose id columns are still crossing PCIe →
+    (r_id, s_id) pairs in page-locked host memory, group by group.
+
+    The last-landing id column (S's; R's for a self-join) arrives in row
+    chunks (to_device_pipelined).  pbsm_group_pairs splits the pairs by the
+    chunk they need; as each chunk lands, its group is mapped to ids
+    (pbsm_map_ids) and copied back on a device→host stream, so the copy back
+    overlaps the rest of the upload (PCIe is full duplex) and only the last
+    group's map and copy follow the last input byte.  The pair list is
+    unordered (engine.py:61-62); groups are laid out in chunk order."""
+    lib = _native.load()
+    device = pairs.device
+    stream = _raw_stream(device)
+    cur = torch.cuda.current_stream(device)
+    host = torch.empty((count, 2), dtype=torch.int64, pin_memory=True)
+    if count == 0:
+        return host.numpy()
+    chunks = s.id_chunks
+    if chunks is None or count < STAGED_MIN_PAIRS:
+        _map_ids(lib, pairs, count, r, s, cur, stream)
+        host.copy_(pairs[:count])
+        return host.numpy()
+    rows, evs = chunks
+    g_n = len(evs)
+    grouped = _buffer(device, "grouped", (count, 2), torch.int64, stream)
+    cnt = _buffer(device, "group_counts", (2 * g_n,), torch.int64, stream)
+    _native.check(lib.pbsm_group_pairs(pairs.data_ptr(), count, rows, g_n, int(s is r),
+                                       grouped.data_ptr(), cnt.data_ptr(), stream),
+                  "pbsm_group_pairs")
+    sizes = torch.empty(g_n, dtype=torch.int64, pin_memory=True)
+    sizes.copy_(cnt[:g_n], non_blocking=True)
+    done = torch.cuda.Event()
+    done.record(cur)
+    done.synchronize()  # (the ids are still landing: the host has time)
+    sizes = sizes.tolist()
+    if sum(sizes) != count:
+        raise KernelError(f"pbsm_group_pairs: groups hold {sum(sizes)} of {count} pairs")
+    d2h = _d2h_streams.get(device.index)
+    if d2h is None:
+        d2h = _d2h_streams[device.index] = torch.cuda.Stream(device)
+    if s is not r:
+        _wait(r.ids_ready, cur)  # R's ids land before S's chunks
+    off = 0
+    for g, n_g in enumerate(sizes):
+        cur.wait_event(evs[g])
+        if n_g == 0:
+            continue
+        part = grouped[off:off + n_g]
+        _native.check(lib.pbsm_map_ids(part.data_ptr(), n_g, _ptr(r.ids), _ptr(s.ids), stream),
+                      "pbsm_map_ids")
+        e = torch.cuda.Event()
+        e.record(cur)
+        d2h.wait_event(e)
+        with torch.cuda.stream(d2h):
+            host[off:off + n_g].copy_(part, non_blocking=True)
+        off += n_g
+    d2h.synchronize()
+    cur.wait_stream(d2h)  # later work on the main stream may reuse the buffers
+    return host.numpy()
 
 
 def _align(v: int, a: int = 256) -> int:

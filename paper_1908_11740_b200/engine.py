@@ -145,13 +145,19 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
     # start while the ids are still in flight
     rd, sd = dev.to_device_pipelined(r, s, device)
     kx, ky = cfg.layout.grid
-    res = dev.run_join(rd, sd, kx, ky, collect=collect_user or refine is not None, timing=True)
+    # (plain joins: the pairs come back as row indices and go home group by
+    # group as the id chunks land, dev.staged_pairs_to_host)
+    res = dev.run_join(rd, sd, kx, ky, collect=collect_user or refine is not None, timing=True,
+                       defer_map=collect_user and refine is None)
     count, pairs = res.count, res.pairs
     if refine is not None:
         count, pairs = refine(res.pairs)
     out = None
     if collect_user:
-        out = _to_host(pairs) if count else np.empty((0, 2), dtype=np.int64)
+        if res.rows_pending:
+            out = dev.staged_pairs_to_host(pairs, count, rd, sd)
+        else:
+            out = _to_host(pairs) if count else np.empty((0, 2), dtype=np.int64)
     t = res.times
     return JoinReport(
         result_count=int(count), pairs=out,

@@ -77,6 +77,52 @@ def test_late_ids_mapped_like_direct_ids():
     assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
 
 
+@pytest.mark.parametrize("groups", [1, 3, 8, 32])
+def test_staged_return_by_id_chunks(monkeypatch, groups):
+    """join() with host inputs sends the last id column in row chunks and
+    returns the pairs group by group (pbsm_group_pairs → pbsm_map_ids per
+    group → device-to-host copy as each chunk lands): the same pair set as the
+    oracle for arbitrary ids, for a join and a self-join, with any group
+    count, and the groups partition the pair list exactly."""
+    monkeypatch.setattr(dev, "ID_CHUNK_MIN", 1)
+    monkeypatch.setattr(dev, "ID_GROUPS", groups)
+    monkeypatch.setattr(dev, "STAGED_MIN_PAIRS", 1)
+    r, s, k = make_config(1, 0.3)
+    rng = np.random.default_rng(groups)
+    r = (rng.permutation(len(r[0])).astype(np.int64) * 7 + 3,) + tuple(r[1:])
+    s = (rng.permutation(len(s[0])).astype(np.int64) * 5 - 11,) + tuple(s[1:])
+    want = oracle.sorted_pairs(oracle.join(r, s, "2d", k)["pairs"])
+    for _ in range(2):  # the second join takes the speculative (cached-plan) path
+        rep = pb.join(pb.RectBatch(*r), pb.RectBatch(*s), _collect("2d", k))
+        assert rep.result_count == len(want)
+        assert np.array_equal(oracle.sorted_pairs(rep.pairs), want)
+    r5, _, k5 = make_config(5, 0.02)
+    b5 = pb.RectBatch(*r5)
+    want5 = oracle.sorted_pairs(oracle.join(r5, r5, "2d", k5)["pairs"])
+    rep5 = pb.join(b5, b5, _collect("2d", k5))
+    assert np.array_equal(oracle.sorted_pairs(rep5.pairs), want5)
+    # the grouping kernel alone: group-major, every pair exactly once
+    R, S = dev.to_device_pipelined(r, s)
+    res = dev.run_join(R, S, k, k, defer_map=True)
+    assert res.rows_pending
+    torch.cuda.synchronize()
+    lib = dev._native.load()
+    n = res.count
+    rows = -(-len(s[0]) // groups)
+    out = torch.empty((n, 2), dtype=torch.int64, device="cuda")
+    cnt = torch.empty(2 * groups, dtype=torch.int64, device="cuda")
+    assert lib.pbsm_group_pairs(res.pairs.data_ptr(), n, rows, groups, 0, out.data_ptr(),
+                                cnt.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    sizes = cnt[:groups].cpu().numpy()
+    assert sizes.sum() == n
+    key = np.minimum(got[:, 1] // rows, groups - 1)
+    assert np.all(np.diff(key) >= 0)
+    assert np.array_equal(np.bincount(key, minlength=groups), sizes)
+    assert np.array_equal(oracle.sorted_pairs(got), oracle.sorted_pairs(res.pairs.cpu().numpy()))
+
+
 def test_reference_synthetic_workloads(golden):
     """The reference's own generate_synthetic workloads: a uniform x clustered
     2D join (pairs from the reference) and the acceptance criterion-3 anchor
