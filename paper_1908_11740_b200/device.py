@@ -76,6 +76,7 @@ _copy_streams: dict = {}
 # staged return of host-input joins: the last id column crosses PCIe in
 # ID_GROUPS chunks when it has at least ID_CHUNK_MIN rows
 ID_GROUPS = int(os.environ.get("PBSM_ID_GROUPS", 8))
+STAGED = os.environ.get("PBSM_STAGED", "1") != "0"
 ID_CHUNK_MIN = 1 << 20
 
 
@@ -122,7 +123,10 @@ def to_device_pipelined(r, s, device="cuda"):
         for j, ((hb, db), cev) in enumerate(zip(zip(host, dev_cols), coord_ev)):
             chunks = None
             n = hb[0].shape[0]
-            if j == last and n >= ID_CHUNK_MIN:
+            # (a self-join's pairs need both ids from the one column: a group
+            # waits for the later of two chunks, so the tail is not shorter —
+            # measured on cfg5, not staged)
+            if j == last and last == 1 and n >= ID_CHUNK_MIN:
                 # the last id column in ID_GROUPS row chunks, an event each:
                 # the pairs whose ids are complete go back while the rest
                 # is still in flight (staged_pairs_to_host)

@@ -148,7 +148,7 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
     # (plain joins: the pairs come back as row indices and go home group by
     # group as the id chunks land, dev.staged_pairs_to_host)
     res = dev.run_join(rd, sd, kx, ky, collect=collect_user or refine is not None, timing=True,
-                       defer_map=collect_user and refine is None)
+                       defer_map=dev.STAGED and collect_user and refine is None)
     count, pairs = res.count, res.pairs
     if refine is not None:
         count, pairs = refine(res.pairs)

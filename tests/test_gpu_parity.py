@@ -99,8 +99,23 @@ def test_staged_return_by_id_chunks(monkeypatch, groups):
     r5, _, k5 = make_config(5, 0.02)
     b5 = pb.RectBatch(*r5)
     want5 = oracle.sorted_pairs(oracle.join(r5, r5, "2d", k5)["pairs"])
-    rep5 = pb.join(b5, b5, _collect("2d", k5))
+    rep5 = pb.join(b5, b5, _collect("2d", k5))  # (self-joins are not staged)
     assert np.array_equal(oracle.sorted_pairs(rep5.pairs), want5)
+    # the self-join grouping rule of the kernel (max of both rows)
+    R5, _ = dev.to_device_pipelined(r5, r5)
+    res5 = dev.run_join(R5, R5, k5, k5, defer_map=True)
+    torch.cuda.synchronize()
+    n5 = res5.count
+    rows5 = -(-len(r5[0]) // groups)
+    out5 = torch.empty((n5, 2), dtype=torch.int64, device="cuda")
+    cnt5 = torch.empty(2 * groups, dtype=torch.int64, device="cuda")
+    assert dev._native.load().pbsm_group_pairs(res5.pairs.data_ptr(), n5, rows5, groups, 1,
+                                               out5.data_ptr(), cnt5.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    got5 = out5.cpu().numpy()
+    key5 = np.minimum(got5.max(axis=1) // rows5, groups - 1)
+    assert np.all(np.diff(key5) >= 0)
+    assert np.array_equal(np.bincount(key5, minlength=groups), cnt5[:groups].cpu().numpy())
     # the grouping kernel alone: group-major, every pair exactly once
     R, S = dev.to_device_pipelined(r, s)
     res = dev.run_join(R, S, k, k, defer_map=True)
