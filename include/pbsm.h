@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 4
+#define PBSM_ABI_VERSION 5
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */

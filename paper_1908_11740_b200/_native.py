@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
