@@ -14,7 +14,7 @@ constexpr int kPlanThreads = 256;
 constexpr int kPlanPer = PBSM_PLAN_PER;               // tiles per thread
 constexpr int kPlanTile = kPlanThreads * kPlanPer;   // 1024 tiles per CTA
 constexpr int kNV = 12;                              // plan scan lanes (see tile_vals)
-constexpr int kNTot = kNV;                           // partials row stride
+constexpr int kNTot = kNV + 2;  // partials rows: kNV scan lanes + per-CTA max tile + pair bound
 
 constexpr int kJoinThreads = 256;
 #ifndef PBSM_CHUNK_B

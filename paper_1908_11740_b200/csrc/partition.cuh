@@ -565,8 +565,10 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
       m = max(m, shmax[w]);
       bs += shb[w];
     }
-    if (m) atomicMax((unsigned long long*)&hdr->max_tile, (unsigned long long)m);
-    if (bs) atomicAdd((unsigned long long*)&hdr->pair_bound, (unsigned long long)bs);
+    // into two extra partials rows, reduced by k_plan_partials (a header
+    // atomic per CTA queued ~4000 same-address atomics at one L2 slice)
+    partials[(u64)kNV * (gridDim.x + 1) + blockIdx.x] = m;
+    partials[(u64)(kNV + 1) * (gridDim.x + 1) + blockIdx.x] = bs;
   }
 }
 
@@ -582,7 +584,35 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
   __shared__ bool last;
   u64* row = partials + (u64)blockIdx.x * (nb + 1);
   u64 carry = 0;
-  for (u64 base = 0; base < nb; base += 4 * kPartThreads) {
+  if (blockIdx.x == kNV) {
+    // the extra CTA: max tile and pair bound over the plan CTAs' rows
+    const u64* rb = row + (nb + 1);
+    u64 m = 0, bs = 0;
+    for (u64 i = threadIdx.x; i < nb; i += kPartThreads) {
+      m = max(m, row[i]);
+      bs += rb[i];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+      bs += __shfl_down_sync(0xffffffffu, bs, o);
+    }
+    __shared__ u64 wm[kPartThreads / 32], wb[kPartThreads / 32];
+    if ((threadIdx.x & 31) == 0) {
+      wm[threadIdx.x >> 5] = m;
+      wb[threadIdx.x >> 5] = bs;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kPartThreads / 32; ++w) {
+        m = max(m, wm[w]);
+        bs += wb[w];
+      }
+      hdr->max_tile = (i64)m;
+      hdr->pair_bound = (i64)bs;
+    }
+  }
+  for (u64 base = 0; blockIdx.x < kNV && base < nb; base += 4 * kPartThreads) {
     const u64 i0 = base + 4 * (u64)threadIdx.x;
     u64 v[4];
 #pragma unroll
@@ -597,9 +627,9 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
     carry += tot;
   }
   if (threadIdx.x == 0) {
-    row[nb] = carry;
+    if (blockIdx.x < kNV) row[nb] = carry;
     __threadfence();
-    last = atomicAdd(&hdr->pad, 1u) == (u32)(kNV - 1);
+    last = atomicAdd(&hdr->pad, 1u) == (u32)kNV;  // kNV + 1 CTAs
   }
   __syncthreads();
   if (!last || threadIdx.x != 0) return;

@@ -126,7 +126,7 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
   const i64 nm = nested_max < 0 ? (i64)kNestedMax : (i64)nested_max;
   k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles, nm,
                                                               w.partials, w.hdr);
-  k_plan_partials<<<kNV, kPartThreads, 0, s>>>(w.partials, w.nblocks, w.hdr, w.cdesc[0],
+  k_plan_partials<<<kNV + 1, kPartThreads, 0, s>>>(w.partials, w.nblocks, w.hdr, w.cdesc[0],
                                                 w.cdesc[1], w.lpre);
   PlanOut P;
   P.cur_r = w.cur_r;
