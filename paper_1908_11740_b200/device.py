@@ -103,26 +103,40 @@ def to_device_pipelined(r, s, device="cuda"):
     if cs is None:
         cs = _copy_streams[device.index] = torch.cuda.Stream(device)
     batches = [r] if s is r else [r, s]
-    host = []
-    for b in batches:
-        cols = b if isinstance(b, (tuple, list)) else (b.ids, b.xl, b.xu, b.yl, b.yu)
-        host.append([_host_tensor(a, dt, True)
-                     for a, dt in zip(cols, (torch.int64,) + (torch.float64,) * 4)])
-    dev_cols = [[torch.empty(h.shape, dtype=h.dtype, device=device) for h in hb] for hb in host]
-    cs.wait_stream(torch.cuda.current_stream(device))  # the buffers' allocation stream
+    cols = [b if isinstance(b, (tuple, list)) else (b.ids, b.xl, b.xu, b.yl, b.yu)
+            for b in batches]
+    dts = (torch.int64,) + (torch.float64,) * 4
+    host = [[None] * 5 for _ in batches]
+    dev_cols = [[None] * 5 for _ in batches]
+    # every later allocation reuses only blocks whose last use is already
+    # enqueued on the current stream: one wait covers them all
+    cs.wait_stream(torch.cuda.current_stream(device))
+
+    def put(j, q, lo=None, hi=None):
+        # each column is prepared right before its copy, so the first bytes
+        # start crossing PCIe after one column's preparation, not ten
+        if host[j][q] is None:
+            host[j][q] = _host_tensor(cols[j][q], dts[q], True)
+            dev_cols[j][q] = torch.empty(host[j][q].shape, dtype=dts[q], device=device)
+        h, d = host[j][q], dev_cols[j][q]
+        if lo is None:
+            d.copy_(h, non_blocking=True)
+        else:
+            d[lo:hi].copy_(h[lo:hi], non_blocking=True)
+
     out = []
     with torch.cuda.stream(cs):
         coord_ev = []
-        for hb, db in zip(host, dev_cols):
+        for j in range(len(batches)):
             for q in range(1, 5):
-                db[q].copy_(hb[q], non_blocking=True)
+                put(j, q)
             ev = torch.cuda.Event()
             ev.record(cs)
             coord_ev.append(ev)
-        last = len(host) - 1
-        for j, ((hb, db), cev) in enumerate(zip(zip(host, dev_cols), coord_ev)):
+        last = len(batches) - 1
+        for j, cev in enumerate(coord_ev):
             chunks = None
-            n = hb[0].shape[0]
+            n = len(cols[j][0])
             # (a self-join's pairs need both ids from the one column: a group
             # waits for the later of two chunks, so the tail is not shorter —
             # measured on cfg5, not staged)
@@ -133,17 +147,18 @@ def to_device_pipelined(r, s, device="cuda"):
                 rows = -(-n // ID_GROUPS)
                 evs = []
                 for a in range(0, n, rows):
-                    db[0][a:a + rows].copy_(hb[0][a:a + rows], non_blocking=True)
+                    put(j, 0, a, a + rows)
                     e = torch.cuda.Event()
                     e.record(cs)
                     evs.append(e)
                 chunks = (rows, evs)
                 iev = evs[-1]
             else:
-                db[0].copy_(hb[0], non_blocking=True)
+                put(j, 0)
                 iev = torch.cuda.Event()
                 iev.record(cs)
-            out.append(DeviceRects(*db, coords_ready=cev, ids_ready=iev, id_chunks=chunks))
+            out.append(DeviceRects(*dev_cols[j], coords_ready=cev, ids_ready=iev,
+                                   id_chunks=chunks))
     return (out[0], out[0]) if s is r else (out[0], out[1])
 
 
