@@ -13,10 +13,14 @@ is split into N tile-row strips (one per rank, weighted by per-row work) and
 each rank joins its strip; the per-rank counts are combined by one
 all_gather (see paper_1908_11740_b200/parallel.py).
 
-``--impl reference`` times the reference's CPU path (the C restatement in
-oracle/, the only place this script executes oracle code besides the
-cpu_baseline leg) with all host threads, on a bounded sample of the same
-workload, and prints the same JSON line with "impl": "reference".
+``--impl reference`` times the reference's CPU path on the SAME full config
+every step (the C restatement in oracle/ with all host threads — the only
+place this script executes oracle code) and prints the same JSON line with
+"impl": "reference".  The GPU arm's ``cpu_baseline`` times the reference's
+own compiled ``sweepjoin.join`` (installed into baseline/_ref by
+oracle/build_ref.sh) on the full config.  Both arms gate their output on the
+reference's full-size truth (``parity``: count, A_R, A_S and the sha256 of the
+sorted pair list, tests/golden/full_truth.json); a mismatch exits 1.
 """
 
 from __future__ import annotations
@@ -52,8 +56,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-budget", type=float, default=20.0,
-                    help="seconds of CPU work for the cpu_baseline sample")
+    ap.add_argument("--cpu-variants", default="x1,xN",
+                    help="cpu_baseline runs of the reference join: axis x|a(daptive) + "
+                         "threads (N = physical cores), e.g. x1,xN,a1,aN")
+    ap.add_argument("--sub-configs", default="5,3,4",
+                    help="other BASELINE configs timed in the same run (N=1), '' for none")
+    ap.add_argument("--sub-steps", type=int, default=5)
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
     return ap.parse_args()
 
@@ -134,40 +143,50 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+# ---------------------------------------------------------------- parity
+TRUTH = ROOT / "tests" / "golden" / "full_truth.json"
+
+
+def truth_for(cfg: int):
+    """Full-size truth computed by the reference itself
+    (tests/golden/make_full_truth.py): count, A_R, A_S, sha256 of the sorted list."""
+    if not TRUTH.exists():
+        return None
+    return json.loads(TRUTH.read_text()).get(f"cfg{cfg}")
+
+
+def sorted_sha256_host(pairs: np.ndarray) -> str:
+    import hashlib
+
+    p = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+    if len(p):
+        p = p[np.lexsort((p[:, 1], p[:, 0]))]
+    return hashlib.sha256(np.ascontiguousarray(p, dtype="<i8").tobytes()).hexdigest()
+
+
+def sorted_sha256_device(pairs) -> str:
+    """sha256 of the lexicographically sorted pair list (sorted on the device,
+    hashed on the host) — the parity form of the unordered list."""
+    import hashlib
+
+    from paper_1908_11740_b200 import parallel
+
+    p = parallel.canonical_pairs(pairs.contiguous()).cpu().numpy()
+    return hashlib.sha256(np.ascontiguousarray(p, dtype="<i8").tobytes()).hexdigest()
+
+
+def parity_record(cfg: int, count: int, a_r: int, a_s: int, digest: str) -> dict:
+    t = truth_for(cfg)
+    if t is None:
+        return {"match": None, "sha256": digest, "note": "no committed truth"}
+    ok = (count == t["count"] and a_r == t["a_r"] and a_s == t["a_s"]
+          and digest == t["pairs_sha256"])
+    return {"match": bool(ok), "sha256": digest[:16], "count": count,
+            "truth": "tests/golden/full_truth.json (reference sweepjoin.join, threads=1, "
+                     "full size)"}
+
+
 # ---------------------------------------------------------------- CPU legs
-def cpu_sample(cfg: int, budget_s: float, threads: int, probe_f: float = 0.02):
-    """A bounded sample of the workload for the CPU: the rectangles overlapping
-    a bottom strip of the square (same density as the full job)."""
-    import oracle
-    from paper_1908_11740_b200.synth import make_config
-
-    r, s, k = make_config(cfg)
-    n_total = len(r[0]) + (0 if s is r else len(s[0]))
-
-    def strip(b, f):
-        m = b[3] < f  # yl below the strip top
-        return tuple(a[m] for a in b)
-
-    frac = 1.0
-    # probe on a small strip, then size the sample to the budget
-    rp = strip(r, probe_f)
-    sp = rp if s is r else strip(s, probe_f)
-    t = oracle.join(rp, sp, "2d", k, threads=threads)["total_time"]
-    per_frac = max(t / probe_f, 1e-6)
-    frac = min(1.0, budget_s / per_frac)
-    rs = strip(r, frac) if frac < 1.0 else r
-    ss = (rs if s is r else (strip(s, frac) if frac < 1.0 else s))
-    n = len(rs[0]) + (0 if s is r else len(ss[0]))
-    return rs, ss, k, frac, n, n_total
-
-
-def run_cpu(cfg, threads, rs, ss, k):
-    import oracle
-
-    res = oracle.join(rs, ss, "2d", k, threads=threads)
-    return res
-
-
 def physical_cores():
     try:
         import psutil
@@ -176,35 +195,131 @@ def physical_cores():
         return os.cpu_count()
 
 
+def import_reference():
+    """The unmodified reference package installed by oracle/build_ref.sh into
+    baseline/_ref (git-ignored; travels to the GPU box), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "sweepjoin").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import sweepjoin
+        if "compiled" not in sweepjoin.available_backends():
+            return None
+        return sweepjoin
+    except Exception:
+        return None
+
+
+def reference_cpu_baseline(cfg: int, variants: str) -> dict | None:
+    """BASELINE.md §2's CPU baseline: the reference's own compiled backend,
+    sweepjoin.join(R, S, JoinConfig(PartitionLayout("2d", K), axis_policy=...,
+    sink_mode="collect-pairs", threads=...)) on the FULL config, one run per
+    variant, best reported (JoinReport.total_time, inputs already in memory)."""
+    sj = import_reference()
+    if sj is None:
+        return None
+    from paper_1908_11740_b200.synth import make_config
+
+    r, s, k = make_config(cfg)
+    R = sj.RectBatch(*r)
+    S = R if s is r else sj.RectBatch(*s)
+    n = len(r[0]) + len(s[0])
+    cores = physical_cores()
+    runs = []
+    for v in variants.split(","):
+        v = v.strip()
+        if not v:
+            continue
+        axis = {"x": "x", "a": "adaptive"}[v[0]]
+        threads = cores if v[1:] == "N" else int(v[1:])
+        rep = sj.join(R, S, sj.JoinConfig(sj.PartitionLayout("2d", k), axis_policy=axis,
+                                          sink_mode="collect-pairs", threads=threads))
+        runs.append({"axis_policy": axis, "threads": threads, "total_time_s": rep.total_time,
+                     "pairs": int(rep.result_count)})
+        del rep
+    if not runs:
+        return None
+    best = min(runs, key=lambda x: x["total_time_s"])
+    return {"value": n / best["total_time_s"], "unit": UNIT, "cores": best["threads"],
+            "kind": "reference",
+            "sample": f"full cfg{cfg} ({n} rects, {best['pairs']} pairs): reference sweepjoin "
+                      f"{getattr(sj, '__version__', '0.1.0')} compiled backend (baseline/_ref, "
+                      f"oracle/build_ref.sh), best of {len(runs)} variant(s)",
+            "pairs_per_s": best["pairs"] / best["total_time_s"], "variants": runs,
+            "host_cores_physical": cores, "host_cpu": host_cpu()}
+
+
+def port_cpu_baseline(cfg: int) -> dict:
+    """Fallback when baseline/_ref is absent: the C port, full config, all threads."""
+    import oracle
+    from paper_1908_11740_b200.synth import make_config
+
+    r, s, k = make_config(cfg)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    res = oracle.join(r, s, "2d", k, threads=threads)
+    dt = time.perf_counter() - t0
+    n = len(r[0]) + len(s[0])
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"full cfg{cfg} ({n} rects, {res['count']} pairs), oracle/pbsm_oracle.c "
+                      f"(C restatement of the reference path), {threads} threads, 1 run",
+            "pairs_per_s": res["count"] / dt, "host_cpu": host_cpu()}
+
+
+def host_cpu() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def reference_arm(args):
+    """``--impl reference``: the reference CPU path on the arm's own config —
+    the FULL config every step (no sample), through the C restatement of the
+    reference's compiled path (oracle/pbsm_oracle.c, kind "port") with every
+    host thread (the reference's own join() takes 34 s per cfg2 step at its
+    best setting; bench.py's cpu_baseline leg times it)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    import oracle
+    from paper_1908_11740_b200.synth import make_config
+
     threads = os.cpu_count() or 1
-    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
-    rs, ss, k, frac, n, n_total = cpu_sample(args.config, budget, threads, probe_f=0.1)
+    r, s, k = make_config(args.config)
+    n = len(r[0]) + len(s[0])
+    res = None
     for _ in range(args.warmup):
-        run_cpu(args.config, threads, rs, ss, k)
-    t0 = time.perf_counter()
-    pairs = 0
+        res = oracle.join(r, s, "2d", k, threads=threads)
+    ts = []
     for _ in range(args.steps):
-        res = run_cpu(args.config, threads, rs, ss, k)
-        pairs = res["count"]
-    dt = (time.perf_counter() - t0) / args.steps
+        t0 = time.perf_counter()
+        res = oracle.join(r, s, "2d", k, threads=threads)
+        ts.append(time.perf_counter() - t0)
+    dt = sum(ts) / len(ts)
     value = n / dt
-    sample = (f"cfg{args.config} rectangles with yl < {frac:.4f} (a bottom strip, "
-              f"{n} of {n_total} rects, {pairs} pairs), oracle C port of the reference path, "
+    parity = parity_record(args.config, res["count"], res["a_r"], res["a_s"],
+                           sorted_sha256_host(res["pairs"]))
+    sample = (f"full cfg{args.config} every step ({n} rects, {res['count']} pairs), "
+              f"oracle/pbsm_oracle.c (C restatement of the reference's compiled path), "
               f"{threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "pairs_per_s": pairs / dt,
-        "config": {"workload": f"cfg{args.config}", "sample_fraction": frac},
+        "pairs_per_s": res["count"] / dt,
+        "config": {"workload": f"cfg{args.config}", "same_config": True, "n_r": len(r[0]),
+                   "n_s": len(s[0]), "grid": f"{k}x{k}", "sink_mode": "collect-pairs"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "host_cpu": host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "parity": parity,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -318,6 +433,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # cold latency: the first join of this shape in the process (synchronous
+    # plan-header read, first allocations of the tile lists and scratch)
+    barrier()
+    t0 = time.perf_counter()
+    res = step()
+    torch.cuda.synchronize()
+    cold_ms = (time.perf_counter() - t0) * 1e3
     clocks = ClockSampler(local).__enter__()  # running through warm-up: no start-up gap
     for _ in range(max(3, args.warmup)):
         res = step()
@@ -340,6 +462,21 @@ def main():
         step(probe)
     torch.cuda.synchronize()
     clocks.__exit__(None, None, None)
+    # parity gate: the last timed step's pair list, sorted on the device and
+    # hashed, against the reference's full-size truth
+    parity = None
+    if not args.no_parity:
+        allp = res.pairs
+        if world > 1:
+            ex = parallel.exchange_counts(res.count, res.header["a_r"], res.header["a_s"],
+                                          device=device)
+            allp = parallel.gather_pairs(res.pairs, ex, dst=0)
+        if rank == 0:
+            ex0 = parallel.exchange_counts(res.count, res.header["a_r"], res.header["a_s"],
+                                           device=device) if world == 1 else ex
+            parity = parity_record(args.config, ex0["pairs"], ex0["a_r"], ex0["a_s"],
+                                   sorted_sha256_device(allp))
+        del allp
     t = t_local
     local_pairs = res.count
     totals = parallel.combine_counts(res.count, res.header["a_r"], res.header["a_s"], t_local,
@@ -452,18 +589,23 @@ def main():
                "api": "paper_1908_11740_b200.parallel.strip_join(strip R, strip S, K, "
                       "row_lo, row_hi) per rank (host strip split outside the timed region)"}
 
+    subs = {}
+    if rank == 0 and world == 1 and args.sub_configs.strip():
+        del rd, sd
+        dev.release_buffers()
+        torch.cuda.empty_cache()
+        for c in [int(x) for x in args.sub_configs.split(",") if x.strip()]:
+            if c == args.config:
+                continue
+            subs[f"cfg{c}"] = time_sub_config(c, args.sub_steps, device, hbm, args.no_parity)
+            dev.release_buffers()
+            torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rs_, ss_, k_, frac, n_smp, n_tot = cpu_sample(args.config, args.cpu_budget, threads)
-        t0 = time.perf_counter()
-        cres = run_cpu(args.config, threads, rs_, ss_, k_)
-        ct = time.perf_counter() - t0
-        cpu = {"value": n_smp / ct, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"cfg{args.config} rectangles with yl < {frac:.4f} ({n_smp} of "
-                         f"{n_tot} rects, {cres['count']} pairs); oracle/pbsm_oracle.c "
-                         f"(C restatement of the reference path), {threads} threads, 1 run",
-               "pairs_per_s": cres["count"] / ct}
+        cpu = reference_cpu_baseline(args.config, args.cpu_variants)
+        if cpu is None:
+            cpu = port_cpu_baseline(args.config)
 
     if rank != 0:
         if world > 1:
@@ -497,13 +639,62 @@ def main():
         "phases_ms": {k_: v * 1e3 for k_, v in phases.items()},
         "clocks": clocks.summary(),
         "gpu_launches": launches,
+        "cold_first_join_ms": cold_ms,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity,
+        "sub_configs": subs,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    bad = [name for name, v in [(f"cfg{args.config}", {"parity": parity})] + list(subs.items())
+           if (v.get("parity") or {}).get("match") is False]
+    if bad:
+        print(f"PARITY MISMATCH against tests/golden/full_truth.json: {bad}", file=sys.stderr)
+        return 1
     return 0
+
+
+def time_sub_config(cfg: int, steps: int, device, hbm: float, no_parity: bool) -> dict:
+    """Another BASELINE config in the same run: device-resident inputs, 2
+    warm-up joins, ``steps`` timed joins (CUDA events), the step roofline and
+    the parity hash of the last join."""
+    import torch
+
+    from paper_1908_11740_b200 import device as dev
+    from paper_1908_11740_b200.synth import make_config
+
+    r, s, k = make_config(cfg)
+    n = len(r[0]) + len(s[0])
+    rd = dev.to_device(r, device)
+    sd = rd if s is r else dev.to_device(s, device)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = dev.run_join(rd, sd, k, k)
+    torch.cuda.synchronize()
+    cold = (time.perf_counter() - t0) * 1e3
+    for _ in range(2):
+        res = dev.run_join(rd, sd, k, k)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        res = dev.run_join(rd, sd, k, k)
+    e1.record()
+    torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) / 1e3 / steps
+    h = res.header
+    b_alg = 40 * n + 80 * (h["a_r"] + h["a_s"]) + 16 * res.count
+    out = {"ms_per_step": dt * 1e3, "value": n / dt, "unit": UNIT, "pairs": res.count,
+           "a_r": h["a_r"], "a_s": h["a_s"], "steps": steps, "cold_first_join_ms": cold,
+           "step_roofline": {"alg_bytes": b_alg, "achieved": b_alg / dt / 1e9, "peak": hbm,
+                             "frac": b_alg / dt / 1e9 / hbm, "unit": "GB/s"}}
+    if not no_parity:
+        out["parity"] = parity_record(cfg, res.count, h["a_r"], h["a_s"],
+                                      sorted_sha256_device(res.pairs))
+    del res, rd, sd
+    return out
 
 
 if __name__ == "__main__":

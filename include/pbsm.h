@@ -22,8 +22,11 @@
  *
  * Conventions
  *   - Every pointer is a DEVICE pointer owned by the caller (PyTorch in the
- *     shipped host code); the library never allocates device memory and keeps
- *     no global mutable state, so it is safe on any device/stream.
+ *     shipped host code); the library never allocates device memory.  Its
+ *     only global state is a per-device cache of two idempotent facts (SM
+ *     count, the shared-memory opt-in of the join kernels), kept in atomics,
+ *     so calls are safe from any host thread on any device/stream; joins in
+ *     flight at the same time need their own workspace, lists and scratch.
  *   - `stream` is a cudaStream_t passed as void*; every entry point only
  *     enqueues work on it (no implicit synchronisation) except
  *     pbsm_read_header, which is the one documented host sync point.
@@ -46,7 +49,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 5
+#define PBSM_ABI_VERSION 6
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -200,13 +203,17 @@ int64_t pbsm_refine_result_offset(int64_t n_cand);
 /* pbsm_join_emit without the host copy of the plan: the kernels read the
  * unit counts from the device header and the grids are the caller's upper
  * bounds (e.g. the previous join's counts), so the pipeline needs no host
- * sync between pbsm_plan and the emit.  Unordered placement only.  After the
- * final pbsm_read_header the caller checks header.chunks_nested <=
- * max_nested_chunks and chunks_sorted + n_items <= max_other_units (and the
- * list capacities it gave pbsm_scatter): otherwise some units were not run
- * and the join must be repeated with pbsm_join_emit. */
+ * sync between pbsm_plan and the emit.  Unordered placement only.
+ * r_capacity / s_capacity are the entries the tile-list buffers hold (the
+ * capacities given to pbsm_scatter): if the plan's lists are longer, no unit
+ * reads them and PBSM_ERR_SCATTER_OVERFLOW is set.  After the final
+ * pbsm_read_header the caller checks header.chunks_nested <=
+ * max_nested_chunks, chunks_sorted + n_items <= max_other_units and the
+ * error bits: otherwise some units were not run and the join must be
+ * repeated with pbsm_join_emit. */
 int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-                           const pbsm_entry* r_list, const pbsm_entry* s_list,
+                           const pbsm_entry* r_list, int64_t r_capacity,
+                           const pbsm_entry* s_list, int64_t s_capacity,
                            int64_t max_nested_chunks, int64_t max_other_units, void* scratch,
                            int64_t* pairs, int64_t capacity, void* stream);
 

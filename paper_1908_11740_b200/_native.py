@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
@@ -80,8 +80,8 @@ _SIGNATURES = {
                                   _P]),
     "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P, _P,
                                  _I64, _I32, _P]),
-    "pbsm_join_emit_bounded": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I64, _I64, _P,
-                                         _P, _I64, _P]),
+    "pbsm_join_emit_bounded": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _I64,
+                                         _I64, _I64, _P, _P, _I64, _P]),
     "pbsm_unpack_records": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "pbsm_map_ids": (C.c_int, [_P, _I64, _P, _P, _P]),
     "pbsm_group_pairs": (C.c_int, [_P, _I64, _I64, _I32, _I32, _P, _P, _P]),

@@ -16,15 +16,23 @@ inline bool grid_ok(int kx, int ky, int row_lo, int row_hi) {
          row_hi <= ky && (u64)kx * (u64)(row_hi - row_lo) < (1ull << 32) - 2;
 }
 
+// Per-device facts, cached per device ordinal (joins may run on several
+// devices, from several host threads: the caches are atomics, and a race only
+// repeats an idempotent query / attribute call).
+constexpr int kMaxDevices = 64;
+
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::atomic<int> n[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int v = n[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    n[dev].store(v, std::memory_order_relaxed);
   }
-  return n;
+  return v;
 }
 
 // grid of the count and bin passes (the same n → the same block ranges)
@@ -59,8 +67,12 @@ inline ScanLayout scan_layout(i64 n) {
 inline size_t join_scratch(i64 n_units) { return 256 + align_up(8 * (size_t)(n_units + 1), 256); }
 
 int set_smem_attrs() {
-  static bool done = false;
-  if (done) return 0;
+  // the dynamic shared-memory opt-in is a per-device function attribute
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & (kMaxDevices - 1));
+  if (done.load(std::memory_order_acquire) & bit) return 0;
   cudaError_t e;
   e = cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(JoinSmem));
@@ -68,15 +80,14 @@ int set_smem_attrs() {
   e = cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(JoinSmem));
   if (e != cudaSuccess) return (int)e;
-
-  done = true;
+  done.fetch_or(bit, std::memory_order_release);
   return 0;
 }
 
 int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, int row_hi,
                 const pbsm_entry* r_list, const pbsm_entry* s_list, const pbsm_header* plan,
                 void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s,
-                i64 max_nested = -1, i64 max_other = -1) {
+                i64 max_nested = -1, i64 max_other = -1, i64 cap_r = -1, i64 cap_s = -1) {
   int rc = set_smem_attrs();
   if (rc) return rc;
   const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
@@ -114,6 +125,8 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.total = (unsigned long long*)&w.hdr->pairs;
   A.ordered = ordered ? 1 : 0;
   A.bounded = bounded ? 1 : 0;
+  A.list_cap_r = cap_r;
+  A.list_cap_s = cap_s;
   A.g_cur_r = w.cur_r;
   A.g_end_r = w.cnt_r;
   A.g_cur_s = w.cur_s;

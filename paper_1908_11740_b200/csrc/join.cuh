@@ -20,6 +20,10 @@ struct JoinArgs {
   i64 n_units;
   pbsm_header* hdr;
   int bounded;     // grids are upper bounds: units past the plan's counts exit
+  // bounded mode: entries the tile-list buffers hold (the scatter stopped at
+  // them); a plan whose lists are longer makes every unit exit (no read past
+  // the buffers) with PBSM_ERR_SCATTER_OVERFLOW, and the caller re-runs
+  i64 list_cap_r, list_cap_s;
   // write guard folded into the nested join (g_tiles > 0): cursor ends vs
   // the counted ends, every tile (partition.py:229-233)
   const u32 *g_cur_r, *g_end_r, *g_cur_s, *g_end_s;
@@ -96,6 +100,15 @@ __device__ u64 lookback_thread(u64* status, i64 unit, u64 count, pbsm_header* hd
   }
   me.store(kFlagPre | (excl + count), cuda::memory_order_release);
   return excl;
+}
+
+// Bounded mode: the plan's tile lists are longer than the buffers the caller
+// sized from a previous plan — the scatter stopped at the capacity, so no unit
+// may stage entries: flag it (the caller re-runs with the exact plan) and exit.
+__device__ __forceinline__ bool lists_overflow(const JoinArgs& A) {
+  const bool over = A.hdr->list_r > A.list_cap_r || A.hdr->list_s > A.list_cap_s;
+  if (over && threadIdx.x == 0) atomicOr(&A.hdr->error, PBSM_ERR_SCATTER_OVERFLOW);
+  return over;
 }
 
 // Output range of one work unit, after its count pass.  Default: one atomic
@@ -749,6 +762,7 @@ __global__ void __launch_bounds__(kNT, PBSM_NESTED_MINB) k_join_nested(JoinArgs 
   const i64 n_plan = A.bounded ? (i64)A.hdr->chunks_nested : n_chunks;
   NestedChunk k = nested_desc(A, c);
   if (c >= n_plan) return;
+  if (A.bounded && lists_overflow(A)) return;
   nested_check(A, k);
   nested_stage(S.buf, A, k);
   cp_async_wait_all();
@@ -775,6 +789,7 @@ __global__ void __launch_bounds__(kJoinThreads, PBSM_JOIN_MINB) k_join(JoinArgs 
   // continue after the nested chunks (k_join_nested)
   const i64 cn = A.hdr->chunks_nested, cs = A.hdr->chunks_sorted;
   if (A.bounded && local >= cs + A.hdr->n_items) return;
+  if (A.bounded && lists_overflow(A)) return;
   const i64 unit = cn + local;
   if (local < cs) join_sorted<EMIT>(U.c, A, unit, local);
   else join_large<EMIT>(U.l, A, unit, local - cs);

@@ -53,6 +53,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "../../include/pbsm.h"
 
@@ -253,15 +254,18 @@ int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
 }
 
 int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-                           const pbsm_entry* r_list, const pbsm_entry* s_list,
+                           const pbsm_entry* r_list, int64_t r_capacity,
+                           const pbsm_entry* s_list, int64_t s_capacity,
                            int64_t max_nested_chunks, int64_t max_other_units, void* scratch,
                            int64_t* pairs, int64_t capacity, void* stream) {
   if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || capacity < 0 ||
       (capacity > 0 && !pairs) || max_nested_chunks < 0 || max_other_units < 0 ||
-      max_nested_chunks > 0x7fffffff || max_other_units > 0x7fffffff)
+      max_nested_chunks > 0x7fffffff || max_other_units > 0x7fffffff || r_capacity < 0 ||
+      s_capacity < 0)
     return PBSM_E_ARG;
   return launch_join(true, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, nullptr, scratch,
-                     pairs, capacity, as_stream(stream), max_nested_chunks, max_other_units);
+                     pairs, capacity, as_stream(stream), max_nested_chunks, max_other_units,
+                     r_capacity, s_capacity);
 }
 
 int64_t pbsm_refine_scratch_bytes(int64_t n_cand) {

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -177,20 +178,28 @@ class DeviceJoinResult:
     rows_pending: bool = False            # pairs still hold row indices (defer_map)
 
 
+# Host-side state of the driver, every cache keyed by (device, stream) so
+# joins enqueued concurrently — from several threads, on several streams or
+# devices — never share a workspace, a list buffer, a side stream or a pinned
+# header; the dicts themselves are guarded by _state_lock.
+_state_lock = threading.RLock()
 _ws_cache: dict = {}
 
 
-def _workspace(lib, device, kx, ky, row_lo, row_hi) -> torch.Tensor:
-    key = (str(device), kx, ky, row_lo, row_hi)
-    ws = _ws_cache.get(key)
-    if ws is None:
+def _workspace(lib, device, kx, ky, row_lo, row_hi, stream: int = 0) -> torch.Tensor:
+    key = (str(device), stream)
+    grid = (kx, ky, row_lo, row_hi)
+    with _state_lock:
+        ent = _ws_cache.get(key)
+        if ent is not None and ent[0] == grid:
+            return ent[1]
         nbytes = lib.pbsm_workspace_bytes(kx, ky, row_lo, row_hi)
         if nbytes < 0:
             raise KernelError(f"invalid grid {kx}x{ky} rows [{row_lo},{row_hi})")
+        _ws_cache.pop(key, None)  # one grid workspace per (device, stream)
         ws = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
-        _ws_cache.clear()  # keep one grid workspace alive at a time
-        _ws_cache[key] = ws
-    return ws
+        _ws_cache[key] = (grid, ws)
+        return ws
 
 
 # Internal buffers of a join (the two tile lists, the join scratch), kept per
@@ -213,25 +222,27 @@ def _buffer(device, name: str, shape: tuple, dtype, stream: int) -> torch.Tensor
     for d in shape:
         n *= d
     # per (device, stream): joins enqueued on different streams never share
-    key = (device, stream, name)
-    ent = _buf_cache.get(key)
-    if ent is not None and ent[1] == shape and ent[0].dtype == dtype:
-        return ent[2]  # the same view as last time
-    buf = ent[0] if ent is not None else None
-    if buf is None or buf.dtype != dtype or buf.numel() < n:
-        _buf_cache.pop(key, None)
-        del buf, ent  # the old block is free before the larger one is requested
-        buf = torch.empty(max(n, 1), dtype=dtype, device=device)
-    view = buf[:n].view(shape)
-    _buf_cache[key] = (buf, shape, view)
-    return view
+    key = (str(device), stream, name)
+    with _state_lock:
+        ent = _buf_cache.get(key)
+        if ent is not None and ent[1] == shape and ent[0].dtype == dtype:
+            return ent[2]  # the same view as last time
+        buf = ent[0] if ent is not None else None
+        if buf is None or buf.dtype != dtype or buf.numel() < n:
+            _buf_cache.pop(key, None)
+            del buf, ent  # the old block is free before the larger one is requested
+            buf = torch.empty(max(n, 1), dtype=dtype, device=device)
+        view = buf[:n].view(shape)
+        _buf_cache[key] = (buf, shape, view)
+        return view
 
 
 def release_buffers() -> None:
     """Drop the cached tile lists, join scratch and grid workspaces."""
-    _buf_cache.clear()
-    _ws_cache.clear()
-    _plan_cache.clear()
+    with _state_lock:
+        _buf_cache.clear()
+        _ws_cache.clear()
+        _plan_cache.clear()
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -249,16 +260,18 @@ _VALIDATION = (
 _VALIDATION_BITS = sum(b for b, _ in _VALIDATION)
 
 
-_hdr_pinned: dict = {}
+_hdr_local = threading.local()
 
 
 def _read_header(lib, ws, stream, allow=0) -> _native.Header:
     # into page-locked memory: a pageable destination would go through the
-    # driver's staging copy on this (synchronising) path
-    buf = _hdr_pinned.get("buf")
+    # driver's staging copy on this (synchronising) path.  One buffer per
+    # host thread: the read is synchronous, so a thread never has two in
+    # flight, and concurrent joins on other threads have their own.
+    buf = getattr(_hdr_local, "buf", None)
     if buf is None:
-        buf = _hdr_pinned["buf"] = torch.empty(C.sizeof(_native.Header), dtype=torch.uint8,
-                                               pin_memory=True)
+        buf = _hdr_local.buf = torch.empty(C.sizeof(_native.Header), dtype=torch.uint8,
+                                           pin_memory=True)
     dst = C.cast(C.c_void_p(buf.data_ptr()), C.POINTER(_native.Header))
     _native.check(lib.pbsm_read_header(ws.data_ptr(), dst, stream), "pbsm_read_header")
     h = _native.Header.from_buffer_copy(C.string_at(buf.data_ptr(), C.sizeof(_native.Header)))
@@ -331,11 +344,15 @@ DUAL = os.environ.get("PBSM_DUAL", "1") != "0"
 _side_streams: dict = {}
 
 
-def _side_stream(device):
-    st = _side_streams.get(device.index)
-    if st is None:
-        st = _side_streams[device.index] = torch.cuda.Stream(device)
-    return st
+def _side_stream(device, stream: int):
+    """The side stream paired with the launching stream ``stream`` (S's count
+    and scatter run there, concurrent with R's)."""
+    key = (device.index, stream)
+    with _state_lock:
+        st = _side_streams.get(key)
+        if st is None:
+            st = _side_streams[key] = torch.cuda.Stream(device)
+        return st
 
 SPECULATE = os.environ.get("PBSM_SPECULATE", "1") != "0"
 
@@ -366,7 +383,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         empty = torch.empty((0, 2), dtype=torch.int64, device=device) if collect else None
         return DeviceJoinResult(0, empty)
     stream = _raw_stream(device)
-    ws = _workspace(lib, device, kx, ky, row_lo, row_hi)
+    ws = _workspace(lib, device, kx, ky, row_lo, row_hi, stream)
     wsp = ws.data_ptr()
     grid = (kx, ky, row_lo, row_hi)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
@@ -390,7 +407,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     main_st = side_st = None
     if DUAL:
         main_st = torch.cuda.current_stream(device)
-        side_st = _side_stream(device)
+        side_st = _side_stream(device, stream)
     dual = DUAL and cur is None
     if dual:
         fork = torch.cuda.Event()
@@ -411,7 +428,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         counts = tuple(v.clone() for v in _tile_count_views(ws, kx, ky, kx * (row_hi - row_lo)))
     _native.check(lib.pbsm_plan(wsp, *grid, nested_max, stream), "pbsm_plan")
     mark("plan")
-    key = (str(device), kx, ky, row_lo, row_hi, len(r), len(s), s is r, nested_max, bin_bytes)
+    key = (str(device), stream, kx, ky, row_lo, row_hi, len(r), len(s), s is r, nested_max,
+           bin_bytes)
     guess = _plan_cache.get(key) if (SPECULATE and collect and not ordered
                                      and not keep_counts) else None
     if guess is None:
@@ -467,8 +485,9 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                           torch.uint8, stream)
         pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
         mark("alloc")
-        _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), sl.data_ptr(), cn,
-                                                 rest, scratch.data_ptr(), pairs.data_ptr(), cap,
+        _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), list_r,
+                                                 sl.data_ptr(), list_s, cn, rest,
+                                                 scratch.data_ptr(), pairs.data_ptr(), cap,
                                                  stream), "pbsm_join_emit_bounded")
         mark("join")
         h2 = _read_header(lib, ws, stream,
@@ -478,7 +497,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                 or h2.chunks_sorted + h2.n_items > rest or h2.pairs > cap
                 or h2.error & (_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW)):
             # another input behind the same shape: redo it with the exact plan
-            _plan_cache.pop(key, None)
+            with _state_lock:
+                _plan_cache.pop(key, None)
             return run_join(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
                             timing=timing, keep_counts=keep_counts, probe=probe,
                             ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes,
@@ -526,8 +546,10 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         if late and not defer_map:
             _map_ids(lib, pairs, count, r, s, cur, stream)
         if not ordered and not keep_counts:
-            _plan_cache.clear()  # one shape at a time
-            _plan_cache[key] = {"list_r": h.list_r, "list_s": h.list_s, "pairs": cap,
+            with _state_lock:
+                for k_ in [k_ for k_ in _plan_cache if k_[:2] == key[:2]]:
+                    del _plan_cache[k_]  # one shape per (device, stream)
+                _plan_cache[key] = {"list_r": h.list_r, "list_s": h.list_s, "pairs": cap,
                                 "nested": h.chunks_nested,
                                 "other": h.chunks_sorted + h.n_items}
     if ev:
@@ -618,6 +640,41 @@ def staged_pairs_to_host(pairs: torch.Tensor, count: int, r: DeviceRects,
     d2h.synchronize()
     cur.wait_stream(d2h)  # later work on the main stream may reuse the buffers
     return host.numpy()
+
+
+def tile_counts(r, s, kx: int, ky: int, row_lo: int = 0, row_hi: int | None = None,
+                device=None):
+    """Per-tile assignment counts of both inputs (count_pass,
+    partition.py:136-148; count_tiles, _kernels.pyx:34-58) as int64 numpy
+    arrays of kx × (row_hi-row_lo) tiles, row-major.  ``r``/``s`` are host
+    batches (RectBatch / 5-tuples) or DeviceRects; one pbsm_init + pbsm_count
+    per input on the device, nothing else of the join runs.  Validation
+    errors raise the reference's ValueError."""
+    lib = _native.load()
+    if row_hi is None:
+        row_hi = ky
+    if not isinstance(r, DeviceRects):
+        dv = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        same = s is None or s is r
+        r = to_device(r, dv)
+        s = r if same else (s if isinstance(s, DeviceRects) else to_device(s, dv))
+    elif s is None:
+        s = r
+    device = r.device
+    stream = _raw_stream(device)
+    ws = _workspace(lib, device, kx, ky, row_lo, row_hi, stream)
+    wsp = ws.data_ptr()
+    grid = (kx, ky, row_lo, row_hi)
+    _native.check(lib.pbsm_init(wsp, *grid, stream), "pbsm_init")
+    for side, b in ((0, r), (1, s)):
+        if len(b):
+            _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
+                                         side, wsp, *grid, stream), "pbsm_count")
+    T = kx * (row_hi - row_lo)
+    cr, cs = (v.to(torch.int64) for v in _tile_count_views(ws, kx, ky, T))
+    out = (cr.cpu().numpy(), cs.cpu().numpy())
+    _read_header(lib, ws, stream)  # validation bits → ValueError
+    return out
 
 
 def _align(v: int, a: int = 256) -> int:

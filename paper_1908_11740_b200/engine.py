@@ -47,6 +47,27 @@ class JoinConfig:
     devices: int = 1
 
 
+class _Lazy:
+    """Dataclass field whose value may be given as a zero-argument callable,
+    evaluated once on first read (the field stays an ordinary constructor
+    argument: ``JoinReport(..., task_sizes=array)`` works as in the reference)."""
+
+    def __set_name__(self, owner, name):
+        self.slot = "_lazy_" + name
+
+    def __get__(self, obj, objtype=None):
+        if obj is None:
+            return None
+        v = obj.__dict__.get(self.slot)
+        if callable(v):
+            v = v()
+            obj.__dict__[self.slot] = v
+        return v
+
+    def __set__(self, obj, value):
+        obj.__dict__[self.slot] = None if isinstance(value, _Lazy) else value
+
+
 @dataclass
 class JoinReport:
     """Result size, optional ``(n, 2)`` int64 (r_id, s_id) pairs and phase times.
@@ -54,7 +75,9 @@ class JoinReport:
     Field meanings follow engine.py:55-70.  ``sort_time`` is 0.0: the
     per-tile sort is fused into the join kernels and accounted in
     ``join_time``.  ``task_sizes`` (|R_T|+|S_T| of every join tile, largest
-    first) is materialised from the device on first access.
+    first, build_task_queue engine.py:84-100) is computed on first read by a
+    device count pass over the HOST inputs the report references — a report
+    holds no device memory.
     """
 
     result_count: int
@@ -63,14 +86,7 @@ class JoinReport:
     sort_time: float
     join_time: float
     total_time: float
-    _task_sizes: object = field(default=None, repr=False)
-
-    @property
-    def task_sizes(self) -> np.ndarray | None:
-        ts = self._task_sizes
-        if callable(ts):
-            ts = self._task_sizes = ts()
-        return ts
+    task_sizes: np.ndarray | None = field(default=_Lazy(), repr=False)
 
 
 def _resolve_policy(cfg: JoinConfig) -> str:
@@ -115,14 +131,15 @@ def _require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _task_sizes_fn(r: dev.DeviceRects, s: dev.DeviceRects, kx: int, ky: int):
+def _task_sizes_fn(r: RectBatch, s: RectBatch, kx: int, ky: int):
+    """Lazy task_sizes: the report keeps references to the caller's host
+    batches only; on first read their coordinates go back to the device for
+    one count pass (pbsm_count) and the join tiles' sizes come back sorted."""
     def compute():
-        # recount per tile (cheap) so the report does not pin the workspace
-        res = dev.run_join(r, s, kx, ky, collect=False, keep_counts=True)
-        cr, cs = (c.to(torch.int64) for c in res.tile_counts)
+        cr, cs = dev.tile_counts(r, s, kx, ky)
         both = (cr > 0) & (cs > 0)
         sizes = (cr + cs)[both]
-        return torch.sort(sizes, descending=True).values.cpu().numpy()
+        return -np.sort(-sizes, kind="stable")
     return compute
 
 
@@ -139,7 +156,7 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
     if len(r) == 0 or len(s) == 0:
         return JoinReport(0, np.empty((0, 2), dtype=np.int64) if collect_user else None,
                           0.0, 0.0, 0.0, time.perf_counter() - t0,
-                          np.empty(0, dtype=np.int64))
+                          task_sizes=np.empty(0, dtype=np.int64))
     device = _require_cuda()
     # column copies on a side stream, coordinates first: the count passes
     # start while the ids are still in flight
@@ -164,7 +181,7 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
         partition_time=t.get("partition", 0.0), sort_time=0.0,
         join_time=t.get("join", 0.0),
         total_time=time.perf_counter() - t0,
-        _task_sizes=_task_sizes_fn(rd, sd, kx, ky))
+        task_sizes=_task_sizes_fn(r, s, kx, ky))
 
 
 def join(r: RectBatch | Sequence[Rect], s: RectBatch | Sequence[Rect],

@@ -116,7 +116,8 @@ class ConfigSpec:
     self_join: bool
     gen_r: object
     gen_s: object
-    # exact full-scale values measured by the survey (SURVEY.md §8 header table)
+    # exact full-scale values (SURVEY.md §8 header table), re-derived by the
+    # reference itself in tests/golden/full_truth.json (make_full_truth.py)
     a_r: int
     a_s: int
     pairs: int

@@ -297,39 +297,52 @@ def test_repeat_runs_identical_sets():
         assert np.array_equal(oracle.sorted_pairs(pb.join(R, S, _collect("2d", k)).pairs), a)
 
 
+def _truth(cfg):
+    import json
+    from pathlib import Path
+
+    p = Path(__file__).resolve().parent / "golden" / "full_truth.json"
+    return json.loads(p.read_text())[f"cfg{cfg}"]
+
+
+def _sorted_sha256(pairs):
+    import hashlib
+
+    from paper_1908_11740_b200 import parallel
+
+    p = parallel.canonical_pairs(pairs.contiguous()).cpu().numpy()
+    return hashlib.sha256(np.ascontiguousarray(p, dtype="<i8").tobytes()).hexdigest()
+
+
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", [2, 5])
-def test_full_size_bit_exact_vs_oracle(cfg):
-    spec = CONFIGS[cfg]
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_full_size_matches_reference_truth(cfg):
+    """Every BASELINE config at FULL size against the reference's own outputs
+    (tests/golden/full_truth.json, made by make_full_truth.py running
+    sweepjoin.join on the same arrays): result_count, A_R, A_S and the sha256
+    of the lexicographically sorted (r_id, s_id) list — identical sorted
+    lists, not survey constants."""
+    t = _truth(cfg)
     r, s, k = make_config(cfg)
     rd = dev.to_device(r)
     sd = rd if s is r else dev.to_device(s)
     res = dev.run_join(rd, sd, k, k, collect=True)
-    assert res.count == spec.pairs
-    assert res.header["a_r"] == spec.a_r and res.header["a_s"] == spec.a_s
-    ref = oracle.join(r, s, "2d", k, threads=8)
-    assert ref["count"] == spec.pairs
-    got = oracle.sorted_pairs(res.pairs.cpu().numpy())
-    assert np.array_equal(got, oracle.sorted_pairs(ref["pairs"]))
+    assert (res.count, res.header["a_r"], res.header["a_s"]) == (t["count"], t["a_r"], t["a_s"])
+    assert _sorted_sha256(res.pairs) == t["pairs_sha256"]
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [3, 4])
-def test_full_size_counts_and_properties(cfg):
-    """cfg3/cfg4 at full size: exact P, A_R, A_S (survey, measured with the
-    reference) and size-independent properties of the pair list."""
-    spec = CONFIGS[cfg]
+def test_full_size_pair_properties(cfg):
+    """cfg3/cfg4 at full size, size-independent properties of the pair list:
+    no duplicates, and every emitted pair intersects (closed intervals)."""
     r, s, k = make_config(cfg)
     rd, sd = dev.to_device(r), dev.to_device(s)
     res = dev.run_join(rd, sd, k, k, collect=True)
-    assert res.header["a_r"] == spec.a_r and res.header["a_s"] == spec.a_s
-    assert res.count == spec.pairs
     p = res.pairs
-    # no duplicates: sort the packed (r, s) keys on the device
     key = p[:, 0] * (len(s[0]) + 1) + p[:, 1]
     ks = torch.sort(key).values
     assert bool((ks[1:] != ks[:-1]).all())
-    # every emitted pair intersects (closed intervals)
     rx = [torch.as_tensor(a, device=p.device) for a in r[1:]]
     sx = [torch.as_tensor(a, device=p.device) for a in s[1:]]
     i, j = p[:, 0], p[:, 1]
@@ -543,6 +556,35 @@ def test_speculative_plan_reuse(golden):
     assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
 
 
+@pytest.mark.slow
+def test_speculative_plan_reuse_full_size_overrun():
+    """Full-size version of the mismatch: a cfg2-shaped join
+    caches its plan sizes; the next input of the same shape has tile lists
+    ~2x longer, so the speculative lists are far too short.  The bounded join
+    must not read past them (it used to stage entries tens of MB beyond the
+    buffers): every unit exits on PBSM_ERR_SCATTER_OVERFLOW, the join is re-run
+    exactly, and the result equals the non-speculative join."""
+    r, s, k = make_config(2)
+    R, S = dev.to_device(r), dev.to_device(s)
+    dev._plan_cache.clear()
+    base = dev.run_join(R, S, k, k)
+    assert base.count == _truth(2)["count"]
+    # same n, same grid; S widened 6x in x and y: many more multi-tile entries
+    s2 = list(s)
+    for lo, hi in ((1, 2), (3, 4)):
+        c = (s[lo] + s[hi]) / 2
+        h = (s[hi] - s[lo]) * 3.0 + 2e-4
+        s2[lo] = np.clip(c - h, 0.0, 1.0)
+        s2[hi] = np.clip(c + h, 0.0, 1.0)
+    S2 = dev.to_device(tuple(s2))
+    got = dev.run_join(R, S2, k, k)          # speculative guess far too small
+    assert got.header["list_s"] > 1.5 * base.header["list_s"]
+    dev._plan_cache.clear()
+    exact = dev.run_join(R, S2, k, k)        # synchronous plan
+    assert got.count == exact.count
+    assert _sorted_sha256(got.pairs) == _sorted_sha256(exact.pairs)
+
+
 def test_write_guard_detects_a_skipped_scatter(golden):
     """The partition write guard (partition.py:229-233): if a scatter did not
     run, the cursor ends disagree with the counted ends and the join reports
@@ -619,3 +661,64 @@ def test_cli_join_matches_reference(tmp_path, golden, capsys):
     text = capsys.readouterr().out
     assert f"result_count={int(g['cfg1_count'])}" in text
     assert np.array_equal(oracle.sorted_pairs(np.load(out)), g["cfg1_pairs"])
+
+
+def test_task_sizes_and_report_holds_no_device_memory(golden):
+    """JoinReport.task_sizes = build_task_queue's join-task sizes, largest
+    first (engine.py:84-100): |R_T|+|S_T| of every tile with both inputs
+    non-empty, from the reference's own per-tile counts (cfg1 fixture).  The
+    report references no device tensor (the lazy field holds host batches)."""
+    import gc
+
+    g = golden["configs"]
+    r, s, k = make_config(1, float(g["cfg1_scale"]))
+    rep = pb.join(pb.RectBatch(*r), pb.RectBatch(*s), _collect("2d", k))
+    pending = rep.__dict__["_lazy_task_sizes"]
+    cells = [c.cell_contents for c in (pending.__closure__ or ())]
+    assert not any(isinstance(c, torch.Tensor) or isinstance(c, dev.DeviceRects) for c in cells)
+    cr, cs = g["cfg1_counts_r"].astype(np.int64), g["cfg1_counts_s"].astype(np.int64)
+    both = (cr > 0) & (cs > 0)
+    want = -np.sort(-(cr + cs)[both])
+    assert np.array_equal(rep.task_sizes, want)
+    assert pb.JoinReport(1, None, 0.0, 0.0, 0.0, 0.0, task_sizes=want).task_sizes is want
+    assert pb.JoinReport(1, None, 0.0, 0.0, 0.0, 0.0).task_sizes is None
+    gc.collect()
+
+
+def test_concurrent_joins_on_two_threads_and_streams(golden):
+    """Two joins at once from two host threads, each on its own CUDA stream
+    (different shapes and data): both bit-exact.  The driver keys every
+    cache — workspace, lists, side stream, plan sizes — by (device, stream)
+    and reads the header through a per-thread pinned buffer."""
+    import threading
+
+    g = golden["configs"]
+    jobs = []
+    for cfg in (2, 5):
+        r, s, k = make_config(cfg, float(g[f"cfg{cfg}_scale"]))
+        R = dev.to_device(r)
+        S = R if s is r else dev.to_device(s)
+        jobs.append((cfg, R, S, k))
+    torch.cuda.synchronize()
+    out, errs = {}, []
+
+    def work(cfg, R, S, k):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(4):  # sync plan, then speculative joins
+                    res = dev.run_join(R, S, k, k)
+                    out[cfg] = (res.count, res.pairs.cpu().numpy())
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+
+    th = [threading.Thread(target=work, args=j) for j in jobs]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for cfg in (2, 5):
+        count, pairs = out[cfg]
+        assert count == int(g[f"cfg{cfg}_count"])
+        assert np.array_equal(oracle.sorted_pairs(pairs), g[f"cfg{cfg}_pairs"])

@@ -108,3 +108,26 @@ def test_oracle_synthetic_join_and_criterion3(golden):
     s = synthetic(1_000_000, 1e-3, 1e-3, seed=302)
     res = oracle.join(r, s, "1d", 100, threads=8, collect=False)
     assert res["count"] == int(g["crit3_count"]) == 3_989_612
+
+
+def test_full_truth_is_consistent_with_fixtures():
+    """tests/golden/full_truth.json (the reference's full-size outputs, made by
+    make_full_truth.py) agrees with the committed cfg1 pair fixture (hash of
+    the same sorted list) and with the survey's A_R / A_S / P constants."""
+    import hashlib
+    import json
+    from pathlib import Path
+
+    import numpy as np
+
+    from paper_1908_11740_b200.synth import CONFIGS
+
+    truth = json.loads((Path(__file__).resolve().parent / "golden" / "full_truth.json")
+                       .read_text())
+    g = np.load(Path(__file__).resolve().parent / "golden" / "configs.npz")
+    p = np.ascontiguousarray(g["cfg1_pairs"], dtype="<i8")
+    assert hashlib.sha256(p.tobytes()).hexdigest() == truth["cfg1"]["pairs_sha256"]
+    for name, t in truth.items():
+        spec = CONFIGS[int(name[3:])]
+        assert (t["count"], t["a_r"], t["a_s"]) == (spec.pairs, spec.a_r, spec.a_s), name
+        assert (t["n_r"], t["n_s"], t["k"]) == (spec.n_r, spec.n_s, spec.k), name
