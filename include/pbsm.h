@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 6
+#define PBSM_ABI_VERSION 7
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -246,6 +246,95 @@ int pbsm_unpack_records(const void* records, int64_t n, int64_t* ids, double* xl
 int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const double* py,
                 const double* qx, const double* qy, const int64_t* p_ids, const int64_t* q_ids,
                 double eps_sq, void* scratch, int64_t* out, void* stream);
+
+/* ======================================================================
+ * Unit pipeline (the default path of run_join where it applies): the grid's
+ * tile rows are cut into UNITS — a tile row × a column range, sized from a
+ * per-cell record histogram so every unit holds a few thousand records —
+ * and each unit is partitioned AND joined by one CTA while its tile lists
+ * are hot in L2:
+ *
+ *   pbsm_unit_count   count_tiles at cell granularity (cell = tile row ×
+ *                     column group) + RectBatch.validate
+ *   pbsm_unit_map     the unit map (cells merged greedily into units,
+ *                     largest first)
+ *   pbsm_unit_bin     every rectangle copied into each unit it overlaps
+ *                     (32-byte MBR + its row index), unit-major
+ *   pbsm_unit_join    per unit: count_tiles (shared-memory counters),
+ *                     compute_segment_offsets, write_tiles into the unit's
+ *                     slice of the scratch lists, then the nested mini-joins
+ *                     of its small tiles (count -> reserve -> emit); tiles of
+ *                     more than LMAX entries are queued and joined after all
+ *                     units by the large-tile kernel (sort_segment by x-lower
+ *                     + forward scan, _kernels.pyx:188-293)
+ *
+ * Same results as the tile-list pipeline above; one host sync (the header
+ * after pbsm_unit_map) on the first join of a shape, none after that when
+ * the caller passes the previous sizes as capacities (overflows are flagged
+ * in pbsm_uheader.error and the join is repeated).
+ * ====================================================================== */
+typedef struct pbsm_uheader {
+  int64_t a_r;            /* Σ tiles covered by R rectangles (= A_R)           */
+  int64_t a_s;            /* same for S                                         */
+  int64_t bin_r;          /* R records binned into live units                   */
+  int64_t bin_s;
+  int64_t n_units;        /* units with both inputs non-empty                   */
+  int64_t max_unit;       /* largest unit (records, R + S)                      */
+  int64_t cells;          /* cells of the histogram (rows × column groups)      */
+  int64_t group_cols;     /* columns per column group                           */
+  uint32_t error;         /* PBSM_ERR_* bits of plan and bin                    */
+  uint32_t pad;
+  /* join phase (reset by every pbsm_unit_join) */
+  int64_t scratch_used;   /* 32-byte scratch slots the units allocated          */
+  uint64_t def_packed;    /* deferred tiles << 40 | their work items            */
+  int64_t work;           /* large-tile kernel's item ticket                    */
+  int64_t pairs;          /* result_count                                       */
+  uint32_t jerror;        /* PBSM_ERR_* bits of the join                        */
+  uint32_t pad2;
+  int64_t nq;             /* chunks heavy units queued for the chunk kernel      */
+  int64_t qticket;        /* its ticket                                         */
+  int64_t n_def_tiles;    /* tiles deferred to the large-tile kernel           */
+  int64_t n_def_items;    /* their work items                                  */
+} pbsm_uheader;
+
+/* Whether the unit pipeline supports this grid strip (unit width and cell
+ * count limits); 1 = yes, 0 = use the tile-list pipeline. */
+int32_t pbsm_unit_supported(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi);
+int64_t pbsm_unit_workspace_bytes(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi);
+/* bytes of a bin buffer holding `records` binned records (36 B each) */
+int64_t pbsm_unit_bin_bytes(int64_t records);
+/* bytes of the join scratch holding `slots` 32-byte list slots (+ row
+ * indices and the deferred-tile table) */
+int64_t pbsm_unit_scratch_bytes(int64_t slots);
+/* Per join: pbsm_unit_init, pbsm_unit_count for R (side 0) and S (side 1) —
+ * on two streams if wanted, both after init — then pbsm_unit_map (target =
+ * records per unit, <= 0: default; n_r / n_s = the counted inputs' sizes).
+ * pbsm_unit_bin of an input must get the same n as its pbsm_unit_count (the
+ * bin places each record from the count pass' per-block tallies).
+ * Validation errors land in the header like pbsm_count's. */
+int pbsm_unit_init(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                   void* stream);
+int pbsm_unit_count(const double* xl, const double* xu, const double* yl, const double* yu,
+                    int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
+                    int32_t row_hi, void* stream);
+int pbsm_unit_map(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                  int64_t n_r, int64_t n_s, int64_t target, void* stream);
+/* the unit-major copy of one input (side 0 = R, 1 = S) into `bin`
+ * (`capacity` records; PBSM_ERR_SCATTER_OVERFLOW past it). */
+int pbsm_unit_bin(const double* xl, const double* xu, const double* yl, const double* yu,
+                  int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
+                  int32_t row_hi, void* bin, int64_t capacity, void* stream);
+/* per-unit partition + nested mini-joins, then the deferred large tiles.
+ * r_ids / s_ids may be NULL (pairs then hold row indices, pbsm_map_ids).
+ * pairs: (capacity, 2) int64; the count lands in pbsm_uheader.pairs. */
+int pbsm_unit_join(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                   const void* bin_r, int64_t bin_r_capacity, const void* bin_s,
+                   int64_t bin_s_capacity, const int64_t* r_ids, const int64_t* s_ids,
+                   void* scratch, int64_t scratch_slots, int64_t max_units, int64_t* pairs,
+                   int64_t capacity, void* stream);
+/* Copy the unit header to *out (page-locked: a tiny kernel stores it) and
+ * synchronise the stream. */
+int pbsm_read_uheader(void* ws, pbsm_uheader* out, void* stream);
 
 /* ABI version / build identification */
 int32_t pbsm_abi_version(void);

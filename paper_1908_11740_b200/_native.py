@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
@@ -31,6 +31,9 @@ EXPORTED = (
     "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit", "pbsm_join_emit_bounded",
     "pbsm_unpack_records", "pbsm_refine_scratch_bytes", "pbsm_refine_result_offset",
     "pbsm_refine", "pbsm_map_ids", "pbsm_group_pairs",
+    "pbsm_unit_supported", "pbsm_unit_workspace_bytes", "pbsm_unit_bin_bytes",
+    "pbsm_unit_scratch_bytes", "pbsm_unit_init", "pbsm_unit_count", "pbsm_unit_map",
+    "pbsm_unit_bin", "pbsm_unit_join", "pbsm_read_uheader",
 )
 
 
@@ -53,6 +56,26 @@ class Header(C.Structure):
     def as_dict(self) -> dict:
         d = {name: getattr(self, name) for name, _ in self._fields_ if name != "pad"}
         d["n_units"] = self.n_units
+        return d
+
+
+class UHeader(C.Structure):
+    """Mirror of ``pbsm_uheader`` (the unit pipeline's header)."""
+
+    _fields_ = [
+        ("a_r", C.c_int64), ("a_s", C.c_int64), ("bin_r", C.c_int64), ("bin_s", C.c_int64),
+        ("n_units", C.c_int64), ("max_unit", C.c_int64), ("cells", C.c_int64),
+        ("group_cols", C.c_int64), ("error", C.c_uint32), ("pad", C.c_uint32),
+        ("scratch_used", C.c_int64), ("def_packed", C.c_uint64), ("work", C.c_int64),
+        ("pairs", C.c_int64), ("jerror", C.c_uint32), ("pad2", C.c_uint32),
+        ("nq", C.c_int64), ("qticket", C.c_int64),
+        ("n_def_tiles", C.c_int64), ("n_def_items", C.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {name: getattr(self, name) for name, _ in self._fields_
+             if name not in ("pad", "pad2", "def_packed", "work", "qticket")}
+        d["pipeline"] = "units"
         return d
 
 
@@ -88,6 +111,18 @@ _SIGNATURES = {
     "pbsm_refine_scratch_bytes": (_I64, [_I64]),
     "pbsm_refine_result_offset": (_I64, [_I64]),
     "pbsm_refine": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),
+    "pbsm_unit_supported": (_I32, [_I32, _I32, _I32, _I32]),
+    "pbsm_unit_workspace_bytes": (_I64, [_I32, _I32, _I32, _I32]),
+    "pbsm_unit_bin_bytes": (_I64, [_I64]),
+    "pbsm_unit_scratch_bytes": (_I64, [_I64]),
+    "pbsm_unit_init": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
+    "pbsm_unit_count": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P]),
+    "pbsm_unit_map": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _I64, _I64, _P]),
+    "pbsm_unit_bin": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P, _I64,
+                                _P]),
+    "pbsm_unit_join": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P,
+                                 _I64, _I64, _P, _I64, _P]),
+    "pbsm_read_uheader": (C.c_int, [_P, C.POINTER(UHeader), _P]),
 }
 
 

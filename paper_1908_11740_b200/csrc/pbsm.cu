@@ -49,6 +49,7 @@
 
 #include <cuda/atomic>
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -71,6 +72,7 @@ namespace {
 #include "join.cuh"
 #include "extras.cuh"
 #include "host.cuh"
+#include "units.cuh"
 
 }  // namespace
 
@@ -343,6 +345,181 @@ int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const dou
   k_refine_compact<<<blocks, 256, 0, s>>>((const i64*)cand, n_cand, flag, base,
                                           (const i64*)p_ids, (const i64*)q_ids, (i64*)out);
   return launch_status();
+}
+
+// ------------------------------------------------------------ unit pipeline
+static int unit_nb() { return std::min(num_sms(), 1024); }
+
+// the dynamic shared-memory opt-in of the 128-KB kernels, per device
+static int unit_smem_attrs() {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & (kMaxDevices - 1));
+  if (done.load(std::memory_order_acquire) & bit) return 0;
+  cudaError_t e = cudaFuncSetAttribute(k_ucount, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       4 * kUnitMaxCells);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_ubin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             4 * kUnitMaxCells);
+  if (e != cudaSuccess) return (int)e;
+  done.fetch_or(bit, std::memory_order_release);
+  return 0;
+}
+
+int32_t pbsm_unit_supported(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi) {
+  UGeo g;
+  return unit_geometry(kx, ky, row_lo, row_hi, g) ? 1 : 0;
+}
+
+int64_t pbsm_unit_workspace_bytes(int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi) {
+  UGeo g;
+  if (!unit_geometry(kx, ky, row_lo, row_hi, g)) return PBSM_E_ARG;
+  return (int64_t)ulayout(g, unit_nb()).total;
+}
+
+int64_t pbsm_unit_bin_bytes(int64_t records) {
+  if (records < 0) return PBSM_E_ARG;
+  return (int64_t)(align_up(32 * (size_t)records, 256) + align_up(4 * (size_t)records, 256));
+}
+
+int64_t pbsm_unit_scratch_bytes(int64_t slots) {
+  if (slots < 0 || slots > 0xffffffffll) return PBSM_E_ARG;
+  return (int64_t)uscratch_bytes((u64)slots);
+}
+
+int pbsm_unit_init(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                   void* stream) {
+  UGeo g;
+  if (!ws || !unit_geometry(kx, ky, row_lo, row_hi, g)) return PBSM_E_ARG;
+  const ULayout L = ulayout(g, unit_nb());
+  UWs w = ubind(ws, L);
+  const u64 nz = (L.cls - L.cont[0]) / 4;  // cont[2]
+  const unsigned blocks = (unsigned)std::max<i64>(1, std::min<i64>((i64)(nz + 255) / 256,
+                                                                    (i64)num_sms() * 2));
+  k_uinit<<<blocks, 256, 0, as_stream(stream)>>>(w.hdr, w.cont[0], nz, w.cls, w.bx, kx, w.by,
+                                                 ky);
+  return launch_status();
+}
+
+int pbsm_unit_count(const double* xl, const double* xu, const double* yl, const double* yu,
+                    int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
+                    int32_t row_hi, void* stream) {
+  UGeo g;
+  if (!ws || !unit_geometry(kx, ky, row_lo, row_hi, g) || n < 0 || (side != 0 && side != 1) ||
+      n > 0xffffffffll)
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!xl || !xu || !yl || !yu) return PBSM_E_ARG;
+  int rc = unit_smem_attrs();
+  if (rc) return rc;
+  UWs w = ubind(ws, ulayout(g, unit_nb()));
+  const int nb = upart_blocks(n, w.nb);
+  k_ucount<<<nb, kUCountThreads, 4 * (size_t)g.cells, as_stream(stream)>>>(
+      xl, xu, yl, yu, n, g, w.bx, w.by, w.bhist[side], w.cont[side], w.hdr, side);
+  return launch_status();
+}
+
+int pbsm_unit_map(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi, int64_t n_r,
+                  int64_t n_s, int64_t target, void* stream) {
+  UGeo g;
+  if (!ws || !unit_geometry(kx, ky, row_lo, row_hi, g) || n_r < 0 || n_s < 0) return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  UWs w = ubind(ws, ulayout(g, unit_nb()));
+  const int nbR = n_r ? upart_blocks(n_r, w.nb) : 0, nbS = n_s ? upart_blocks(n_s, w.nb) : 0;
+  const u32 t = target > 0 ? (u32)std::min<int64_t>(target, 1 << 30) : (u32)PBSM_UNIT_TARGET;
+  k_ucell_sum<<<(2 * g.cells + 255) / 256, 256, 0, s>>>(w.bhist[0], nbR, w.bhist[1], nbS,
+                                                         g.cells, w.first[0], w.first[1]);
+  const unsigned rb = (unsigned)((g.rows + kMapRowsPerBlock - 1) / kMapRowsPerBlock);
+  k_umap_rows<<<rb, 256, 0, s>>>(g, w.first[0], w.cont[0], w.first[1], w.cont[1], t,
+                                 w.cell_unit, w.unR, w.unS, w.row_live, w.row_nR, w.row_nS,
+                                 w.cls, w.hdr);
+  k_umap_scan<<<1, kUMapThreads, 0, s>>>(g, w.row_live, w.row_nR, w.row_nS, w.cls, w.hdr);
+  k_umap_write<<<rb, 256, 0, s>>>(g, w.cell_unit, w.unR, w.unS, w.row_live, w.row_nR, w.row_nS,
+                                  w.cls, w.units, w.order, w.bhist[0], nbR, w.bhist[1], nbS,
+                                  w.blk_base[0], w.blk_base[1], w.ccur[0], w.ccur[1]);
+  return launch_status();
+}
+
+int pbsm_unit_bin(const double* xl, const double* xu, const double* yl, const double* yu,
+                  int64_t n, int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
+                  int32_t row_hi, void* bin, int64_t capacity, void* stream) {
+  UGeo g;
+  if (!ws || !unit_geometry(kx, ky, row_lo, row_hi, g) || n < 0 || (side != 0 && side != 1) ||
+      capacity < 0 || n > 0xffffffffll)
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!xl || !xu || !yl || !yu || (!bin && capacity > 0)) return PBSM_E_ARG;
+  int rc = unit_smem_attrs();
+  if (rc) return rc;
+  UWs w = ubind(ws, ulayout(g, unit_nb()));
+  URec* b = reinterpret_cast<URec*>(bin);
+  u32* bidx = reinterpret_cast<u32*>(reinterpret_cast<char*>(bin) +
+                                     align_up(32 * (size_t)capacity, 256));
+  const int nb = upart_blocks(n, w.nb);  // the same blocks as pbsm_unit_count
+  k_ubin<<<nb, kUCountThreads, 4 * (size_t)g.cells, as_stream(stream)>>>(
+      xl, xu, yl, yu, n, g, w.bx, w.by, w.cell_unit, w.blk_base[side], w.ccur[side], b, bidx,
+      capacity, w.hdr);
+  return launch_status();
+}
+
+int pbsm_unit_join(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                   const void* bin_r, int64_t bin_r_capacity, const void* bin_s,
+                   int64_t bin_s_capacity, const int64_t* r_ids, const int64_t* s_ids,
+                   void* scratch, int64_t scratch_slots, int64_t max_units, int64_t* pairs,
+                   int64_t capacity, void* stream) {
+  UGeo g;
+  if (!ws || !unit_geometry(kx, ky, row_lo, row_hi, g) || bin_r_capacity < 0 ||
+      bin_s_capacity < 0 || scratch_slots < 0 || scratch_slots > 0xffffffffll || capacity < 0 ||
+      (capacity > 0 && !pairs) || !scratch)
+    return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  UWs w = ubind(ws, ulayout(g, unit_nb()));
+  // reset the join-phase block of the header (scratch_used .. pad2)
+  cudaMemsetAsync(&w.hdr->scratch_used, 0,
+                  offsetof(pbsm_uheader, n_def_tiles) - offsetof(pbsm_uheader, scratch_used), s);
+  UJoinArgs A;
+  A.g = g;
+  A.bx = w.bx;
+  A.by = w.by;
+  A.units = w.units;
+  A.order = w.order;
+  A.hdr = w.hdr;
+  const void* bins[2] = {bin_r, bin_s};
+  const i64 caps[2] = {bin_r_capacity, bin_s_capacity};
+  for (int q = 0; q < 2; ++q) {
+    A.bin[q] = reinterpret_cast<const URec*>(bins[q]);
+    A.bidx[q] = reinterpret_cast<const u32*>(reinterpret_cast<const char*>(bins[q]) +
+                                             align_up(32 * (size_t)caps[q], 256));
+    A.bcap[q] = caps[q];
+  }
+  A.ids[0] = (const i64*)r_ids;
+  A.ids[1] = (const i64*)s_ids;
+  A.sc = uscratch_bind(scratch, (u64)scratch_slots);
+  A.pairs = (i64*)pairs;
+  A.capacity = capacity;
+  const i64 grid = max_units > 0 ? std::min<i64>(max_units, g.cells) : g.cells;
+  k_ujoin<<<(unsigned)std::max<i64>(1, grid), kUJoinThreads, 0, s>>>(A);
+  k_uchunks<<<(unsigned)(num_sms() * 6), kUJoinThreads, 0, s>>>(A);
+  k_ularge<<<(unsigned)(num_sms() * 2), kJoinThreads, sizeof(ULargeSmem), s>>>(A);
+  return launch_status();
+}
+
+int pbsm_read_uheader(void* ws, pbsm_uheader* out, void* stream) {
+  if (!ws || !out) return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, out);
+  if (e == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer == (void*)out) {
+    k_publish_uheader<<<1, 32, 0, s>>>(reinterpret_cast<const pbsm_uheader*>(ws), out);
+    e = cudaGetLastError();
+  } else {
+    cudaGetLastError();
+    e = cudaMemcpyAsync(out, ws, sizeof(pbsm_uheader), cudaMemcpyDeviceToHost, s);
+  }
+  if (e != cudaSuccess) return (int)e;
+  e = cudaStreamSynchronize(s);
+  return e == cudaSuccess ? 0 : (int)e;
 }
 
 }  // extern "C"

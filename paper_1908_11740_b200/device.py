@@ -355,14 +355,200 @@ def _side_stream(device, stream: int):
         return st
 
 SPECULATE = os.environ.get("PBSM_SPECULATE", "1") != "0"
+# The unit pipeline (units.cuh) is parity-green but measured slower than the
+# tile-list pipeline on every BASELINE config: opt-in only.
+UNITS = os.environ.get("PBSM_UNITS", "0") == "1"
+UNIT_TARGET = int(os.environ.get("PBSM_UNIT_TARGET", "-1"))
+_uhdr_local = threading.local()
+
+
+def _read_uheader(lib, ws, stream, allow=0) -> _native.UHeader:
+    buf = getattr(_uhdr_local, "buf", None)
+    if buf is None:
+        buf = _uhdr_local.buf = torch.empty(C.sizeof(_native.UHeader), dtype=torch.uint8,
+                                            pin_memory=True)
+    dst = C.cast(C.c_void_p(buf.data_ptr()), C.POINTER(_native.UHeader))
+    _native.check(lib.pbsm_read_uheader(ws.data_ptr(), dst, stream), "pbsm_read_uheader")
+    h = _native.UHeader.from_buffer_copy(C.string_at(buf.data_ptr(), C.sizeof(_native.UHeader)))
+    for bit, msg in _VALIDATION:
+        if h.error & bit:
+            raise ValueError(msg)
+    bad = (h.error | h.jerror) & ~allow & ~_VALIDATION_BITS
+    if bad:
+        raise KernelError(f"device guard: {_native.describe_error(bad)} "
+                          "(partition write overflow check, partition.py:229-233)")
+    return h
+
+
+def _uworkspace(lib, device, kx, ky, row_lo, row_hi, stream: int) -> torch.Tensor:
+    key = (str(device), stream, "units")
+    grid = (kx, ky, row_lo, row_hi)
+    with _state_lock:
+        ent = _ws_cache.get(key)
+        if ent is not None and ent[0] == grid:
+            return ent[1]
+        nbytes = lib.pbsm_unit_workspace_bytes(kx, ky, row_lo, row_hi)
+        if nbytes < 0:
+            raise KernelError(f"unit pipeline: unsupported grid {kx}x{ky} [{row_lo},{row_hi})")
+        _ws_cache.pop(key, None)
+        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
+        _ws_cache[key] = (grid, ws)
+        return ws
+
+
+def _unit_slots(a_total: int, n_units: int) -> int:
+    """Scratch slots for the unit join: every join-tile entry (<= A_R + A_S),
+    a tile record per two small tiles (<= A/4), chunk descriptors and the
+    per-unit 128-byte alignment."""
+    return int(a_total + a_total // 4 + a_total // 512 + 16 * n_units + 1024)
+
+
+def _run_units(lib, r: DeviceRects, s: DeviceRects, kx: int, ky: int, row_lo: int, row_hi: int,
+               *, collect: bool, timing: bool, mark, defer_map: bool,
+               exact: bool = False) -> DeviceJoinResult:
+    """The unit pipeline (include/pbsm.h): init → cell counts (R and S on two
+    streams) → unit map → [header read, first join of a shape only] → unit
+    bins (two streams) → per-unit partition + nested mini-joins → deferred
+    large tiles → header read.  Repeated shapes allocate from the previous
+    join's sizes; any overflow (flagged on the device, nothing written out of
+    bounds) re-runs the join with the exact sizes."""
+    device = r.device
+    stream = _raw_stream(device)
+    ws = _uworkspace(lib, device, kx, ky, row_lo, row_hi, stream)
+    wsp = ws.data_ptr()
+    grid = (kx, ky, row_lo, row_hi)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
+    if ev:
+        ev[0].record()
+    mark("start")
+    _native.check(lib.pbsm_unit_init(wsp, *grid, stream), "pbsm_unit_init")
+    mark("init")
+    cur = (torch.cuda.current_stream(device)
+           if r.coords_ready is not None or s.coords_ready is not None else None)
+    late = r.ids_ready is not None and s.ids_ready is not None
+    main_st = torch.cuda.current_stream(device)
+    side_st = _side_stream(device, stream)
+    dual = DUAL and cur is None
+
+    def two(fn):
+        """fn(side, batch, stream) for R then S; S on the side stream when dual."""
+        if dual:
+            fork = torch.cuda.Event()
+            fork.record(main_st)
+            side_st.wait_event(fork)
+        for side, b in ((0, r), (1, s)):
+            _wait(b.coords_ready, cur)
+            fn(side, b, side_st.cuda_stream if (dual and side == 1) else stream)
+        if dual:
+            j = torch.cuda.Event()
+            j.record(side_st)
+            main_st.wait_event(j)
+
+    two(lambda side, b, st: _native.check(
+        lib.pbsm_unit_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b), side, wsp,
+                            *grid, st), "pbsm_unit_count"))
+    mark("count")
+    _native.check(lib.pbsm_unit_map(wsp, *grid, len(r), len(s), UNIT_TARGET, stream),
+                  "pbsm_unit_map")
+    mark("map")
+    key = (str(device), stream, "units", *grid, len(r), len(s), s is r)
+    guess = None if (exact or not SPECULATE) else _plan_cache.get(key)
+    if guess is None:
+        h = _read_uheader(lib, ws, stream)
+        mark("header")
+        a_tot = int(h.a_r + h.a_s)
+        sizes = {"bin_r": max(int(h.bin_r), 1), "bin_s": max(int(h.bin_s), 1),
+                 "slots": _unit_slots(a_tot, int(h.n_units)),
+                 "units": max(int(h.n_units), 1),
+                 "pairs": int(min(2 * a_tot + (1 << 20), 1 << 34))}
+    else:
+        sizes = guess
+    if sizes["slots"] > 0xffffffff:
+        raise KernelError("unit pipeline: more than 2^32 list slots; use pipeline='tiles'")
+    bins = []
+
+    def do_bin(side, b, st):
+        cap = sizes["bin_r" if side == 0 else "bin_s"]
+        buf = _buffer(device, f"ubin{side}", (int(lib.pbsm_unit_bin_bytes(cap)),), torch.uint8,
+                      stream)
+        bins.append((buf, cap))
+        _native.check(lib.pbsm_unit_bin(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
+                                        side, wsp, *grid, buf.data_ptr(), cap, st),
+                      "pbsm_unit_bin")
+
+    two(do_bin)
+    mark("bin")
+    if ev:
+        ev[1].record()
+    scratch = _buffer(device, "uscratch", (int(lib.pbsm_unit_scratch_bytes(sizes["slots"])),),
+                      torch.uint8, stream)
+    ids_r = None if late else _ptr(r.ids)
+    ids_s = None if late else _ptr(s.ids)
+    (b0, c0), (b1, c1) = bins
+    cap = sizes["pairs"] if collect else 0  # count-only: every chunk counts, none writes
+    while True:
+        pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
+        _native.check(lib.pbsm_unit_join(wsp, *grid, b0.data_ptr(), c0, b1.data_ptr(), c1,
+                                         ids_r, ids_s, scratch.data_ptr(), sizes["slots"],
+                                         sizes["units"], pairs.data_ptr(), cap, stream),
+                      "pbsm_unit_join")
+        mark("join")
+        h2 = _read_uheader(lib, ws, stream, allow=_native.ERR_PAIR_OVERFLOW
+                           | _native.ERR_SCATTER_OVERFLOW | _native.ERR_INTERNAL)
+        mark("header2")
+        structural = (h2.bin_r > c0 or h2.bin_s > c1 or h2.scratch_used > sizes["slots"]
+                      or h2.n_units > sizes["units"]
+                      or (h2.error | h2.jerror) & (_native.ERR_SCATTER_OVERFLOW
+                                                   | _native.ERR_INTERNAL))
+        if structural:
+            if guess is None and not exact:
+                raise KernelError(f"unit pipeline: sizes from the plan were exceeded "
+                                  f"({_native.describe_error(h2.error | h2.jerror)})")
+            # another input behind the same shape: redo it with the exact plan
+            with _state_lock:
+                _plan_cache.pop(key, None)
+            return _run_units(lib, r, s, kx, ky, row_lo, row_hi, collect=collect,
+                              timing=timing, mark=mark, defer_map=defer_map, exact=True)
+        if h2.pairs <= cap or not collect:
+            break
+        cap = int(h2.pairs)  # the pair estimate was short: join again into an exact buffer
+    count = int(h2.pairs)
+    pairs = pairs[:count]
+    with _state_lock:
+        for k_ in [k_ for k_ in _plan_cache if k_[:3] == key[:3]]:
+            del _plan_cache[k_]
+        _plan_cache[key] = {"bin_r": max(int(h2.bin_r), 1), "bin_s": max(int(h2.bin_s), 1),
+                            "slots": int(h2.scratch_used) + 1024,
+                            "units": max(int(h2.n_units), 1),
+                            "pairs": max(cap, 1) if collect else sizes["pairs"]}
+    if late and not defer_map:
+        _map_ids(lib, pairs, count, r, s, cur, stream)
+    if ev:
+        ev[2].record()
+        ev[2].synchronize()
+    hd = h2.as_dict()
+    hd["list_r"], hd["list_s"] = int(h2.a_r), int(h2.a_s)
+    res = DeviceJoinResult(count, pairs if collect else None, header=hd,
+                           rows_pending=late and defer_map and collect)
+    if ev:
+        res.times = {"partition": ev[0].elapsed_time(ev[1]) / 1e3,
+                     "join": ev[1].elapsed_time(ev[2]) / 1e3,
+                     "total": ev[0].elapsed_time(ev[2]) / 1e3}
+    return res
 
 
 def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool = True,
              row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
              keep_counts: bool = False, probe: PhaseProbe | None = None,
              ordered: bool = False, nested_max: int = -1,
-             bin_bytes: int | None = None, defer_map: bool = False) -> DeviceJoinResult:
+             bin_bytes: int | None = None, defer_map: bool = False,
+             pipeline: str | None = None) -> DeviceJoinResult:
     """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
+
+    Two device pipelines compute the same pair set: the tile-list pipeline
+    below (the default) and the unit pipeline (``pipeline="units"`` or
+    PBSM_UNITS=1, where ``pbsm_unit_supported``; not for the ordered emit,
+    forced cost-model thresholds, the binned scatter or ``keep_counts``).
 
     ``probe`` (optional) gets an event after each library call, named after
     the phase that call ran: init, count, plan, header, scatter, join, header2.
@@ -382,6 +568,11 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     if len(r) == 0 or len(s) == 0:
         empty = torch.empty((0, 2), dtype=torch.int64, device=device) if collect else None
         return DeviceJoinResult(0, empty)
+    if (pipeline == "units" or (pipeline is None and UNITS)) and not ordered and not keep_counts \
+            and nested_max == -1 and bin_bytes is None \
+            and lib.pbsm_unit_supported(kx, ky, row_lo, row_hi) == 1:
+        return _run_units(lib, r, s, kx, ky, row_lo, row_hi, collect=collect, timing=timing,
+                          mark=mark, defer_map=defer_map)
     stream = _raw_stream(device)
     ws = _workspace(lib, device, kx, ky, row_lo, row_hi, stream)
     wsp = ws.data_ptr()
@@ -502,7 +693,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
             return run_join(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
                             timing=timing, keep_counts=keep_counts, probe=probe,
                             ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes,
-                            defer_map=defer_map)
+                            defer_map=defer_map, pipeline="tiles")
         count = int(h2.pairs)
         if late and not defer_map:
             _map_ids(lib, pairs, count, r, s, cur, stream)

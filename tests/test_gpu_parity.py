@@ -209,7 +209,7 @@ def test_scatter_entries_are_the_join_tile_assignments(golden):
     stream = torch.cuda.current_stream().cuda_stream
     for side, b, own, other, n in ((0, r, cr, cs, res.header["list_r"]),
                                    (1, s, cs, cr, res.header["list_s"])):
-        lst = dev._buf_cache[(torch.device("cuda", 0), stream, f"list{side}")][2][:n].cpu().numpy()
+        lst = dev._buf_cache[(str(torch.device("cuda", 0)), stream, f"list{side}")][2][:n].cpu().numpy()
         key = lst[:, 0].view(np.uint64)
         got_ids, got_lab = lst[:, 4], (key >> np.uint64(62)).astype(np.int64)
         assert sorted(zip(got_ids.tolist(), got_lab.tolist())) == \
