@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 7
+#define PBSM_ABI_VERSION 8
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -88,7 +88,9 @@ typedef struct pbsm_entry {
  *            than sorting when the tile is this small);
  *   sorted — |R_T|+|S_T| <= LMAX otherwise: per-tile segmented sort by x-lower
  *            + forward-scan sweep (Alg. 1) in shared memory;
- *   large  — |R_T|+|S_T| > LMAX: split over several CTAs.
+ *   large  — |R_T|+|S_T| > LMAX: each side sorted by x-lower in global
+ *            memory (sort_segment), then the forward-scan sweep (Alg. 1)
+ *            with one leader per thread, 256 leaders per work item.
  * Work units of one join launch: [nested chunks | sorted chunks | large items]. */
 typedef struct pbsm_header {
   int64_t a_r;            /* Σ per-tile R counts = PartitionedDataset.total_assigned */
@@ -106,6 +108,11 @@ typedef struct pbsm_header {
   int64_t pairs;          /* result_count, valid after pbsm_join_count/emit         */
   int64_t pair_bound;     /* Σ |R_T|·|S_T| over join tiles (>= pairs)               */
   int64_t max_tile;       /* largest |R_T|+|S_T| over join tiles                   */
+  int64_t large_r;        /* R entries in large tiles                               */
+  int64_t large_s;        /* same for S                                             */
+  int64_t sweep_min;      /* large tiles with |R_T|*|S_T| above this are sorted +   */
+                          /* swept, the others brute-forced (pbsm_plan)             */
+  int64_t max_huge;       /* largest side of a sorted + swept tile                  */
   uint32_t error;         /* PBSM_ERR_* bits                                        */
   uint32_t pad;
 } pbsm_header;
@@ -129,9 +136,11 @@ int pbsm_count(const double* xl, const double* xu, const double* yl,
  * join-task plan (build_task_queue, engine.py:84-100): CSR offsets, the join
  * tiles of each mini-join strategy, their CTA chunks and the large-tile work
  * items.  nested_max: cost-model threshold on |R_T|*|S_T| for the nested
- * strategy (< 0: the built-in default; 0: sort + sweep every small tile). */
+ * strategy (< 0: the built-in default; 0: sort + sweep every small tile);
+ * sweep_min: large tiles with |R_T|*|S_T| above it are sorted + swept, the
+ * others brute-forced (< 0: the built-in default; 0: sweep every large tile). */
 int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-              int64_t nested_max, void* stream);
+              int64_t nested_max, int64_t sweep_min, void* stream);
 
 /* Copy the device header to *out and synchronise the stream. */
 int pbsm_read_header(void* ws, pbsm_header* out, void* stream);
@@ -164,10 +173,11 @@ int pbsm_scatter_banded(const void* band, int64_t n, int32_t side, void* ws, int
                         int64_t capacity, void* stream);
 
 /* Scratch bytes for one join over n_units work units
- * (n_units = chunks_nested + chunks_sorted + n_items).  The join entry points
- * take `plan`, the host copy of the header read after pbsm_plan, for the
- * work-unit counts (nested chunks run on a persistent double-buffered grid). */
-int64_t pbsm_join_scratch_bytes(int64_t n_units);
+ * (n_units = chunks_nested + chunks_sorted + n_items) whose large tiles hold
+ * large_entries entries (header.large_r + large_s): the output reservation
+ * state plus the large tiles' sort buffers and sorted copies.  The join entry
+ * points take `plan`, the host copy of the header read after pbsm_plan. */
+int64_t pbsm_join_scratch_bytes(int64_t n_units, int64_t large_entries);
 
 /* sort_segment + sweep_count (_kernels.pyx:188-228, 231-315) for every join
  * tile: the write guard (partition.py:229-233), then the mini-joins over the
@@ -206,7 +216,10 @@ int64_t pbsm_refine_result_offset(int64_t n_cand);
  * sync between pbsm_plan and the emit.  Unordered placement only.
  * r_capacity / s_capacity are the entries the tile-list buffers hold (the
  * capacities given to pbsm_scatter): if the plan's lists are longer, no unit
- * reads them and PBSM_ERR_SCATTER_OVERFLOW is set.  After the final
+ * reads them and PBSM_ERR_SCATTER_OVERFLOW is set; likewise large_capacity
+ * (the large entries the scratch was sized for, pbsm_join_scratch_bytes) and
+ * max_tile (an upper bound of header.max_huge: sets the sort's merge passes)
+ * against the plan's.  After the final
  * pbsm_read_header the caller checks header.chunks_nested <=
  * max_nested_chunks, chunks_sorted + n_items <= max_other_units and the
  * error bits: otherwise some units were not run and the join must be
@@ -214,7 +227,8 @@ int64_t pbsm_refine_result_offset(int64_t n_cand);
 int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                            const pbsm_entry* r_list, int64_t r_capacity,
                            const pbsm_entry* s_list, int64_t s_capacity,
-                           int64_t max_nested_chunks, int64_t max_other_units, void* scratch,
+                           int64_t max_nested_chunks, int64_t max_other_units,
+                           int64_t large_capacity, int64_t max_tile, void* scratch,
                            int64_t* pairs, int64_t capacity, void* stream);
 
 /* pairs[2i], pairs[2i+1] (row indices, i < n) → r_ids[...], s_ids[...] in

@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
@@ -45,8 +45,9 @@ class Header(C.Structure):
         ("n_nested", C.c_int64), ("n_sorted", C.c_int64), ("n_large", C.c_int64),
         ("w_nested", C.c_int64), ("w_sorted", C.c_int64), ("chunks_nested", C.c_int64),
         ("chunks_sorted", C.c_int64), ("n_items", C.c_int64), ("pairs", C.c_int64),
-        ("pair_bound", C.c_int64), ("max_tile", C.c_int64), ("error", C.c_uint32),
-        ("pad", C.c_uint32),
+        ("pair_bound", C.c_int64), ("max_tile", C.c_int64), ("large_r", C.c_int64),
+        ("large_s", C.c_int64), ("sweep_min", C.c_int64), ("max_huge", C.c_int64),
+        ("error", C.c_uint32), ("pad", C.c_uint32),
     ]
 
     @property
@@ -92,19 +93,19 @@ _SIGNATURES = {
     "pbsm_workspace_bytes": (_I64, [_I32, _I32, _I32, _I32]),
     "pbsm_init": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
     "pbsm_count": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P]),
-    "pbsm_plan": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _P]),
+    "pbsm_plan": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _I64, _P]),
     "pbsm_read_header": (C.c_int, [_P, C.POINTER(Header), _P]),
     "pbsm_scatter": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32,
                                _P, _I64, _P]),
     "pbsm_bin": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P, _P]),
     "pbsm_scatter_banded": (C.c_int, [_P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P, _I64, _P]),
-    "pbsm_join_scratch_bytes": (_I64, [_I64]),
+    "pbsm_join_scratch_bytes": (_I64, [_I64, _I64]),
     "pbsm_join_count": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P,
                                   _P]),
     "pbsm_join_emit": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P, _P,
                                  _I64, _I32, _P]),
     "pbsm_join_emit_bounded": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _I64,
-                                         _I64, _I64, _P, _P, _I64, _P]),
+                                         _I64, _I64, _I64, _I64, _P, _P, _I64, _P]),
     "pbsm_unpack_records": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "pbsm_map_ids": (C.c_int, [_P, _I64, _P, _P, _P]),
     "pbsm_group_pairs": (C.c_int, [_P, _I64, _I64, _I32, _I32, _P, _P, _P]),

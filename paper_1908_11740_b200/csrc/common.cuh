@@ -13,8 +13,8 @@ constexpr int kPlanThreads = 256;
 #endif
 constexpr int kPlanPer = PBSM_PLAN_PER;               // tiles per thread
 constexpr int kPlanTile = kPlanThreads * kPlanPer;   // 1024 tiles per CTA
-constexpr int kNV = 12;                              // plan scan lanes (see tile_vals)
-constexpr int kNTot = kNV + 2;  // partials rows: kNV scan lanes + per-CTA max tile + pair bound
+constexpr int kNV = 13;                              // plan scan lanes (see tile_vals)
+constexpr int kNTot = kNV + 3;  // partials rows: kNV scan lanes + per-CTA max tile, pair bound, max huge side
 
 constexpr int kJoinThreads = 256;
 #ifndef PBSM_CHUNK_B
@@ -50,6 +50,19 @@ constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work it
 #define PBSM_LARGE_OTHER 2048
 #endif
 constexpr int kLargeOther = PBSM_LARGE_OTHER;  // other-side entries per large work item
+constexpr int kSweepLeaders = 256;    // leaders per sweep work item (sweep.cuh)
+#ifndef PBSM_SWEEP_MIN
+#define PBSM_SWEEP_MIN (1ll << 26)
+#endif
+// A large tile whose |R_T|*|S_T| exceeds this is sorted + swept (sweep.cuh);
+// smaller ones are brute-forced in work items of 256 x 2048 entries, which
+// on a GPU beats the sort + scan (bounded cost, no divergence) below ~10^8
+// pair tests per tile
+constexpr long long kSweepMin = PBSM_SWEEP_MIN;
+__host__ __device__ __forceinline__ bool is_huge(unsigned a, unsigned b, long long sweep_min) {
+  return (long long)((unsigned long long)a * (unsigned long long)b) > sweep_min;
+}
+constexpr int kSortWindow = 4096;     // entries per shared-memory sort window (sweep.cuh)
 
 constexpr int kScanThreads = 256;
 constexpr int kScanPer = 16;
@@ -108,7 +121,7 @@ struct __align__(32) Half {  // the MBR half of a record: one sector
 
 // ---------------------------------------------------------------- workspace
 struct WsLayout {
-  size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec[2], cdesc[2], lrec, lpre,
+  size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec[2], cdesc[2], lrec, lpre, lwin,
       partials, bc[2], bo, bscan, total;
   u64 tiles;
   u64 nblocks;
@@ -135,6 +148,7 @@ inline WsLayout ws_layout(int kx, int ky, int row_lo, int row_hi) {
   }
   L.lrec = o; o = align_up(o + 16 * T, 256);
   L.lpre = o; o = align_up(o + 4 * (T + 1), 256);
+  L.lwin = o; o = align_up(o + 4 * (T + 1), 256);
   L.partials = o; o = align_up(o + sizeof(u64) * kNTot * (L.nblocks + 1), 256);
   for (int q = 0; q < 2; ++q) {  // per-(band, block) rectangle counts of each input
     L.bc[q] = o; o = align_up(o + 4 * (size_t)kBinSlots * kMaxPartBlocks, 256);
@@ -149,7 +163,7 @@ struct Ws {
   pbsm_header* hdr;
   double* bx;
   double* by;
-  u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *lpre;
+  u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *lpre, *lwin;
   uint4* cdesc[2];  // chunk c: {first tile j0, r_start, s_start, -}; [n_chunks] = ends
   uint4* jrec[2];   // {r_start, s_start, nR, nS}
   uint4* lrec;
@@ -176,6 +190,7 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
   }
   w.lrec = (uint4*)(b + L.lrec);
   w.lpre = (u32*)(b + L.lpre);
+  w.lwin = (u32*)(b + L.lwin);
   w.partials = (u64*)(b + L.partials);
   for (int q = 0; q < 2; ++q) w.bc[q] = (u32*)(b + L.bc[q]);
   w.bo = (u64*)(b + L.bo);

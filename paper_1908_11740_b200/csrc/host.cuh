@@ -63,8 +63,21 @@ inline ScanLayout scan_layout(i64 n) {
   return L;
 }
 
-// join scratch: [ticket | status[n_units]]
-inline size_t join_scratch(i64 n_units) { return 256 + align_up(8 * (size_t)(n_units + 1), 256); }
+// join scratch: [ticket | status[n_units] | large-tile sort area (sweep.cuh)]
+inline size_t join_status_bytes(i64 n_units) {
+  return 256 + align_up(8 * (size_t)(n_units + 1), 256);
+}
+inline size_t join_scratch(i64 n_units, i64 large_entries) {
+  return join_status_bytes(n_units) + large_sort_bytes(large_entries);
+}
+
+// merge passes after the 4096-entry window sort so that a side of `max_tile`
+// entries is one sorted run
+inline int sort_passes(i64 max_tile) {
+  int p = 0;
+  while (((i64)kSortWindow << p) < max_tile) ++p;
+  return p;
+}
 
 int set_smem_attrs() {
   // the dynamic shared-memory opt-in is a per-device function attribute
@@ -80,6 +93,9 @@ int set_smem_attrs() {
   e = cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(JoinSmem));
   if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(k_lsort_win, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSortWindow * 12);
+  if (e != cudaSuccess) return (int)e;
   done.fetch_or(bit, std::memory_order_release);
   return 0;
 }
@@ -87,7 +103,8 @@ int set_smem_attrs() {
 int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, int row_hi,
                 const pbsm_entry* r_list, const pbsm_entry* s_list, const pbsm_header* plan,
                 void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s,
-                i64 max_nested = -1, i64 max_other = -1, i64 cap_r = -1, i64 cap_s = -1) {
+                i64 max_nested = -1, i64 max_other = -1, i64 cap_r = -1, i64 cap_s = -1,
+                i64 large_cap = 0, i64 max_tile = 0) {
   int rc = set_smem_attrs();
   if (rc) return rc;
   const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
@@ -96,6 +113,9 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   const i64 cn = bounded ? max_nested : plan->chunks_nested;
   const i64 rest = bounded ? max_other : plan->chunks_sorted + plan->n_items;
   const i64 n_units = cn + rest;
+  // large tiles: sort buffers sized from the plan (or the caller's bounds)
+  const i64 lcap = bounded ? large_cap : plan->large_r + plan->large_s;
+  const i64 mtile = bounded ? max_tile : plan->max_huge;
   // the write guard (reads the cursors the scatter left behind) runs inside
   // the nested join when there is one, else as its own kernel
   const bool fused_guard = cn > 0;
@@ -106,7 +126,7 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   }
   cudaMemsetAsync(&w.hdr->pairs, 0, sizeof(int64_t), s);
   if (n_units == 0) return launch_status();
-  if (ordered) cudaMemsetAsync(scratch, 0, join_scratch(n_units), s);
+  if (ordered) cudaMemsetAsync(scratch, 0, join_status_bytes(n_units), s);
   JoinArgs A;
   for (int q = 0; q < 2; ++q) {
     A.jrec[q] = w.jrec[q];
@@ -114,6 +134,8 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   }
   A.lrec = w.lrec;
   A.lpre = w.lpre;
+  A.ls = large_sort_bind((char*)scratch + join_status_bytes(n_units), lcap);
+  A.ls.passes = sort_passes(mtile);
   A.rl = reinterpret_cast<const Rec*>(r_list);
   A.sl = reinterpret_cast<const Rec*>(s_list);
   A.ticket = (u32*)scratch;
@@ -138,6 +160,20 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
       k_join_nested<true><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
     else
       k_join_nested<false><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+  }
+  if (rest > 0 && lcap > 0 && mtile > 0) {
+    // huge tiles: window sort, merge passes, sorted copy (sweep.cuh); a CTA
+    // per sort window (grid: an upper bound, CTAs past the last window exit)
+    const i64 windows = std::min<i64>((lcap + kSortWindow - 1) / kSortWindow +
+                                          2 * (bounded ? max_other : plan->n_large) + 2,
+                                      0x7fffffff);
+    const Rec* rr = reinterpret_cast<const Rec*>(r_list);
+    const Rec* sr = reinterpret_cast<const Rec*>(s_list);
+    k_lsort_win<<<(unsigned)windows, kSortThreads, kSortWindow * 12, s>>>(rr, sr, w.lrec, w.lwin,
+                                                                          w.hdr, A.ls);
+    for (int p = 0; p < A.ls.passes; ++p)
+      k_lmerge<<<(unsigned)windows, 256, 0, s>>>(w.lrec, w.lwin, w.hdr, A.ls, p);
+    k_lgather<<<(unsigned)windows, 256, 0, s>>>(rr, sr, w.lrec, w.lwin, w.hdr, A.ls);
   }
   if (rest > 0) {
     // the sorted/large launch keeps its own ticket (the look-back ids follow

@@ -9,6 +9,7 @@ struct JoinArgs {
   const uint4* cdesc[2];
   const uint4* lrec;
   const u32* lpre;
+  LargeSort ls;            // huge tiles: sort buffers and the sorted copies (sweep.cuh)
   const Rec* rl;
   const Rec* sl;
   u32* ticket;
@@ -65,6 +66,7 @@ struct LargeSmem {
 union JoinSmem {
   ChunkSmem c;
   LargeSmem l;
+  SweepSmem w;
 };
 
 // Decoupled look-back (one thread): publish this unit's count, accumulate the
@@ -344,24 +346,9 @@ __device__ __forceinline__ u32 large_pass(LargeSmem& S, int n, bool have, const 
 }
 
 template <bool EMIT>
-__device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) {
+__device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item, int lj,
+                           uint4 rec) {
   const int tid = threadIdx.x;
-  // item → large tile: the last tile whose work-item prefix is <= item.
-  // 32-ary search, every warp on its own (same addresses): each step the
-  // lanes probe 32 evenly spaced prefixes at once, so the dependent chain is
-  // log32 instead of log2 loads long (the binary search was ~12% of the
-  // kernel's stall samples on cfg2)
-  int lo = 0, hi = (int)A.hdr->n_large;  // lpre[0] = 0 <= item
-  const int lane = tid & 31;
-  while (hi - lo > 1) {
-    const int step = (hi - lo + 31) >> 5;
-    const int m = lo + lane * step;
-    const unsigned le = __ballot_sync(0xffffffffu, m < hi && (i64)__ldg(A.lpre + m) <= item);
-    lo += (31 - __clz(le)) * step;  // prefixes are non-decreasing: le is a lane prefix
-    hi = min(hi, lo + step);
-  }
-  const int lj = lo;
-  const uint4 rec = A.lrec[lj];
   const u32 nR = rec.z, nS = rec.w;
   const bool lead_r = nR >= nS;
   const u32 no = lead_r ? nS : nR;
@@ -439,6 +426,119 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item) 
       if (!ok && cnt) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
       out = A.pairs + 2 * start;
     }
+  }
+}
+
+// Huge join tiles (large, and |R_T|*|S_T| above the plan's sweep threshold):
+// both sides were sorted by x-lower
+// (sweep.cuh: k_lsort_win, k_lmerge, k_lgather); work item = 256 consecutive
+// sorted entries of one side, one leader per thread, each running the
+// forward scan with a binary-searched start (sweep_leader).  Items of a tile:
+// its R leader blocks, then its S leader blocks.
+template <bool EMIT>
+__device__ void join_sweep(SweepSmem& S, const JoinArgs& A, i64 unit, i64 item, int lo,
+                           uint4 rec) {
+  const int tid = threadIdx.x;
+  const LargeGeo g = large_geo(A.hdr);
+  const bool ok = large_fits(g, A.hdr, A.ls);
+  const LargeSort& L = A.ls;
+  const i64 nbR = (rec.z + kSweepLeaders - 1) / kSweepLeaders;
+  const i64 li = item - (i64)A.lpre[lo];
+  const bool lead_r = li < nbR;
+  const i64 blk = lead_r ? li : li - nbR;
+  const i64 r_lo = (i64)rec.x - g.rl0, s_lo = g.LR + ((i64)rec.y - g.sl0);
+  const i64 l_lo = lead_r ? r_lo : s_lo, l_n = lead_r ? rec.z : rec.w;
+  const i64 p_lo = lead_r ? s_lo : r_lo, p_n = lead_r ? rec.w : rec.z;
+  const i64 me = l_lo + blk * kSweepLeaders + tid;
+  const bool have = ok && me < l_lo + l_n;
+  if (tid == 0) {
+    S.pin_n = ok ? xin_count(L, p_lo, p_lo + p_n) : 0;
+    S.ulo = 0x7fffffffffffffffll;
+    S.uhi = 0;
+    S.nhit = 0;
+    if (!ok) atomicOr(&A.hdr->error, PBSM_ERR_SCATTER_OVERFLOW);
+  }
+  __syncthreads();
+  const i64 pn = S.pin_n;
+  u64 mk = 0;
+  double mxu = 0, myl = 0, myu = 0;
+  i64 k0 = 0, k1 = 0;
+  if (have) {
+    mk = L.sk[me];
+    mxu = L.sxu[me];
+    myl = L.syl[me];
+    myu = L.syu[me];
+    sweep_range(L, mk, mxu, lead_r, p_lo, pn, k0, k1);
+    if (k1 > k0) {
+      atomicMin(&S.ulo, (long long)k0);
+      atomicMax(&S.uhi, (long long)k1);
+    }
+  }
+  __syncthreads();
+  const i64 ulo = S.ulo, uhi = S.uhi;
+  const bool myin = !(mk & kYOut);
+  // one pass over the union in pieces; pass 2 only if the hit list overflowed
+  u32 cnt = 0;
+  i64* out = nullptr;
+  bool list_ok = true;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (i64 pb = ulo; pb < uhi; pb += kSweepPiece) {
+      const int n = (int)min((i64)kSweepPiece, uhi - pb);
+      __syncthreads();  // previous piece consumed
+      for (int k = tid; k < n; k += kJoinThreads) {
+        S.pk[k] = L.sk[pb + k];
+        S.py[k] = make_double2(L.syl[pb + k], L.syu[pb + k]);
+      }
+      __syncthreads();
+      const i64 a = max(k0, pb), b = min(k1, pb + n);
+      for (i64 k = a; k < b; ++k) {
+        const u64 ok_ = S.pk[k - pb];
+        const double2 oy = S.py[k - pb];
+        if (myl <= oy.y && oy.x <= myu && (myin || !(ok_ & kYOut))) {
+          if (pass == 0) {
+            if (EMIT) {
+              const u32 h = atomicAdd_block(&S.nhit, 1u);
+              if (h < (u32)kSweepHits) {
+                S.hit_p[h] = (u32)k;
+                S.hit_l[h] = (unsigned char)tid;
+              }
+            }
+            ++cnt;
+          } else {
+            const i64 a_id = L.sid[me], o_id = L.sid[k];
+            *reinterpret_cast<longlong2*>(out) =
+                lead_r ? make_longlong2(a_id, o_id) : make_longlong2(o_id, a_id);
+            out += 2;
+          }
+        }
+      }
+    }
+    if (pass == 1) break;
+    u64 total;
+    const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
+    if (!EMIT) {
+      if (tid == 0 && total) atomicAdd(A.total, total);
+      return;
+    }
+    if (tid == 0) S.base = reserve(A, unit, total);
+    __syncthreads();
+    if ((i64)(S.base + total) > A.capacity) {
+      if (tid == 0 && total) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
+      return;
+    }
+    if (total <= (u64)kSweepHits) {
+      // every hit is in the list: one coalesced 16-byte store per hit
+      i64* o = A.pairs + 2 * (i64)S.base;
+      for (u32 h = tid; h < (u32)total; h += kJoinThreads) {
+        const i64 a_id = L.sid[l_lo + blk * kSweepLeaders + S.hit_l[h]];
+        const i64 o_id = L.sid[S.hit_p[h]];
+        *reinterpret_cast<longlong2*>(o + 2 * (i64)h) =
+            lead_r ? make_longlong2(a_id, o_id) : make_longlong2(o_id, a_id);
+      }
+      return;
+    }
+    out = A.pairs + 2 * (i64)(S.base + excl);
+    (void)list_ok;
   }
 }
 
@@ -792,5 +892,22 @@ __global__ void __launch_bounds__(kJoinThreads, PBSM_JOIN_MINB) k_join(JoinArgs 
   if (A.bounded && lists_overflow(A)) return;
   const i64 unit = cn + local;
   if (local < cs) join_sorted<EMIT>(U.c, A, unit, local);
-  else join_large<EMIT>(U.l, A, unit, local - cs);
+  else {
+    // large work item → its tile: the last whose item prefix is <= item
+    // (32-ary search, every warp on its own: log32 dependent loads)
+    const i64 item = local - cs;
+    const i64 smin = A.hdr->sweep_min;  // (in flight during the search)
+    int lo = 0, hi = (int)A.hdr->n_large;  // lpre[0] = 0 <= item
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 1) {
+      const int step = (hi - lo + 31) >> 5;
+      const int m = lo + lane * step;
+      const unsigned le = __ballot_sync(0xffffffffu, m < hi && (i64)__ldg(A.lpre + m) <= item);
+      lo += (31 - __clz(le)) * step;  // prefixes are non-decreasing: le is a lane prefix
+      hi = min(hi, lo + step);
+    }
+    const uint4 rec = A.lrec[lo];
+    if (is_huge(rec.z, rec.w, smin)) join_sweep<EMIT>(U.w, A, unit, item, lo, rec);
+    else join_large<EMIT>(U.l, A, unit, item, lo, rec);
+  }
 }

@@ -462,11 +462,12 @@ __global__ void k_guard(const u32* __restrict__ cur_r, const u32* __restrict__ e
 }
 
 // ---------------------------------------------------------------- 1b plan
-// Per tile t the plan scans twelve lanes at once (one exclusive scan each):
+// Per tile t the plan scans thirteen lanes at once (one exclusive scan each):
 //   0 |R_T|  1 |S_T|                          all tiles (A_R, A_S totals)
 //   2..4   nested tiles: flag, |R_T|, |S_T|
 //   5..7   sorted tiles: flag, |R_T|, |S_T|
-//   8..11  large tiles:  flag, work items, |R_T|, |S_T|
+//   8..12  large tiles:  flag, sweep work items (256 leaders of one side
+//          each), |R_T|, |S_T|, sort windows (4096 entries of one side each)
 // A join tile has both inputs non-empty (build_task_queue, engine.py:97);
 // its strategy comes from the cost model in include/pbsm.h.  The |R_T| /
 // |S_T| lanes of the three strategies give the tile-list offsets
@@ -477,7 +478,7 @@ __global__ void k_guard(const u32* __restrict__ cur_r, const u32* __restrict__ e
 // lanes are u32 (a CTA's sums never exceed the u32-checked totals); the
 // per-CTA partial sums are u64.
 enum TileKind { kNone = 0, kNested = 1, kSorted = 2, kLarge = 3 };
-enum Lane { L_A, L_B, L_NF, L_NA, L_NB, L_SF, L_SA, L_SB, L_LF, L_LI, L_LA, L_LB };
+enum Lane { L_A, L_B, L_NF, L_NA, L_NB, L_SF, L_SA, L_SB, L_LF, L_LI, L_LA, L_LB, L_LW };
 
 __device__ __forceinline__ int tile_kind(u32 a, u32 b, i64 nested_max) {
   if (a == 0u || b == 0u) return kNone;
@@ -485,9 +486,8 @@ __device__ __forceinline__ int tile_kind(u32 a, u32 b, i64 nested_max) {
   return (i64)((u64)a * (u64)b) <= nested_max ? kNested : kSorted;
 }
 
-__device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u32 v[kNV]) {
+__device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u32 v[kNV], i64 sm) {
   const int kind = tile_kind(a, b, nm);
-  const u32 lead = a >= b ? a : b, other = a >= b ? b : a;
 #pragma unroll
   for (int q = 0; q < kNV; ++q) v[q] = 0;
   v[L_A] = a;
@@ -502,24 +502,31 @@ __device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u32 v[kNV]) {
     v[L_SB] = b;
   } else if (kind == kLarge) {
     v[L_LF] = 1;
-    v[L_LI] = ((lead + kLargeLead - 1) / kLargeLead) * ((other + kLargeOther - 1) / kLargeOther);
     v[L_LA] = a;
     v[L_LB] = b;
+    if (is_huge(a, b, sm)) {  // sort + sweep: leader blocks of each side, sort windows
+      v[L_LI] = (a + kSweepLeaders - 1) / kSweepLeaders + (b + kSweepLeaders - 1) / kSweepLeaders;
+      v[L_LW] = (a + kSortWindow - 1) / kSortWindow + (b + kSortWindow - 1) / kSortWindow;
+    } else {  // brute force: lead blocks × other blocks
+      const u32 lead = a >= b ? a : b, other = a >= b ? b : a;
+      v[L_LI] = ((lead + kLargeLead - 1) / kLargeLead) * ((other + kLargeOther - 1) / kLargeOther);
+    }
   }
 }
 
 __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restrict__ cr,
                                                               const u32* __restrict__ cs,
-                                                              u64 T, i64 nm,
+                                                              u64 T, i64 nm, i64 sm,
                                                               u64* __restrict__ partials,
                                                               pbsm_header* hdr) {
   __shared__ u32 sh[kPlanThreads / 32][kNV];
   __shared__ u32 shmax[kPlanThreads / 32];
+  __shared__ u32 shhuge[kPlanThreads / 32];
   __shared__ u64 shb[kPlanThreads / 32];
   u32 acc[kNV];
 #pragma unroll
   for (int q = 0; q < kNV; ++q) acc[q] = 0;
-  u32 mx = 0;
+  u32 mx = 0, mh = 0;
   u64 bound = 0;
   const u64 base = (u64)blockIdx.x * kPlanTile;
 #pragma unroll
@@ -527,12 +534,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
     const u64 t = base + (u64)i * kPlanThreads + threadIdx.x;
     const u32 a = t < T ? cr[t] : 0u, b = t < T ? cs[t] : 0u;
     u32 v[kNV];
-    tile_vals(a, b, nm, v);
+    tile_vals(a, b, nm, v, sm);
 #pragma unroll
     for (int q = 0; q < kNV; ++q) acc[q] += v[q];
     if (a && b) {
       mx = max(mx, a + b);
       bound += (u64)a * (u64)b;
+      if (a + b > (u32)kLmax && is_huge(a, b, sm)) mh = max(mh, max(a, b));
     }
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -546,10 +554,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    mh = max(mh, __shfl_down_sync(0xffffffffu, mh, o));
     bound += __shfl_down_sync(0xffffffffu, bound, o);
   }
   if (lane == 0) {
     shmax[wid] = mx;
+    shhuge[wid] = mh;
     shb[wid] = bound;
   }
   __syncthreads();
@@ -559,16 +569,18 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
     partials[(u64)threadIdx.x * (gridDim.x + 1) + blockIdx.x] = s;
   }
   if (threadIdx.x == 0) {
-    u32 m = 0;
+    u32 m = 0, h = 0;
     u64 bs = 0;
     for (int w = 0; w < kPlanThreads / 32; ++w) {
       m = max(m, shmax[w]);
+      h = max(h, shhuge[w]);
       bs += shb[w];
     }
     // into two extra partials rows, reduced by k_plan_partials (a header
     // atomic per CTA queued ~4000 same-address atomics at one L2 slice)
     partials[(u64)kNV * (gridDim.x + 1) + blockIdx.x] = m;
     partials[(u64)(kNV + 1) * (gridDim.x + 1) + blockIdx.x] = bs;
+    partials[(u64)(kNV + 2) * (gridDim.x + 1) + blockIdx.x] = h;
   }
 }
 
@@ -579,7 +591,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
 constexpr int kPartThreads = 1024;
 __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict__ partials, u64 nb,
                                                                  pbsm_header* hdr, uint4* cd_n,
-                                                                 uint4* cd_s, u32* lpre) {
+                                                                 uint4* cd_s, u32* lpre,
+                                                                 u32* lwin, i64 sm) {
   __shared__ u64 sh[kPartThreads / 32 + 1];
   __shared__ bool last;
   u64* row = partials + (u64)blockIdx.x * (nb + 1);
@@ -587,29 +600,36 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
   if (blockIdx.x == kNV) {
     // the extra CTA: max tile and pair bound over the plan CTAs' rows
     const u64* rb = row + (nb + 1);
-    u64 m = 0, bs = 0;
+    const u64* rh = rb + (nb + 1);
+    u64 m = 0, bs = 0, mh = 0;
     for (u64 i = threadIdx.x; i < nb; i += kPartThreads) {
       m = max(m, row[i]);
       bs += rb[i];
+      mh = max(mh, rh[i]);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+      mh = max(mh, __shfl_down_sync(0xffffffffu, mh, o));
       bs += __shfl_down_sync(0xffffffffu, bs, o);
     }
-    __shared__ u64 wm[kPartThreads / 32], wb[kPartThreads / 32];
+    __shared__ u64 wm[kPartThreads / 32], wb[kPartThreads / 32], wh[kPartThreads / 32];
     if ((threadIdx.x & 31) == 0) {
       wm[threadIdx.x >> 5] = m;
       wb[threadIdx.x >> 5] = bs;
+      wh[threadIdx.x >> 5] = mh;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int w = 1; w < kPartThreads / 32; ++w) {
         m = max(m, wm[w]);
         bs += wb[w];
+        mh = max(mh, wh[w]);
       }
       hdr->max_tile = (i64)m;
       hdr->pair_bound = (i64)bs;
+      hdr->max_huge = (i64)mh;
+      hdr->sweep_min = sm;
     }
   }
   for (u64 base = 0; blockIdx.x < kNV && base < nb; base += 4 * kPartThreads) {
@@ -649,6 +669,8 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
     const u64 lr = c[L_NA] + c[L_SA] + c[L_LA], ls = c[L_NB] + c[L_SB] + c[L_LB];
     hdr->list_r = (i64)lr;
     hdr->list_s = (i64)ls;
+    hdr->large_r = (i64)c[L_LA];
+    hdr->large_s = (i64)c[L_LB];
     // chunk counts and the closing descriptors (see k_plan_apply)
     const u64 wn = c[L_NA] + c[L_NB], ws = c[L_SA] + c[L_SB];
     const u64 chn = wn ? (wn - 1) / kChunkBN + 1 : 0, chs = ws ? (ws - 1) / kChunkB + 1 : 0;
@@ -660,6 +682,7 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
     if (c[L_A] >= kSkip || c[L_B] >= kSkip || lr >= kSkip || ls >= kSkip || c[L_LI] >= kSkip)
       hdr->error |= PBSM_ERR_TOTAL_RANGE;
     lpre[c[L_LF]] = (u32)c[L_LI];
+    lwin[c[L_LF]] = (u32)c[L_LW];
   }
 }
 
@@ -669,13 +692,14 @@ struct PlanOut {
   uint4* cdesc[2];
   uint4* lrec;
   u32* lpre;
+  u32* lwin;
 };
 
 // the lanes k_plan_apply scans: every lane but the two totals (L_A, L_B)
 constexpr int kNA = kNV - 2;
 __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32* __restrict__ cr,
                                                              u32* __restrict__ cs, u64 T, u64 nb,
-                                                             i64 nm,
+                                                             i64 nm, i64 sm,
                                                              const u64* __restrict__ partials,
                                                              PlanOut P) {
   __shared__ u32 sa[kPlanTile];   // counts, then the tiles' list starts
@@ -709,7 +733,7 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
     a[i] = sa[threadIdx.x * kPlanPer + i];
     b[i] = sb[threadIdx.x * kPlanPer + i];
     u32 v[kNV];
-    tile_vals(a[i], b[i], nm, v);
+    tile_vals(a[i], b[i], nm, v, sm);
 #pragma unroll
     for (int q = 0; q < kNA; ++q) pre[q] += v[q + 2];
   }
@@ -770,13 +794,15 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
       if (t < T) {
         P.lrec[g(L_LF)] = make_uint4(r0, s0, a[i], b[i]);
         P.lpre[g(L_LF)] = (u32)g(L_LI);
+        P.lwin[g(L_LF)] = (u32)g(L_LW);
       }
       u32 v[kNV];
-      tile_vals(a[i], b[i], nm, v);
+      tile_vals(a[i], b[i], nm, v, sm);
       pre[L_LF - 2] += 1u;
       pre[L_LI - 2] += v[L_LI];
       pre[L_LA - 2] += a[i];
       pre[L_LB - 2] += b[i];
+      pre[L_LW - 2] += v[L_LW];
     }
     sa[threadIdx.x * kPlanPer + i] = r0;
     sb[threadIdx.x * kPlanPer + i] = s0;

@@ -69,6 +69,7 @@ namespace {
 // so every kernel is in one fatbinary and nothing crosses a link boundary).
 #include "common.cuh"
 #include "partition.cuh"
+#include "sweep.cuh"
 #include "join.cuh"
 #include "extras.cuh"
 #include "host.cuh"
@@ -122,15 +123,16 @@ int pbsm_count(const double* xl, const double* xu, const double* yl, const doubl
 }
 
 int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
-              int64_t nested_max, void* stream) {
+              int64_t nested_max, int64_t sweep_min, void* stream) {
   if (!ws || !grid_ok(kx, ky, row_lo, row_hi)) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
   cudaStream_t s = as_stream(stream);
   const i64 nm = nested_max < 0 ? (i64)kNestedMax : (i64)nested_max;
-  k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles, nm,
+  const i64 sm = sweep_min < 0 ? (i64)kSweepMin : (i64)sweep_min;
+  k_plan_reduce<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles, nm, sm,
                                                               w.partials, w.hdr);
   k_plan_partials<<<kNV + 1, kPartThreads, 0, s>>>(w.partials, w.nblocks, w.hdr, w.cdesc[0],
-                                                w.cdesc[1], w.lpre);
+                                                w.cdesc[1], w.lpre, w.lwin, sm);
   PlanOut P;
   P.cur_r = w.cur_r;
   P.cur_s = w.cur_s;
@@ -140,8 +142,9 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
   }
   P.lrec = w.lrec;
   P.lpre = w.lpre;
+  P.lwin = w.lwin;
   k_plan_apply<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles,
-                                                             w.nblocks, nm, w.partials, P);
+                                                             w.nblocks, nm, sm, w.partials, P);
   return launch_status();
 }
 
@@ -231,9 +234,9 @@ int pbsm_bin(const int64_t* ids, const double* xl, const double* xu, const doubl
   return launch_status();
 }
 
-int64_t pbsm_join_scratch_bytes(int64_t n_units) {
-  if (n_units < 0) return PBSM_E_ARG;
-  return (int64_t)join_scratch(n_units);
+int64_t pbsm_join_scratch_bytes(int64_t n_units, int64_t large_entries) {
+  if (n_units < 0 || large_entries < 0) return PBSM_E_ARG;
+  return (int64_t)join_scratch(n_units, large_entries);
 }
 
 int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
@@ -258,16 +261,17 @@ int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
 int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                            const pbsm_entry* r_list, int64_t r_capacity,
                            const pbsm_entry* s_list, int64_t s_capacity,
-                           int64_t max_nested_chunks, int64_t max_other_units, void* scratch,
+                           int64_t max_nested_chunks, int64_t max_other_units,
+                           int64_t large_capacity, int64_t max_tile, void* scratch,
                            int64_t* pairs, int64_t capacity, void* stream) {
   if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || capacity < 0 ||
       (capacity > 0 && !pairs) || max_nested_chunks < 0 || max_other_units < 0 ||
       max_nested_chunks > 0x7fffffff || max_other_units > 0x7fffffff || r_capacity < 0 ||
-      s_capacity < 0)
+      s_capacity < 0 || large_capacity < 0 || max_tile < 0)
     return PBSM_E_ARG;
   return launch_join(true, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, nullptr, scratch,
                      pairs, capacity, as_stream(stream), max_nested_chunks, max_other_units,
-                     r_capacity, s_capacity);
+                     r_capacity, s_capacity, large_capacity, max_tile);
 }
 
 int64_t pbsm_refine_scratch_bytes(int64_t n_cand) {

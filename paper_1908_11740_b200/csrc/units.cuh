@@ -1088,10 +1088,11 @@ __global__ void __launch_bounds__(kUJoinThreads, 6) k_uchunks(UJoinArgs A) {
 // predicate and the class rule, count → reserve → emit (hits kept in a list;
 // a second pass re-tests if the list overflows).  Persistent CTAs take items
 // by ticket.
+constexpr int kULargeHitCap = 4096;  // hits of a deferred-tile work item kept for the emit
 struct ULargeSmem {
   URec other[kCap];
   u32 oidx[kCap];
-  u32 hit[kLargeHitCap];  // lead thread | other index (in the item) << 8
+  u32 hit[kULargeHitCap];  // lead thread | other index (in the item) << 8
   u32 lead_idx[kJoinThreads];
   u64 scan[kJoinThreads / 32 + 1];
   u64 base;
@@ -1120,7 +1121,7 @@ __device__ __forceinline__ u32 ularge_pass(ULargeSmem& S, int n, bool have, cons
       }
       if (LIST) {
         const u32 h = atomicAdd_block(&S.nhit, 1u);
-        if (h < (u32)kLargeHitCap) S.hit[h] = threadIdx.x | ((k0 + (u32)k) << 8);
+        if (h < (u32)kULargeHitCap) S.hit[h] = threadIdx.x | ((k0 + (u32)k) << 8);
       }
       ++c;
     }
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(kJoinThreads, 2) k_ularge(UJoinArgs A) {
       S.lead_idx[tid] = my_idx;
       __syncthreads();
       if (S.base == ~0ull || total == 0) break;
-      if (total <= (u64)kLargeHitCap) {
+      if (total <= (u64)kULargeHitCap) {
         i64* o = A.pairs + 2 * (i64)S.base;
         for (u32 h = tid; h < (u32)total; h += kJoinThreads) {
           const u32 hv = S.hit[h];

@@ -542,7 +542,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
              keep_counts: bool = False, probe: PhaseProbe | None = None,
              ordered: bool = False, nested_max: int = -1,
              bin_bytes: int | None = None, defer_map: bool = False,
-             pipeline: str | None = None) -> DeviceJoinResult:
+             pipeline: str | None = None, sweep_min: int = -1) -> DeviceJoinResult:
     """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
 
     Two device pipelines compute the same pair set: the tile-list pipeline
@@ -553,6 +553,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     ``probe`` (optional) gets an event after each library call, named after
     the phase that call ran: init, count, plan, header, scatter, join, header2.
     ``nested_max`` overrides the mini-join cost-model threshold (pbsm_plan);
+    ``sweep_min``: large tiles with |R_T|*|S_T| above it are sorted and swept,
+    the others brute-forced (pbsm_plan; -1 = default, 0 = sweep them all);
     ``ordered`` selects the look-back (unit-major) output placement;
     ``bin_bytes``: tile lists larger than this go through the row-band copy
     (pbsm_bin) before the scatter (default BIN_LIST_BYTES; 0 = always).
@@ -569,7 +571,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         empty = torch.empty((0, 2), dtype=torch.int64, device=device) if collect else None
         return DeviceJoinResult(0, empty)
     if (pipeline == "units" or (pipeline is None and UNITS)) and not ordered and not keep_counts \
-            and nested_max == -1 and bin_bytes is None \
+            and nested_max == -1 and bin_bytes is None and sweep_min == -1 \
             and lib.pbsm_unit_supported(kx, ky, row_lo, row_hi) == 1:
         return _run_units(lib, r, s, kx, ky, row_lo, row_hi, collect=collect, timing=timing,
                           mark=mark, defer_map=defer_map)
@@ -617,10 +619,10 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     counts = None
     if keep_counts:  # per-tile counts, before the plan turns them into cursor ends
         counts = tuple(v.clone() for v in _tile_count_views(ws, kx, ky, kx * (row_hi - row_lo)))
-    _native.check(lib.pbsm_plan(wsp, *grid, nested_max, stream), "pbsm_plan")
+    _native.check(lib.pbsm_plan(wsp, *grid, nested_max, sweep_min, stream), "pbsm_plan")
     mark("plan")
     key = (str(device), stream, kx, ky, row_lo, row_hi, len(r), len(s), s is r, nested_max,
-           bin_bytes)
+           bin_bytes, sweep_min)
     guess = _plan_cache.get(key) if (SPECULATE and collect and not ordered
                                      and not keep_counts) else None
     if guess is None:
@@ -672,12 +674,14 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     rl, sl = lists
     if guess is not None:
         cap, cn, rest = guess["pairs"], guess["nested"], guess["other"]
-        scratch = _buffer(device, "scratch", (int(lib.pbsm_join_scratch_bytes(cn + rest)),),
+        lcap, mtile = guess["large"], guess["max_huge"]
+        scratch = _buffer(device, "scratch",
+                          (int(lib.pbsm_join_scratch_bytes(cn + rest, lcap)),),
                           torch.uint8, stream)
         pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
         mark("alloc")
         _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), list_r,
-                                                 sl.data_ptr(), list_s, cn, rest,
+                                                 sl.data_ptr(), list_s, cn, rest, lcap, mtile,
                                                  scratch.data_ptr(), pairs.data_ptr(), cap,
                                                  stream), "pbsm_join_emit_bounded")
         mark("join")
@@ -693,7 +697,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
             return run_join(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
                             timing=timing, keep_counts=keep_counts, probe=probe,
                             ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes,
-                            defer_map=defer_map, pipeline="tiles")
+                            defer_map=defer_map, pipeline="tiles", sweep_min=sweep_min)
         count = int(h2.pairs)
         if late and not defer_map:
             _map_ids(lib, pairs, count, r, s, cur, stream)
@@ -709,7 +713,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         return res
 
     n_units = h.n_units
-    scratch = _buffer(device, "scratch", (int(lib.pbsm_join_scratch_bytes(n_units)),),
+    scratch = _buffer(device, "scratch",
+                      (int(lib.pbsm_join_scratch_bytes(n_units, h.large_r + h.large_s)),),
                       torch.uint8, stream)
     pairs = None
     if not collect:
@@ -742,7 +747,9 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                     del _plan_cache[k_]  # one shape per (device, stream)
                 _plan_cache[key] = {"list_r": h.list_r, "list_s": h.list_s, "pairs": cap,
                                 "nested": h.chunks_nested,
-                                "other": h.chunks_sorted + h.n_items}
+                                "other": h.chunks_sorted + h.n_items,
+                                "large": int(h.large_r + h.large_s),
+                                "max_huge": int(h.max_huge)}
     if ev:
         ev[2].record()
         ev[2].synchronize()

@@ -34,8 +34,10 @@ def test_workspace_sizing_and_argument_errors():
     assert lib.pbsm_workspace_bytes(0, 100, 0, 100) < 0
     assert lib.pbsm_workspace_bytes(10, 10, 5, 5) < 0
     assert lib.pbsm_init(None, 4, 4, 0, 4, None) < 0
-    assert lib.pbsm_join_scratch_bytes(-1) < 0
-    assert lib.pbsm_join_scratch_bytes(0) > 0
+    assert lib.pbsm_join_scratch_bytes(-1, 0) < 0
+    assert lib.pbsm_join_scratch_bytes(0, -1) < 0
+    assert lib.pbsm_join_scratch_bytes(0, 0) > 0
+    assert lib.pbsm_join_scratch_bytes(10, 1000) > lib.pbsm_join_scratch_bytes(10, 0)
 
 
 @pytest.mark.parametrize("kw,exc", [

@@ -357,11 +357,13 @@ def test_every_strategy_bit_exact(golden, nested_max, ordered):
     """Force all small tiles through the sort + forward-scan path (0), or all
     through the nested path (huge), in both output-order modes."""
     g = golden["configs"]
-    for cfg in (1, 2, 4, 5):
+    for cfg in (1, 2, 3, 4, 5):
         r, s, k = make_config(cfg, float(g[f"cfg{cfg}_scale"]))
         rd = dev.to_device(r)
         sd = rd if s is r else dev.to_device(s)
-        res = dev.run_join(rd, sd, k, k, collect=True, nested_max=nested_max, ordered=ordered)
+        # (and every large tile sorted + swept when the small ones are)
+        res = dev.run_join(rd, sd, k, k, collect=True, nested_max=nested_max, ordered=ordered,
+                           sweep_min=0 if nested_max == 0 else -1)
         h = res.header
         if nested_max == 0:
             assert h["n_nested"] == 0 and h["n_sorted"] > 0
@@ -605,7 +607,7 @@ def test_write_guard_detects_a_skipped_scatter(golden):
         for side, b in ((0, R), (1, S)):
             lib.pbsm_count(b.xl.data_ptr(), b.xu.data_ptr(), b.yl.data_ptr(), b.yu.data_ptr(),
                            len(b), side, wsp, k, k, 0, k, st)
-        lib.pbsm_plan(wsp, k, k, 0, k, nested_max, st)
+        lib.pbsm_plan(wsp, k, k, 0, k, nested_max, -1, st)
         h = _native.Header()
         lib.pbsm_read_header(wsp, C.byref(h), st)
         rl = torch.empty((h.list_r, 8), dtype=torch.int64, device="cuda")
@@ -613,7 +615,8 @@ def test_write_guard_detects_a_skipped_scatter(golden):
         lib.pbsm_scatter(R.ids.data_ptr(), R.xl.data_ptr(), R.xu.data_ptr(), R.yl.data_ptr(),
                          R.yu.data_ptr(), len(R), 0, wsp, k, k, 0, k, rl.data_ptr(), h.list_r, st)
         # S's scatter deliberately skipped
-        scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(h.n_units)), dtype=torch.uint8,
+        scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(h.n_units, h.large_r + h.large_s)),
+                              dtype=torch.uint8,
                               device="cuda")
         pairs = torch.empty((max(h.pair_bound, 1), 2), dtype=torch.int64, device="cuda")
         assert lib.pbsm_join_emit(wsp, k, k, 0, k, rl.data_ptr(), sl.data_ptr(), C.byref(h),
@@ -722,3 +725,56 @@ def test_concurrent_joins_on_two_threads_and_streams(golden):
         count, pairs = out[cfg]
         assert count == int(g[f"cfg{cfg}_count"])
         assert np.array_equal(oracle.sorted_pairs(pairs), g[f"cfg{cfg}_pairs"])
+
+
+def _dense(n, seed, ext):
+    rng = np.random.default_rng(seed)
+    xl, yl = rng.random(n), rng.random(n)
+    return (np.arange(n, dtype=np.int64), xl, np.minimum(xl + rng.random(n) * ext, 1.0), yl,
+            np.minimum(yl + rng.random(n) * ext, 1.0))
+
+
+def test_large_tile_sort_and_sweep_200k():
+    """One dense 200K x 200K tile (K = 1): both sides sorted by x-lower in
+    global memory (window sort + 7 merge passes) and joined by the forward
+    scan — bit-exact against the oracle, in well under 50 ms (the brute force
+    it replaces tested 4e10 pairs, ~11 s)."""
+    import time
+
+    r, s = _dense(200_000, 5, 2e-4), _dense(200_000, 6, 2e-4)
+    want = oracle.sorted_pairs(oracle.join(r, s, "2d", 1, threads=8)["pairs"])
+    R, S = dev.to_device(r), dev.to_device(s)
+    res = dev.run_join(R, S, 1, 1)
+    h = res.header
+    assert h["n_large"] == 1 and h["max_tile"] == 400_000 and h["max_huge"] == 200_000
+    assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        res = dev.run_join(R, S, 1, 1)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 3
+    assert dt < 0.05, dt
+    assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+
+
+@pytest.mark.parametrize("k,n,ext", [(2, 30_000, 3e-2), (3, 50_000, 1e-2), (7, 20_000, 0.2)])
+def test_large_tiles_mixed_sizes_and_classes(k, n, ext):
+    """Several large tiles of uneven sizes (segments not multiples of the
+    4096-entry sort window), many entries of classes B/C/D (big extents):
+    the sorted sweep over each tile's class combinations equals the oracle;
+    also through the ordered (look-back) emit."""
+    r, s = _dense(n, k, ext), _dense(n + 777, k + 100, ext)
+    want = oracle.sorted_pairs(oracle.join(r, s, "2d", k, threads=8)["pairs"])
+    R, S = dev.to_device(r), dev.to_device(s)
+    # sweep every large tile (0), brute-force them all (2^62), the default rule
+    for sweep_min, ordered in ((0, False), (0, True), (1 << 62, False), (-1, False)):
+        res = dev.run_join(R, S, k, k, ordered=ordered, sweep_min=sweep_min)
+        h = res.header
+        assert h["n_large"] > 0
+        if sweep_min == 0:
+            assert h["max_huge"] > 0
+        if sweep_min == 1 << 62:
+            assert h["max_huge"] == 0
+        assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want), (sweep_min,
+                                                                                    ordered)

@@ -35,7 +35,7 @@ for it in range(a.reps + 2):
     for side, b in ((0, R), (1, S)):
         lib.pbsm_count(b.xl.data_ptr(), b.xu.data_ptr(), b.yl.data_ptr(), b.yu.data_ptr(), len(b),
                        side, wsp, k, k, 0, k, st)
-    lib.pbsm_plan(wsp, k, k, 0, k, -1, st)
+    lib.pbsm_plan(wsp, k, k, 0, k, -1, -1, st)
     h = _native.Header()
     lib.pbsm_read_header(wsp, h, st)
     if lists is None:
