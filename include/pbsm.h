@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 8
+#define PBSM_ABI_VERSION 9
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -157,6 +157,28 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu,
                  void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
                  pbsm_entry* out, int64_t capacity, void* stream);
 
+/* ε-distance join (epsilon_distance_join, engine.py:326-353), fused: the
+ * inputs are the POINT columns px, py (the lower corners of the caller's
+ * rectangles, engine.py:333-334) and each one stands for the side-eps square
+ * clip(p -/+ half, 0, 1), half = eps / 2.0 — computed inside the kernels with
+ * the reference's numpy arithmetic (engine.py:342-350), never materialised.
+ * pbsm_count_points / pbsm_scatter_points are pbsm_count / pbsm_scatter over
+ * those squares; each entry also carries its point (pbsm_entry.pad[1..2]),
+ * and pbsm_join_count_eps / pbsm_join_emit_eps keep a candidate pair only if
+ * dx*dx + dy*dy <= eps_sq (every operation rounded on its own, as numpy:
+ * _refine_pairs, engine.py:201-206) — in the count pass and the emit alike,
+ * so no candidate list is ever written.  The plan must come from
+ * pbsm_plan(..., sweep_min = INT64_MAX) (no sorted + swept tiles: their
+ * sorted copies carry no points); otherwise PBSM_E_ARG.  ids may be NULL
+ * (row indices, see pbsm_map_ids). */
+int pbsm_count_points(const double* px, const double* py, int64_t n, int32_t side, double half,
+                      void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                      void* stream);
+int pbsm_scatter_points(const int64_t* ids, const double* px, const double* py, int64_t n,
+                        int32_t side, double half, void* ws, int32_t kx, int32_t ky,
+                        int32_t row_lo, int32_t row_hi, pbsm_entry* out, int64_t capacity,
+                        void* stream);
+
 /* Binned scatter (worth it when an input's tile lists are large, e.g. > 1 GB).
  * pbsm_bin copies the input's rectangles into row-band order — 256 bands of
  * the strip's tile rows, band-major, from the band counts pbsm_count
@@ -187,6 +209,10 @@ int pbsm_join_count(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t ro
                     const pbsm_entry* r_list, const pbsm_entry* s_list,
                     const pbsm_header* plan, void* scratch, void* stream);
 
+int pbsm_join_count_eps(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                        const pbsm_entry* r_list, const pbsm_entry* s_list,
+                        const pbsm_header* plan, void* scratch, double eps_sq, void* stream);
+
 /* sweep_collect (_kernels.pyx:318-341) + aggregation (engine.py:293-309):
  * the same mini-joins; each work unit counts its pairs (pass 1 over shared
  * memory), reserves its output range, and writes its (r_id, s_id) int64
@@ -201,15 +227,11 @@ int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
                    const pbsm_entry* r_list, const pbsm_entry* s_list,
                    const pbsm_header* plan, void* scratch,
                    int64_t* pairs, int64_t capacity, int32_t ordered, void* stream);
+int pbsm_join_emit_eps(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                       const pbsm_entry* r_list, const pbsm_entry* s_list,
+                       const pbsm_header* plan, void* scratch, int64_t* pairs,
+                       int64_t capacity, int32_t ordered, double eps_sq, void* stream);
 
-/* ε-distance refinement (engine.py:201-206, 298-300) of candidate pairs given
- * as ROW indices (cand[2i], cand[2i+1]) into the point arrays p / q: keeps the
- * pairs with dx*dx + dy*dy <= eps_sq (no FMA contraction, numpy rounding) and
- * writes their (p_ids, q_ids) compacted, in candidate order, to out (capacity
- * n_cand pairs).  The kept count is the int64 at byte offset
- * pbsm_refine_result_offset(n_cand) of scratch. */
-int64_t pbsm_refine_scratch_bytes(int64_t n_cand);
-int64_t pbsm_refine_result_offset(int64_t n_cand);
 /* pbsm_join_emit without the host copy of the plan: the kernels read the
  * unit counts from the device header and the grids are the caller's upper
  * bounds (e.g. the previous join's counts), so the pipeline needs no host
@@ -256,10 +278,6 @@ int pbsm_group_pairs(const int64_t* pairs, int64_t n, int64_t chunk_rows, int32_
  * DatasetError for. */
 int pbsm_unpack_records(const void* records, int64_t n, int64_t* ids, double* xl, double* xu,
                         double* yl, double* yu, uint32_t* bad, void* stream);
-
-int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const double* py,
-                const double* qx, const double* qy, const int64_t* p_ids, const int64_t* q_ids,
-                double eps_sq, void* scratch, int64_t* out, void* stream);
 
 /* ======================================================================
  * Unit pipeline (the default path of run_join where it applies): the grid's
@@ -349,6 +367,42 @@ int pbsm_unit_join(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
 /* Copy the unit header to *out (page-locked: a tiny kernel stores it) and
  * synchronise the stream. */
 int pbsm_read_uheader(void* ws, pbsm_uheader* out, void* stream);
+
+/* ======================================================================
+ * Multi-GPU plumbing
+ * ====================================================================== */
+
+/* Strip routing (the input distribution of a strip-sharded join; the
+ * reference is single-process, the step is distributed PBSM's,
+ * PAPER.md:492-496): every rectangle of this rank's slice goes to each strip
+ * [cuts[g], cuts[g+1]) its tile rows [tile_of(yl), tile_of(yu)] meet
+ * (cuts: device int32[world+1], strictly increasing, cuts[0] = 0,
+ * cuts[world] = ky).  pbsm_route_count writes the rectangles per destination
+ * to dest_counts (device int64[world]); pbsm_route_pack (same n, same
+ * scratch, after route_count) then writes them destination-major into
+ * `records` (Σ dest_counts packed 40-byte SJB1 records {id, x_l, y_l, x_u,
+ * y_u}, io.py:113-141): one send buffer for one all_to_all, unpacked on the
+ * receiver by pbsm_unpack_records.  ids may be NULL (row indices). */
+int64_t pbsm_route_scratch_bytes(int64_t n, int32_t ky, int32_t world);
+int pbsm_route_count(const double* yl, const double* yu, int64_t n, int32_t ky,
+                     const int32_t* cuts, int32_t world, void* scratch, int64_t* dest_counts,
+                     void* stream);
+int pbsm_route_pack(const int64_t* ids, const double* xl, const double* xu, const double* yl,
+                    const double* yu, int64_t n, int32_t ky, const int32_t* cuts, int32_t world,
+                    void* scratch, void* records, void* stream);
+
+/* Canonical pair order: a stable LSD radix sort of n (r_id, s_id) int64
+ * pairs (16-byte aligned) into lexicographic order, in place — the parity form
+ * of the reference's unordered pair list (engine.py:61-62, 293-300).
+ * pbsm_pair_digits fills hist (device uint32[16*256]) with the histogram of
+ * every 8-bit digit (d < 8: byte d of s_id, else byte d-8 of r_id, sign bits
+ * flipped); the caller passes as pass_mask the digits that do not hold all
+ * n keys in one bucket (the others cannot reorder anything).  tmp: 16*n
+ * bytes; scratch: pbsm_sort_pairs_scratch_bytes(n). */
+int64_t pbsm_sort_pairs_scratch_bytes(int64_t n);
+int pbsm_pair_digits(const int64_t* pairs, int64_t n, uint32_t* hist, void* stream);
+int pbsm_sort_pairs(int64_t* pairs, int64_t n, uint32_t pass_mask, void* tmp, void* scratch,
+                    void* stream);
 
 /* ABI version / build identification */
 int32_t pbsm_abi_version(void);

@@ -117,3 +117,30 @@ def sorted_pairs(pairs: np.ndarray) -> np.ndarray:
     if len(p) == 0:
         return p
     return p[np.lexsort((p[:, 1], p[:, 0]))]
+
+
+def epsilon_join(p, q, eps: float, k: int) -> dict:
+    """epsilon_distance_join (engine.py:326-353) on the CPU: side-eps squares
+    around the lower corners (engine.py:342-350, row-index ids), the square
+    join through ``join`` above, then _refine_pairs (engine.py:201-206:
+    ``dx*dx + dy*dy <= eps*eps`` in numpy float64) and the id map
+    (engine.py:298-300).  ``q`` may be ``p`` (self-join)."""
+    pc = _cols(p)
+    qc = pc if q is p else _cols(q)
+    half = eps / 2.0
+
+    def squares(c):
+        n = len(c[0])
+        return (np.arange(n, dtype=np.int64), np.clip(c[1] - half, 0.0, 1.0),
+                np.clip(c[1] + half, 0.0, 1.0), np.clip(c[3] - half, 0.0, 1.0),
+                np.clip(c[3] + half, 0.0, 1.0))
+
+    sp = squares(pc)
+    sq = sp if q is p else squares(qc)
+    cand = join(sp, sq, "2d", k)["pairs"]
+    rr, ss = cand[:, 0], cand[:, 1]
+    dx = pc[1][rr] - qc[1][ss]
+    dy = pc[3][rr] - qc[3][ss]
+    keep = dx * dx + dy * dy <= eps * eps
+    pairs = np.stack([pc[0][rr[keep]], qc[0][ss[keep]]], axis=1)
+    return {"count": int(keep.sum()), "pairs": pairs, "candidates": int(len(cand))}

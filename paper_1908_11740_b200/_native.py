@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
@@ -29,8 +29,10 @@ EXPORTED = (
     "pbsm_count", "pbsm_plan", "pbsm_read_header", "pbsm_scatter", "pbsm_bin",
     "pbsm_scatter_banded",
     "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit", "pbsm_join_emit_bounded",
-    "pbsm_unpack_records", "pbsm_refine_scratch_bytes", "pbsm_refine_result_offset",
-    "pbsm_refine", "pbsm_map_ids", "pbsm_group_pairs",
+    "pbsm_unpack_records", "pbsm_map_ids", "pbsm_group_pairs",
+    "pbsm_count_points", "pbsm_scatter_points", "pbsm_join_count_eps", "pbsm_join_emit_eps",
+    "pbsm_route_scratch_bytes", "pbsm_route_count", "pbsm_route_pack",
+    "pbsm_sort_pairs_scratch_bytes", "pbsm_pair_digits", "pbsm_sort_pairs",
     "pbsm_unit_supported", "pbsm_unit_workspace_bytes", "pbsm_unit_bin_bytes",
     "pbsm_unit_scratch_bytes", "pbsm_unit_init", "pbsm_unit_count", "pbsm_unit_map",
     "pbsm_unit_bin", "pbsm_unit_join", "pbsm_read_uheader",
@@ -109,9 +111,20 @@ _SIGNATURES = {
     "pbsm_unpack_records": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "pbsm_map_ids": (C.c_int, [_P, _I64, _P, _P, _P]),
     "pbsm_group_pairs": (C.c_int, [_P, _I64, _I64, _I32, _I32, _P, _P, _P]),
-    "pbsm_refine_scratch_bytes": (_I64, [_I64]),
-    "pbsm_refine_result_offset": (_I64, [_I64]),
-    "pbsm_refine": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),
+    "pbsm_count_points": (C.c_int, [_P, _P, _I64, _I32, C.c_double, _P, _I32, _I32, _I32, _I32,
+                                    _P]),
+    "pbsm_scatter_points": (C.c_int, [_P, _P, _P, _I64, _I32, C.c_double, _P, _I32, _I32, _I32,
+                                      _I32, _P, _I64, _P]),
+    "pbsm_join_count_eps": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P,
+                                      C.c_double, _P]),
+    "pbsm_join_emit_eps": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P,
+                                     _P, _I64, _I32, C.c_double, _P]),
+    "pbsm_route_scratch_bytes": (_I64, [_I64, _I32, _I32]),
+    "pbsm_route_count": (C.c_int, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
+    "pbsm_route_pack": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
+    "pbsm_sort_pairs_scratch_bytes": (_I64, [_I64]),
+    "pbsm_pair_digits": (C.c_int, [_P, _I64, _P, _P]),
+    "pbsm_sort_pairs": (C.c_int, [_P, _I64, C.c_uint32, _P, _P, _P]),
     "pbsm_unit_supported": (_I32, [_I32, _I32, _I32, _I32]),
     "pbsm_unit_workspace_bytes": (_I64, [_I32, _I32, _I32, _I32]),
     "pbsm_unit_bin_bytes": (_I64, [_I64]),

@@ -1,22 +1,7 @@
 // extras.cuh — part of pbsm.cu (one translation unit: included inside its
 // anonymous namespace, after the types and includes at its top).
-// Contents: epsilon refinement, SJB1 unpack, id map.
+// Contents: SJB1 unpack, header publish, id map, pair groups.
 #pragma once
-
-// ---------------------------------------------------------------- ε refinement
-// _refine_pairs (engine.py:201-206): keep a candidate (row i of P, row j of Q)
-// iff dx*dx + dy*dy <= eps^2 with every operation rounded on its own (numpy
-// semantics: no FMA contraction), then map row indices to ids (:298-300).
-__device__ __forceinline__ bool within_eps(const i64* __restrict__ cand, i64 i,
-                                           const double* __restrict__ px,
-                                           const double* __restrict__ py,
-                                           const double* __restrict__ qx,
-                                           const double* __restrict__ qy, double eps_sq) {
-  const i64 a = cand[2 * i], b = cand[2 * i + 1];
-  const double dx = __dsub_rn(px[a], qx[b]);
-  const double dy = __dsub_rn(py[a], qy[b]);
-  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= eps_sq;
-}
 
 // ---------------------------------------------------------------- input formats
 // SJB1 body (io.py:113-141 in the reference): packed little-endian records
@@ -43,29 +28,6 @@ __global__ void k_unpack_records(const u64* __restrict__ rec, i64 n, i64* __rest
     b |= !(a <= bb) || !(c <= d);
   }
   if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1u);
-}
-
-__global__ void k_refine_flag(const i64* __restrict__ cand, i64 n, const double* __restrict__ px,
-                              const double* __restrict__ py, const double* __restrict__ qx,
-                              const double* __restrict__ qy, double eps_sq,
-                              u32* __restrict__ flag) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
-       i += (i64)gridDim.x * blockDim.x)
-    flag[i] = within_eps(cand, i, px, py, qx, qy, eps_sq) ? 1u : 0u;
-}
-
-__global__ void k_refine_compact(const i64* __restrict__ cand, i64 n,
-                                 const u32* __restrict__ flag, const u64* __restrict__ base,
-                                 const i64* __restrict__ p_ids, const i64* __restrict__ q_ids,
-                                 i64* __restrict__ out) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
-       i += (i64)gridDim.x * blockDim.x) {
-    if (flag[i]) {
-      const u64 o = base[i];
-      out[2 * o] = p_ids[cand[2 * i]];
-      out[2 * o + 1] = q_ids[cand[2 * i + 1]];
-    }
-  }
 }
 
 // header → page-locked host memory (see pbsm_read_header)

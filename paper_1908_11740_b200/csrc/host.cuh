@@ -104,7 +104,7 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
                 const pbsm_entry* r_list, const pbsm_entry* s_list, const pbsm_header* plan,
                 void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s,
                 i64 max_nested = -1, i64 max_other = -1, i64 cap_r = -1, i64 cap_s = -1,
-                i64 large_cap = 0, i64 max_tile = 0) {
+                i64 large_cap = 0, i64 max_tile = 0, int eps = 0, double eps_sq = 0.0) {
   int rc = set_smem_attrs();
   if (rc) return rc;
   const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
@@ -154,12 +154,20 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.g_cur_s = w.cur_s;
   A.g_end_s = w.cnt_s;
   A.g_tiles = fused_guard ? L.tiles : 0;
+  A.eps = eps;
+  A.eps_sq = eps_sq;
   if (cn > 0) {
     // one CTA per chunk (the ordered look-back takes tickets in launch order)
-    if (emit)
-      k_join_nested<true><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
-    else
-      k_join_nested<false><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+    if (eps) {
+      if (emit)
+        k_join_nested<true, true><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+      else
+        k_join_nested<false, true><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+    } else if (emit) {
+      k_join_nested<true, false><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+    } else {
+      k_join_nested<false, false><<<(unsigned)cn, kNT, 0, s>>>(A, cn);
+    }
   }
   if (rest > 0 && lcap > 0 && mtile > 0) {
     // huge tiles: window sort, merge passes, sorted copy (sweep.cuh); a CTA

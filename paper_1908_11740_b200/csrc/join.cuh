@@ -29,7 +29,24 @@ struct JoinArgs {
   // the counted ends, every tile (partition.py:229-233)
   const u32 *g_cur_r, *g_end_r, *g_cur_s, *g_end_s;
   u64 g_tiles;
+  // ε-distance join (engine.py:201-206 fused into the mini-joins): a pair of
+  // squares is kept only if its points, carried in the entries' pad words,
+  // are within sqrt(eps_sq); eps = 0: plain join
+  int eps;
+  double eps_sq;
 };
+
+// _refine_pairs (engine.py:201-206): dx*dx + dy*dy <= eps^2, every operation
+// rounded on its own (numpy: no FMA contraction).  Symmetric in a, b: IEEE
+// a - b = -(b - a) exactly, and squares lose the sign.
+__device__ __forceinline__ bool within_eps(double2 a, double2 b, double eps_sq) {
+  const double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y);
+  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= eps_sq;
+}
+// the point {px, py} of an ε-join entry (pad[1], pad[2], see write_rec)
+__device__ __forceinline__ double2 rec_point(const Rec& r) {
+  return *reinterpret_cast<const double2*>(&r.pad[1]);
+}
 
 struct ChunkSmem {
   Rec recs[kCap];      // TMA landing zone: the chunk's R range then its S range
@@ -195,7 +212,8 @@ __device__ __forceinline__ void stage_chunk(Smem& S, const JoinArgs& A, int whic
 // x rule above leaves exactly the nine class combinations AA AB AC AD BA BC CA
 // CB DA.
 template <bool EMIT>
-__device__ __forceinline__ u32 sweep_one(const ChunkSmem& S, int p, i64* out) {
+__device__ __forceinline__ u32 sweep_one(const ChunkSmem& S, int p, i64* out, int eps,
+                                         double eps_sq) {
   const int lt = S.seg[p];
   const int rb = S.tR0[lt], sb = S.tS0[lt];
   const bool lead_r = p < sb;
@@ -229,9 +247,11 @@ __device__ __forceinline__ u32 sweep_one(const ChunkSmem& S, int p, i64* out) {
   u32 c = 0;
   i64 my_id = 0;
   if (EMIT) my_id = S.recs[S.sidx[p]].id;
+  const double2 mpt = eps ? rec_point(S.recs[S.sidx[p]]) : make_double2(0.0, 0.0);
   for (; k < hi; ++k) {
     if (S.sxl[k] > mxu) break;
-    if (myl <= S.syu[k] && S.syl[k] <= myu && (yme || S.syin[k])) {
+    if (myl <= S.syu[k] && S.syl[k] <= myu && (yme || S.syin[k]) &&
+        (!eps || within_eps(mpt, rec_point(S.recs[S.sidx[k]]), eps_sq))) {
       if (EMIT) {
         const i64 oid = S.recs[S.sidx[k]].id;
         *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
@@ -293,7 +313,7 @@ __device__ void join_sorted(ChunkSmem& S, const JoinArgs& A, i64 unit, int c) {
 
   // ---- 3/4: forward-scan mini-joins: count, look-back, emit
   u32 cnt = 0;
-  for (int p = tid; p < N; p += kJoinThreads) cnt += sweep_one<false>(S, p, nullptr);
+  for (int p = tid; p < N; p += kJoinThreads) cnt += sweep_one<false>(S, p, nullptr, A.eps, A.eps_sq);
   u64 total;
   const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
   if (!EMIT) {
@@ -308,7 +328,8 @@ __device__ void join_sorted(ChunkSmem& S, const JoinArgs& A, i64 unit, int c) {
     return;
   }
   i64* out = A.pairs + 2 * start;
-  for (int p = tid; p < N; p += kJoinThreads) out += 2 * (i64)sweep_one<true>(S, p, out);
+  for (int p = tid; p < N; p += kJoinThreads)
+    out += 2 * (i64)sweep_one<true>(S, p, out, A.eps, A.eps_sq);
 }
 
 // Large join tiles (|R_T|+|S_T| > kLmax): work items of kLargeLead entries of
@@ -320,7 +341,8 @@ __device__ void join_sorted(ChunkSmem& S, const JoinArgs& A, i64 unit, int c) {
 // hit list while it has room
 template <bool EMIT, bool LIST>
 __device__ __forceinline__ u32 large_pass(LargeSmem& S, int n, bool have, const Half& me,
-                                          bool lead_r, i64 my_id, i64* out, u32 k0) {
+                                          bool lead_r, i64 my_id, i64* out, u32 k0,
+                                          double2 mpt, int eps, double eps_sq) {
   u32 c = 0;
   if (!have) return 0;
   const double mxl = key_x(me.xl_key);
@@ -330,7 +352,8 @@ __device__ __forceinline__ u32 large_pass(LargeSmem& S, int n, bool have, const 
     const u64 ok = o.xl_key;
     const double oxl = key_x(ok);
     if (mxl <= o.xu && oxl <= me.xu && me.yl <= o.yu && o.yl <= me.yu &&
-        (mxin || !(ok & kXOut)) && (myin || !(ok & kYOut))) {
+        (mxin || !(ok & kXOut)) && (myin || !(ok & kYOut)) &&
+        (!eps || within_eps(mpt, rec_point(o), eps_sq))) {
       if (EMIT) {
         *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
             lead_r ? make_longlong2(my_id, o.id) : make_longlong2(o.id, my_id);
@@ -364,9 +387,11 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item, 
   const bool have = a < nl;
   Half me;
   i64 my_id = 0;
+  double2 mpt = make_double2(0.0, 0.0);
   if (have) {
     me = *reinterpret_cast<const Half*>(L + a);
     my_id = L[a].id;
+    if (A.eps) mpt = rec_point(L[a]);
   }
   if (tid == 0) {
     mbar_init(&S.bar, 1);
@@ -390,9 +415,11 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item, 
       mbar_wait(&S.bar, phase);
       phase ^= 1u;
       if (pass == 0) {
-        cnt += large_pass<false, EMIT>(S, n, have, me, lead_r, my_id, nullptr, ob - o_beg);
+        cnt += large_pass<false, EMIT>(S, n, have, me, lead_r, my_id, nullptr, ob - o_beg, mpt,
+                                       A.eps, A.eps_sq);
       } else if (ok) {
-        out += 2 * (i64)large_pass<true, false>(S, n, have, me, lead_r, my_id, out, 0);
+        out += 2 * (i64)large_pass<true, false>(S, n, have, me, lead_r, my_id, out, 0, mpt,
+                                                A.eps, A.eps_sq);
       }
     }
     if (pass == 0) {
@@ -661,7 +688,8 @@ __device__ __forceinline__ void nested_check(const JoinArgs& A, NestedChunk& k) 
 
 // all threads: async copies of the chunk's entries (coords + id; the pad is
 // skipped) and tile records into B
-__device__ __forceinline__ void nested_stage(NestedBuf& B, const JoinArgs& A,
+template <bool EPS>
+__device__ __forceinline__ void nested_stage(NestedBuf& B, double2* ap, const JoinArgs& A,
                                              const NestedChunk& k) {
   const int N = k.NR + k.NS;
   for (int e = threadIdx.x; e < N; e += kNT) {
@@ -670,6 +698,7 @@ __device__ __forceinline__ void nested_stage(NestedBuf& B, const JoinArgs& A,
     cp_async16(&B.ax[e], g);
     cp_async16(&B.ay[e], g + 16);
     cp_async8(&B.aid[e], g + 32);
+    if (EPS) cp_async16(&ap[e], g + 48);  // the point (pad[1], pad[2])
   }
   for (int t = threadIdx.x; t < k.nt; t += kNT) cp_async16(&B.jr[t], A.jrec[0] + k.d0.x + t);
 }
@@ -679,8 +708,9 @@ __device__ __forceinline__ void nested_stage(NestedBuf& B, const JoinArgs& A,
 // |R_T|*|S_T| <= 1024; <= 64 for any nested tile, |R_T|+|S_T| <= 128).  No per-pair index arithmetic; a warp runs max(|other|)
 // steps over its 32 lead entries.  body(hit, pr, ps, ballot) is called by
 // every lane of every step.
-template <typename Body>
-__device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf& B, u32 e_beg,
+template <bool EPS, typename Body>
+__device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf& B,
+                                            const double2* ap, double eps_sq, u32 e_beg,
                                             u32 e_end, u32 e_step, int lane, Body&& body) {
   for (u32 g = e_beg; g < e_end; g += e_step) {
     const u32 ei = g + lane;
@@ -691,6 +721,7 @@ __device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf
     const ulonglong2 mx = B.ax[pos];
     const double2 my = B.ay[pos];
     const double mxu = __longlong_as_double((long long)mx.y);
+    const double2 mp = EPS ? ap[pos] : make_double2(0.0, 0.0);
     const u32 steps = __reduce_max_sync(0xffffffffu, nO);
     for (u32 j = 0; j < steps; ++j) {
       bool hit = false;
@@ -699,6 +730,7 @@ __device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf
         const double2 oy = B.ay[o0 + j];
         hit = pair_ok(mx.x, mxu, my.x, my.y, ox.x, __longlong_as_double((long long)ox.y), oy.x,
                       oy.y);
+        if (EPS) hit = hit && within_eps(mp, ap[o0 + j], eps_sq);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       body(hit, lr ? pos : o0 + j, lr ? o0 + j : pos, m);
@@ -708,8 +740,9 @@ __device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf
 
 // Pair-flattened form (PBSM_NESTED_ROWS=0): every (r, s) pair of every tile
 // gets an index (tile-major, then r, then s); lane q of a warp-step tests pair q.
-template <typename Body>
-__device__ __forceinline__ void nested_flat(const NestedSmem& S, const NestedBuf& B, int nt,
+template <bool EPS, typename Body>
+__device__ __forceinline__ void nested_flat(const NestedSmem& S, const NestedBuf& B,
+                                            const double2* ap, double eps_sq, int nt,
                                             u32 q_beg, u32 q_end, int lt, int lane,
                                             Body&& body) {
   for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
@@ -720,15 +753,17 @@ __device__ __forceinline__ void nested_flat(const NestedSmem& S, const NestedBuf
     if (q < q_end) {
       nested_pair(S, t, q, pr, ps);
       hit = nested_hit(B, pr, ps);
+      if (EPS) hit = hit && within_eps(ap[pr], ap[ps], eps_sq);
     }
     body(hit, (u32)pr, (u32)ps, __ballot_sync(0xffffffffu, hit));
   }
 }
 
 // One staged chunk (B landed and visible): tables, count, reserve, emit.
-template <bool EMIT>
+template <bool EMIT, bool EPS>
 __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
-                                             const JoinArgs& A, const NestedChunk& k, i64 c) {
+                                             const double2* ap, const JoinArgs& A,
+                                             const NestedChunk& k, i64 c) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = k.nt, NR = k.NR;
   constexpr int kTPT = (kMaxTilesN + kNT - 1) / kNT;
@@ -787,8 +822,8 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     }
     wcnt += __popc(m);
   };
-  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, 32u * kW, lane, count);
-  else nested_flat(S, B, nt, w_beg, w_end, lt_beg, lane, count);
+  if (PBSM_NESTED_ROWS) nested_rows<EPS>(S, B, ap, A.eps_sq, w_beg, w_end, 32u * kW, lane, count);
+  else nested_flat<EPS>(S, B, ap, A.eps_sq, nt, w_beg, w_end, lt_beg, lane, count);
   if (lane == 0) S.wtot[warp] = wcnt;
   __syncthreads();
   if (tid == 0) {
@@ -830,8 +865,8 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     }
     out += 2 * (i64)__popc(m);
   };
-  if (PBSM_NESTED_ROWS) nested_rows(S, B, w_beg, w_end, 32u * kW, lane, emit);
-  else nested_flat(S, B, nt, w_beg, w_end, lt_beg, lane, emit);
+  if (PBSM_NESTED_ROWS) nested_rows<EPS>(S, B, ap, A.eps_sq, w_beg, w_end, 32u * kW, lane, emit);
+  else nested_flat<EPS>(S, B, ap, A.eps_sq, nt, w_beg, w_end, lt_beg, lane, emit);
 }
 
 // One CTA per chunk (chunks handed out by ticket in the ordered mode, whose
@@ -839,12 +874,14 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
 // addresses it with constant offsets.  (A persistent variant that staged chunk
 // i+1 with cp.async while joining chunk i was measured slower twice: more
 // resident CTAs beat the deeper pipeline.)
-template <bool EMIT>
+template <bool EMIT, bool EPS>
 #ifndef PBSM_NESTED_MINB
 #define PBSM_NESTED_MINB (1536 / kNT)
 #endif
-__global__ void __launch_bounds__(kNT, PBSM_NESTED_MINB) k_join_nested(JoinArgs A, i64 n_chunks) {
+__global__ void __launch_bounds__(kNT, EPS ? 4 : PBSM_NESTED_MINB) k_join_nested(JoinArgs A,
+                                                                          i64 n_chunks) {
   __shared__ __align__(128) NestedSmem S;
+  __shared__ __align__(16) double2 s_pt[EPS ? kCapN : 1];  // ε-join: the entries' points
   if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
     bool bad = false;
     for (u64 t = blockIdx.x * (u64)kNT + threadIdx.x; t < A.g_tiles; t += (u64)gridDim.x * kNT)
@@ -864,10 +901,10 @@ __global__ void __launch_bounds__(kNT, PBSM_NESTED_MINB) k_join_nested(JoinArgs 
   if (c >= n_plan) return;
   if (A.bounded && lists_overflow(A)) return;
   nested_check(A, k);
-  nested_stage(S.buf, A, k);
+  nested_stage<EPS>(S.buf, s_pt, A, k);
   cp_async_wait_all();
   __syncthreads();
-  nested_chunk<EMIT>(S, S.buf, A, k, c);
+  nested_chunk<EMIT, EPS>(S, S.buf, s_pt, A, k, c);
 }
 
 template <bool EMIT>
@@ -907,7 +944,15 @@ __global__ void __launch_bounds__(kJoinThreads, PBSM_JOIN_MINB) k_join(JoinArgs 
       hi = min(hi, lo + step);
     }
     const uint4 rec = A.lrec[lo];
-    if (is_huge(rec.z, rec.w, smin)) join_sweep<EMIT>(U.w, A, unit, item, lo, rec);
-    else join_large<EMIT>(U.l, A, unit, item, lo, rec);
+    if (is_huge(rec.z, rec.w, smin)) {
+      // (an ε-join's plan has no huge tiles: the sorted copies carry no points)
+      if (A.eps) {
+        if (threadIdx.x == 0) atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
+        return;
+      }
+      join_sweep<EMIT>(U.w, A, unit, item, lo, rec);
+    } else {
+      join_large<EMIT>(U.l, A, unit, item, lo, rec);
+    }
   }
 }

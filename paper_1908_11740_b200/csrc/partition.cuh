@@ -106,6 +106,32 @@ __device__ __forceinline__ u32 cur_inc(u32* p) {
 #endif
 }
 
+// Points mode (PTS, the ε-distance join): the input is the point columns
+// px = xl, py = yl only (xu, yu unused) and each rectangle is the side-ε square
+// around its point, clip(p ∓ half, 0, 1) — computed here with the reference's
+// numpy arithmetic (engine.py:342-350), never materialised.
+__device__ __forceinline__ double clip01(double v) { return fmin(fmax(v, 0.0), 1.0); }
+template <bool PTS>
+__device__ __forceinline__ void load_mbr(const double* __restrict__ xl,
+                                         const double* __restrict__ xu,
+                                         const double* __restrict__ yl,
+                                         const double* __restrict__ yu, i64 i, double half,
+                                         double& a, double& b, double& c, double& d) {
+  if (PTS) {
+    const double px = __ldcs(xl + i), py = __ldcs(yl + i);
+    a = clip01(__dsub_rn(px, half));
+    b = clip01(__dadd_rn(px, half));
+    c = clip01(__dsub_rn(py, half));
+    d = clip01(__dadd_rn(py, half));
+  } else {
+    a = __ldcs(xl + i);
+    b = __ldcs(xu + i);
+    c = __ldcs(yl + i);
+    d = __ldcs(yu + i);
+  }
+}
+
+template <bool PTS>
 __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __restrict__ xl,
                                                const double* __restrict__ xu,
                                                const double* __restrict__ yl,
@@ -115,7 +141,7 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
                                                const double* __restrict__ by,
                                                u32* __restrict__ cnt, int side,
                                                u32* __restrict__ band_cnt,
-                                               pbsm_header* hdr) {
+                                               pbsm_header* hdr, double half) {
   __shared__ u32 hist[kBinSlots];
   for (int g = threadIdx.x; g < kBinSlots; g += blockDim.x) hist[g] = 0;
   __syncthreads();
@@ -126,21 +152,11 @@ __global__ void __launch_bounds__(256, PBSM_PART_MINB) k_count(const double* __r
   // software pipeline: the next rectangle's loads are in flight while this
   // one is binned (streamed once: evict-first keeps the counters in L2)
   double a = 0, b = 0, c = 0, d = 0;
-  if (i < end) {
-    a = __ldcs(xl + i);
-    b = __ldcs(xu + i);
-    c = __ldcs(yl + i);
-    d = __ldcs(yu + i);
-  }
+  if (i < end) load_mbr<PTS>(xl, xu, yl, yu, i, half, a, b, c, d);
   for (; i < end; i += blockDim.x) {
     const i64 nx = i + blockDim.x;
     double na = 0, nb = 0, nc = 0, nd = 0;
-    if (nx < end) {
-      na = __ldcs(xl + nx);
-      nb = __ldcs(xu + nx);
-      nc = __ldcs(yl + nx);
-      nd = __ldcs(yu + nx);
-    }
+    if (nx < end) load_mbr<PTS>(xl, xu, yl, yu, nx, half, na, nb, nc, nd);
     if (!(a <= b) || !(c <= d)) bad |= PBSM_ERR_INVERTED;
     if (a < 0.0 || c < 0.0 || b > 1.0 || d > 1.0) bad |= PBSM_ERR_RANGE;
     const int c0 = tile_of(a, kx, bx);
@@ -317,11 +333,13 @@ __device__ __forceinline__ void st256_hint(void* p, u64 a, u64 b, u64 c, u64 d, 
 #endif
 }
 
+// pt = the point {px, py} bits of an ε-join entry (pad[1], pad[2]: one
+// 16-byte-aligned pair the join stages with the rest), else zero
 __device__ __forceinline__ void write_rec(Rec* r, u64 key, double xu, double yl, double yu,
-                                          i64 id, u64 pol) {
+                                          i64 id, u64 pol, ulonglong2 pt) {
   st256_hint(r, key, (u64)__double_as_longlong(xu), (u64)__double_as_longlong(yl),
              (u64)__double_as_longlong(yu), pol);
-  st256_hint(&r->id, (u64)id, 0ull, 0ull, 0ull, pol);
+  st256_hint(&r->id, (u64)id, 0ull, pt.x, pt.y, pol);
 }
 
 // write_tiles (_kernels.pyx:61-98): copy each rectangle into every tile it
@@ -334,10 +352,19 @@ struct ScatterIn {
   const i64* ids;
   const double *xl, *xu, *yl, *yu;
   const BRec* band;  // non-null: read the row-band copy instead
-  template <bool BANDED>
+  double half;       // points mode: square half-side (see load_mbr)
+  template <bool BANDED, bool PTS>
   __device__ __forceinline__ void load(i64 i, double& a, double& b, double& c, double& d,
-                                       i64& id) const {
-    if (BANDED) {
+                                       i64& id, ulonglong2& pt) const {
+    if (PTS) {
+      id = ids ? __ldcs(ids + i) : i;
+      const double px = __ldcs(xl + i), py = __ldcs(yl + i);
+      pt = make_ulonglong2((u64)__double_as_longlong(px), (u64)__double_as_longlong(py));
+      a = clip01(__dsub_rn(px, half));
+      b = clip01(__dadd_rn(px, half));
+      c = clip01(__dsub_rn(py, half));
+      d = clip01(__dadd_rn(py, half));
+    } else if (BANDED) {
       const BRec* r = band + i;
       id = __ldcs(&r->id);
       a = __ldcs(&r->xl);
@@ -356,7 +383,7 @@ struct ScatterIn {
 
 // 5 resident CTAs per SM measured best for the SoA input (cfg3: 4.77 vs 4.91
 // ms at 4), 4 for the 40-byte band records (cfg4: 6.65 vs 7.02 ms at 5)
-template <bool BANDED>
+template <bool BANDED, bool PTS>
 #ifndef PBSM_SCAT_MINB
 #define PBSM_SCAT_MINB 5
 #endif
@@ -372,11 +399,13 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
   i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   double pa = 0, pb = 0, pc = 0, pd = 0;
   i64 pid = 0;
-  if (i < n) in.load<BANDED>(i, pa, pb, pc, pd, pid);  // software pipeline: next one in flight
+  ulonglong2 ppt = make_ulonglong2(0ull, 0ull);
+  if (i < n) in.load<BANDED, PTS>(i, pa, pb, pc, pd, pid, ppt);  // software pipeline: next one in flight
   for (; i < n; i += stride) {
     const double a = pa, b = pb, c = pc, d = pd;
     const i64 id = pid;
-    if (i + stride < n) in.load<BANDED>(i + stride, pa, pb, pc, pd, pid);
+    const ulonglong2 pt = ppt;
+    if (i + stride < n) in.load<BANDED, PTS>(i + stride, pa, pb, pc, pd, pid, ppt);
     const int c0 = tile_of(a, kx, bx);
     const int c1 = tile_of(b, kx, bx);
     const int rr0 = tile_of(c, ky, by);
@@ -388,7 +417,7 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
     if (nc * nr == 1) {  // one tile: most rectangles
       const u32 p = cur_inc(cursor + (size_t)(r0 - row_lo) * kx + c0);
       if (p < kSkip) {
-        if ((i64)p < capacity) write_rec(out + p, xk | ((r0 != rr0) ? kYOut : 0ull), b, c, d, id, pol);
+        if ((i64)p < capacity) write_rec(out + p, xk | ((r0 != rr0) ? kYOut : 0ull), b, c, d, id, pol, pt);
         else bad |= PBSM_ERR_SCATTER_OVERFLOW;
       }
       continue;
@@ -428,7 +457,7 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
           continue;
         }
         const u64 key = xk | ((rows[q] != rr0) ? kYOut : 0ull) | ((cols[q] != c0) ? kXOut : 0ull);
-        write_rec(out + pos[q], key, b, c, d, id, pol);
+        write_rec(out + pos[q], key, b, c, d, id, pol, pt);
       }
       continue;
     }
@@ -442,7 +471,7 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
           bad |= PBSM_ERR_SCATTER_OVERFLOW;
           continue;
         }
-        write_rec(out + p, xk | ylab | ((col != c0) ? kXOut : 0ull), b, c, d, id, pol);
+        write_rec(out + p, xk | ylab | ((col != c0) ? kXOut : 0ull), b, c, d, id, pol, pt);
       }
     }
   }

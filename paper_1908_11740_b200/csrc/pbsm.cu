@@ -73,6 +73,7 @@ namespace {
 #include "join.cuh"
 #include "extras.cuh"
 #include "host.cuh"
+#include "dist.cuh"
 #include "units.cuh"
 
 }  // namespace
@@ -115,10 +116,26 @@ int pbsm_count(const double* xl, const double* xu, const double* yl, const doubl
   if (n == 0) return 0;
   if (!xl || !xu || !yl || !yu) return PBSM_E_ARG;
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
-  k_count<<<part_blocks(n), 256, 0, as_stream(stream)>>>(xl, xu, yl, yu, n, kx, ky, row_lo,
-                                                         row_hi, w.bx, w.by,
-                                                         side ? w.cnt_s : w.cnt_r, side,
-                                                         w.bc[side], w.hdr);
+  k_count<false><<<part_blocks(n), 256, 0, as_stream(stream)>>>(xl, xu, yl, yu, n, kx, ky,
+                                                                row_lo, row_hi, w.bx, w.by,
+                                                                side ? w.cnt_s : w.cnt_r, side,
+                                                                w.bc[side], w.hdr, 0.0);
+  return launch_status();
+}
+
+int pbsm_count_points(const double* px, const double* py, int64_t n, int32_t side, double half,
+                      void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                      void* stream) {
+  if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1) ||
+      !(half > 0.0))
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!px || !py) return PBSM_E_ARG;
+  Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
+  k_count<true><<<part_blocks(n), 256, 0, as_stream(stream)>>>(px, nullptr, py, nullptr, n, kx,
+                                                               ky, row_lo, row_hi, w.bx, w.by,
+                                                               side ? w.cnt_s : w.cnt_r, side,
+                                                               w.bc[side], w.hdr, half);
   return launch_status();
 }
 
@@ -171,21 +188,26 @@ int pbsm_read_header(void* ws, pbsm_header* out, void* stream) {
 static int scatter_impl(const int64_t* ids, const double* xl, const double* xu,
                         const double* yl, const double* yu, const void* band, int64_t n,
                         int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
-                        int32_t row_hi, pbsm_entry* out, int64_t capacity, void* stream) {
+                        int32_t row_hi, pbsm_entry* out, int64_t capacity, void* stream,
+                        double half = 0.0) {
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
 #ifndef PBSM_SCAT_GRID
 #define PBSM_SCAT_GRID 32  // blocks per SM (swept 8-1000 on cfg2/cfg3: 32 best)
 #endif
   const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * PBSM_SCAT_GRID);
-  ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band)};
-  if (band)
-    k_scatter<true><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
-        in, n, kx, ky, row_lo, row_hi, w.bx, w.by, side ? w.cur_s : w.cur_r,
-        reinterpret_cast<Rec*>(out), capacity, w.hdr);
+  ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band), half};
+  u32* cur = side ? w.cur_s : w.cur_r;
+  Rec* o = reinterpret_cast<Rec*>(out);
+  cudaStream_t s = as_stream(stream);
+  if (half > 0.0)
+    k_scatter<false, true><<<(unsigned)blocks, 256, 0, s>>>(in, n, kx, ky, row_lo, row_hi, w.bx,
+                                                            w.by, cur, o, capacity, w.hdr);
+  else if (band)
+    k_scatter<true, false><<<(unsigned)blocks, 256, 0, s>>>(in, n, kx, ky, row_lo, row_hi, w.bx,
+                                                            w.by, cur, o, capacity, w.hdr);
   else
-    k_scatter<false><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
-        in, n, kx, ky, row_lo, row_hi, w.bx, w.by, side ? w.cur_s : w.cur_r,
-        reinterpret_cast<Rec*>(out), capacity, w.hdr);
+    k_scatter<false, false><<<(unsigned)blocks, 256, 0, s>>>(in, n, kx, ky, row_lo, row_hi,
+                                                             w.bx, w.by, cur, o, capacity, w.hdr);
   return launch_status();
 }
 
@@ -200,6 +222,19 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu, const d
   if (!xl || !xu || !yl || !yu || (!out && capacity > 0)) return PBSM_E_ARG;
   return scatter_impl(ids, xl, xu, yl, yu, nullptr, n, side, ws, kx, ky, row_lo, row_hi, out,
                       capacity, stream);
+}
+
+int pbsm_scatter_points(const int64_t* ids, const double* px, const double* py, int64_t n,
+                        int32_t side, double half, void* ws, int32_t kx, int32_t ky,
+                        int32_t row_lo, int32_t row_hi, pbsm_entry* out, int64_t capacity,
+                        void* stream) {
+  if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1) ||
+      capacity < 0 || !(half > 0.0))
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!px || !py || (!out && capacity > 0)) return PBSM_E_ARG;
+  return scatter_impl(ids, px, nullptr, py, nullptr, nullptr, n, side, ws, kx, ky, row_lo,
+                      row_hi, out, capacity, stream, half);
 }
 
 int pbsm_scatter_banded(const void* band, int64_t n, int32_t side, void* ws, int32_t kx,
@@ -274,15 +309,31 @@ int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int
                      r_capacity, s_capacity, large_capacity, max_tile);
 }
 
-int64_t pbsm_refine_scratch_bytes(int64_t n_cand) {
-  if (n_cand < 0) return PBSM_E_ARG;
-  return (int64_t)scan_layout(n_cand).total;
+// ε-distance join: the plan must hold no huge (sorted + swept) tiles, whose
+// sorted copies carry no points — pbsm_plan with sweep_min = INT64_MAX
+static bool eps_ok(const pbsm_header* plan, double eps_sq) {
+  return plan && plan->max_huge == 0 && eps_sq >= 0.0;
 }
 
-int64_t pbsm_refine_result_offset(int64_t n_cand) {
-  if (n_cand < 0) return PBSM_E_ARG;
-  const ScanLayout SL = scan_layout(n_cand);
-  return (int64_t)(SL.base + 8 * SL.n);
+int pbsm_join_count_eps(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                        const pbsm_entry* r_list, const pbsm_entry* s_list,
+                        const pbsm_header* plan, void* scratch, double eps_sq, void* stream) {
+  if (!ws || !scratch || !eps_ok(plan, eps_sq) || !grid_ok(kx, ky, row_lo, row_hi))
+    return PBSM_E_ARG;
+  return launch_join(false, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan, scratch,
+                     nullptr, 0, as_stream(stream), -1, -1, -1, -1, 0, 0, 1, eps_sq);
+}
+
+int pbsm_join_emit_eps(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                       const pbsm_entry* r_list, const pbsm_entry* s_list,
+                       const pbsm_header* plan, void* scratch, int64_t* pairs,
+                       int64_t capacity, int32_t ordered, double eps_sq, void* stream) {
+  if (!ws || !scratch || !eps_ok(plan, eps_sq) || !grid_ok(kx, ky, row_lo, row_hi) ||
+      capacity < 0 || (capacity > 0 && !pairs))
+    return PBSM_E_ARG;
+  return launch_join(true, ordered != 0, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan,
+                     scratch, pairs, capacity, as_stream(stream), -1, -1, -1, -1, 0, 0, 1,
+                     eps_sq);
 }
 
 int pbsm_map_ids(int64_t* pairs, int64_t n, const int64_t* r_ids, const int64_t* s_ids,
@@ -327,27 +378,102 @@ int pbsm_unpack_records(const void* records, int64_t n, int64_t* ids, double* xl
   return launch_status();
 }
 
-int pbsm_refine(const int64_t* cand, int64_t n_cand, const double* px, const double* py,
-                const double* qx, const double* qy, const int64_t* p_ids, const int64_t* q_ids,
-                double eps_sq, void* scratch, int64_t* out, void* stream) {
-  if (n_cand < 0 || !scratch) return PBSM_E_ARG;
-  const ScanLayout SL = scan_layout(n_cand);
+// ------------------------------------------------------------ strip routing
+int64_t pbsm_route_scratch_bytes(int64_t n, int32_t ky, int32_t world) {
+  if (n < 0 || ky < 1 || ky > 65535 || world < 1 || world > kMaxRanks) return PBSM_E_ARG;
+  return (int64_t)route_layout(n, ky, world).total;
+}
+
+int pbsm_route_count(const double* yl, const double* yu, int64_t n, int32_t ky,
+                     const int32_t* cuts, int32_t world, void* scratch, int64_t* dest_counts,
+                     void* stream) {
+  if (n < 0 || ky < 1 || ky > 65535 || world < 1 || world > kMaxRanks || !cuts || !scratch ||
+      !dest_counts)
+    return PBSM_E_ARG;
   cudaStream_t s = as_stream(stream);
-  u64* base = (u64*)((char*)scratch + SL.base);
-  if (n_cand == 0) {
-    cudaMemsetAsync(base, 0, sizeof(u64), s);
-    return launch_status();
+  const RouteLayout L = route_layout(n, ky, world);
+  char* b = (char*)scratch;
+  double* by = (double*)(b + L.by);
+  u32* cnt = (u32*)(b + L.cnt);
+  u64* base = (u64*)(b + L.base);
+  u64* part = (u64*)(b + L.part);
+  k_bounds<<<(unsigned)((ky + 256) / 256), 256, 0, s>>>(by, ky);
+  if (n > 0) {
+    if (!yl || !yu) return PBSM_E_ARG;
+    k_route<false><<<(unsigned)L.nb, kRouteThreads, 0, s>>>(nullptr, nullptr, nullptr, yl, yu, n,
+                                                            ky, by, cuts, world, cnt, nullptr,
+                                                            nullptr);
+  } else {
+    cudaMemsetAsync(cnt, 0, 4 * L.m, s);
   }
-  if (!cand || !px || !py || !qx || !qy || !p_ids || !q_ids || !out) return PBSM_E_ARG;
-  u32* flag = (u32*)((char*)scratch + SL.cnt);
-  u64* part = (u64*)((char*)scratch + SL.partials);
-  const unsigned blocks = (unsigned)std::min<i64>((n_cand + 255) / 256, (i64)num_sms() * 16);
-  k_refine_flag<<<blocks, 256, 0, s>>>((const i64*)cand, n_cand, px, py, qx, qy, eps_sq, flag);
-  k_scan_reduce<<<(unsigned)SL.nb, kScanThreads, 0, s>>>(flag, SL.n, part);
-  k_scan_partials<<<1, 1024, 0, s>>>(part, SL.nb, base, SL.n);
-  k_scan_apply<<<(unsigned)SL.nb, kScanThreads, 0, s>>>(flag, SL.n, part, base);
-  k_refine_compact<<<blocks, 256, 0, s>>>((const i64*)cand, n_cand, flag, base,
-                                          (const i64*)p_ids, (const i64*)q_ids, (i64*)out);
+  const u64 sb = (L.m + kScanTile - 1) / kScanTile;
+  k_scan_reduce<<<(unsigned)sb, kScanThreads, 0, s>>>(cnt, L.m, part);
+  k_scan_partials<<<1, 1024, 0, s>>>(part, sb, base, L.m);
+  k_scan_apply<<<(unsigned)sb, kScanThreads, 0, s>>>(cnt, L.m, part, base);
+  k_route_totals<<<(unsigned)((world + 255) / 256), 256, 0, s>>>(base, L.nb, world, L.m,
+                                                                 (i64*)dest_counts);
+  return launch_status();
+}
+
+int pbsm_route_pack(const int64_t* ids, const double* xl, const double* xu, const double* yl,
+                    const double* yu, int64_t n, int32_t ky, const int32_t* cuts, int32_t world,
+                    void* scratch, void* records, void* stream) {
+  if (n < 0 || ky < 1 || ky > 65535 || world < 1 || world > kMaxRanks || !cuts || !scratch)
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!xl || !xu || !yl || !yu || !records || ((uintptr_t)records & 7u)) return PBSM_E_ARG;
+  const RouteLayout L = route_layout(n, ky, world);
+  char* b = (char*)scratch;
+  k_route<true><<<(unsigned)L.nb, kRouteThreads, 0, as_stream(stream)>>>(
+      (const i64*)ids, xl, xu, yl, yu, n, ky, (const double*)(b + L.by), cuts, world, nullptr,
+      (const u64*)(b + L.base), (u64*)records);
+  return launch_status();
+}
+
+// ------------------------------------------------------------ pair sort
+int64_t pbsm_sort_pairs_scratch_bytes(int64_t n) {
+  if (n < 0) return PBSM_E_ARG;
+  return (int64_t)pair_sort_layout(n).total;
+}
+
+int pbsm_pair_digits(const int64_t* pairs, int64_t n, uint32_t* hist, void* stream) {
+  if (n < 0 || !hist) return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(hist, 0, 4 * 16 * 256, s);
+  if (n == 0) return launch_status();
+  if (!pairs || ((uintptr_t)pairs & 15u)) return PBSM_E_ARG;
+  const unsigned blocks = (unsigned)std::max<i64>(1, std::min<i64>((n + 4095) / 4096,
+                                                                   (i64)num_sms() * 4));
+  k_pair_digits<<<blocks, kSortT, 0, s>>>((const ulonglong2*)pairs, n, hist);
+  return launch_status();
+}
+
+int pbsm_sort_pairs(int64_t* pairs, int64_t n, uint32_t pass_mask, void* tmp, void* scratch,
+                    void* stream) {
+  if (n < 0) return PBSM_E_ARG;
+  if (n <= 1 || (pass_mask & 0xffffu) == 0) return 0;
+  if (!pairs || !tmp || !scratch || ((uintptr_t)pairs & 15u) || ((uintptr_t)tmp & 15u))
+    return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  const PairSortLayout L = pair_sort_layout(n);
+  char* b = (char*)scratch;
+  u32* cnt = (u32*)(b + L.cnt);
+  u64* base = (u64*)(b + L.base);
+  u64* part = (u64*)(b + L.part);
+  const u64 sb = (L.m + kScanTile - 1) / kScanTile;
+  ulonglong2* src = (ulonglong2*)pairs;
+  ulonglong2* dst = (ulonglong2*)tmp;
+  for (int d = 0; d < 16; ++d) {
+    if (!((pass_mask >> d) & 1u)) continue;
+    k_pair_count<<<(unsigned)L.nb, kSortT, 0, s>>>(src, n, d, cnt);
+    k_scan_reduce<<<(unsigned)sb, kScanThreads, 0, s>>>(cnt, L.m, part);
+    k_scan_partials<<<1, 1024, 0, s>>>(part, sb, base, L.m);
+    k_scan_apply<<<(unsigned)sb, kScanThreads, 0, s>>>(cnt, L.m, part, base);
+    k_pair_scatter<<<(unsigned)L.nb, kSortT, 0, s>>>(src, dst, n, d, base);
+    std::swap(src, dst);
+  }
+  if (src != (ulonglong2*)pairs)
+    cudaMemcpyAsync(pairs, src, 16 * (size_t)n, cudaMemcpyDeviceToDevice, s);
   return launch_status();
 }
 

@@ -26,7 +26,7 @@ from . import _native
 from .errors import KernelError
 
 __all__ = ["DeviceRects", "DeviceJoinResult", "PhaseProbe", "release_buffers", "run_join",
-           "to_device", "to_device_pipelined"]
+           "points_to_device", "to_device", "to_device_pipelined"]
 
 
 @dataclass
@@ -56,6 +56,21 @@ class DeviceRects:
 
     def columns(self):
         return self.ids, self.xl, self.xu, self.yl, self.yu
+
+
+def points_to_device(batch, device="cuda") -> DeviceRects:
+    """The point columns of an ε-distance join — ids and the lower corners
+    (xl, yl) of a ``RectBatch`` (engine.py:333-334) — on the GPU; the square
+    around each point is computed inside the kernels (pbsm_count_points).
+    ``xu`` / ``yu`` alias ``xl`` / ``yl`` and are never read."""
+    cols = []
+    for a, dt in ((batch.ids, torch.int64), (batch.xl, torch.float64), (batch.yl, torch.float64)):
+        cols.append(_host_tensor(a, dt, True).to(device, non_blocking=True))
+    ids, px, py = cols
+    return DeviceRects(ids, px, px, py, py)
+
+
+INT64_MAX = (1 << 63) - 1
 
 
 def to_device(batch, device="cuda", pinned: bool = True) -> DeviceRects:
@@ -542,7 +557,8 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
              keep_counts: bool = False, probe: PhaseProbe | None = None,
              ordered: bool = False, nested_max: int = -1,
              bin_bytes: int | None = None, defer_map: bool = False,
-             pipeline: str | None = None, sweep_min: int = -1) -> DeviceJoinResult:
+             pipeline: str | None = None, sweep_min: int = -1,
+             eps: float | None = None) -> DeviceJoinResult:
     """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
 
     Two device pipelines compute the same pair set: the tile-list pipeline
@@ -561,6 +577,10 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     ``defer_map``: with id columns still in flight (to_device_pipelined) the
     pairs are returned as row indices (``rows_pending``) for
     staged_pairs_to_host instead of being mapped here.
+    ``eps``: ε-distance join (epsilon_distance_join, engine.py:326-353) —
+    ``r``/``s`` hold points (``points_to_device``: xl, yl = px, py), each
+    standing for its side-eps square; candidates are refined inside the
+    mini-joins (pbsm_join_emit_eps), so the count is the refined count.
     """
     mark = probe.mark if probe is not None else (lambda name: None)
     lib = _native.load()
@@ -570,6 +590,12 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     if len(r) == 0 or len(s) == 0:
         empty = torch.empty((0, 2), dtype=torch.int64, device=device) if collect else None
         return DeviceJoinResult(0, empty)
+    half = eps_sq = None
+    if eps is not None:
+        # squares computed in the kernels; their entries carry the points, and
+        # no tile is sorted + swept (its sorted copy would not carry them)
+        half, eps_sq = eps / 2.0, eps * eps
+        sweep_min, bin_bytes, pipeline = INT64_MAX, INT64_MAX, "tiles"
     if (pipeline == "units" or (pipeline is None and UNITS)) and not ordered and not keep_counts \
             and nested_max == -1 and bin_bytes is None and sweep_min == -1 \
             and lib.pbsm_unit_supported(kx, ky, row_lo, row_hi) == 1:
@@ -609,8 +635,12 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     for side, b in ((0, r), (1, s)):
         _wait(b.coords_ready, cur)
         st_ = side_st.cuda_stream if (dual and side == 1) else stream
-        _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
-                                     side, wsp, *grid, st_), "pbsm_count")
+        if half is not None:
+            _native.check(lib.pbsm_count_points(_ptr(b.xl), _ptr(b.yl), len(b), side, half, wsp,
+                                                *grid, st_), "pbsm_count_points")
+        else:
+            _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
+                                         side, wsp, *grid, st_), "pbsm_count")
     if dual:
         join_ev = torch.cuda.Event()
         join_ev.record(side_st)
@@ -624,7 +654,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     key = (str(device), stream, kx, ky, row_lo, row_hi, len(r), len(s), s is r, nested_max,
            bin_bytes, sweep_min)
     guess = _plan_cache.get(key) if (SPECULATE and collect and not ordered
-                                     and not keep_counts) else None
+                                     and not keep_counts and eps is None) else None
     if guess is None:
         h = _read_header(lib, ws, stream)
         mark("header")
@@ -643,6 +673,19 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64,
                       stream)  # 64 B records
         ids_p = None if late else _ptr(b.ids)
+        if half is not None:
+            _native.check(lib.pbsm_scatter_points(ids_p, _ptr(b.xl), _ptr(b.yl), len(b), side,
+                                                  half, wsp, *grid, ent.data_ptr(), total,
+                                                  side_st.cuda_stream if (dual_sc and side)
+                                                  else stream), "pbsm_scatter_points")
+            if dual_sc and side == 1:
+                join_ev = torch.cuda.Event()
+                join_ev.record(side_st)
+                main_st.wait_event(join_ev)
+            if side == 1:
+                mark("scatter")
+            lists.append(ent)
+            continue
         if dual_sc:
             _native.check(lib.pbsm_scatter(ids_p, _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
                                            _ptr(b.yu), len(b), side, wsp, *grid, ent.data_ptr(),
@@ -697,7 +740,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
             return run_join(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
                             timing=timing, keep_counts=keep_counts, probe=probe,
                             ordered=ordered, nested_max=nested_max, bin_bytes=bin_bytes,
-                            defer_map=defer_map, pipeline="tiles", sweep_min=sweep_min)
+                            defer_map=defer_map, pipeline="tiles", sweep_min=sweep_min, eps=eps)
         count = int(h2.pairs)
         if late and not defer_map:
             _map_ids(lib, pairs, count, r, s, cur, stream)
@@ -718,8 +761,14 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                       torch.uint8, stream)
     pairs = None
     if not collect:
-        _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(), C.byref(h),
-                                          scratch.data_ptr(), stream), "pbsm_join_count")
+        if eps_sq is not None:
+            _native.check(lib.pbsm_join_count_eps(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
+                                                  C.byref(h), scratch.data_ptr(), eps_sq, stream),
+                          "pbsm_join_count_eps")
+        else:
+            _native.check(lib.pbsm_join_count(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
+                                              C.byref(h), scratch.data_ptr(), stream),
+                          "pbsm_join_count")
         mark("join")
         h2 = _read_header(lib, ws, stream)
         mark("header2")
@@ -728,9 +777,15 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         cap = pair_capacity(h)
         while True:
             pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
-            _native.check(lib.pbsm_join_emit(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
-                                             C.byref(h), scratch.data_ptr(), pairs.data_ptr(),
-                                             cap, int(ordered), stream), "pbsm_join_emit")
+            if eps_sq is not None:
+                _native.check(lib.pbsm_join_emit_eps(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
+                                                     C.byref(h), scratch.data_ptr(),
+                                                     pairs.data_ptr(), cap, int(ordered), eps_sq,
+                                                     stream), "pbsm_join_emit_eps")
+            else:
+                _native.check(lib.pbsm_join_emit(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
+                                                 C.byref(h), scratch.data_ptr(), pairs.data_ptr(),
+                                                 cap, int(ordered), stream), "pbsm_join_emit")
             mark("join")
             h2 = _read_header(lib, ws, stream, allow=_native.ERR_PAIR_OVERFLOW)
             mark("header2")
@@ -741,7 +796,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         pairs = pairs[:count]
         if late and not defer_map:
             _map_ids(lib, pairs, count, r, s, cur, stream)
-        if not ordered and not keep_counts:
+        if not ordered and not keep_counts and eps is None:
             with _state_lock:
                 for k_ in [k_ for k_ in _plan_cache if k_[:2] == key[:2]]:
                     del _plan_cache[k_]  # one shape per (device, stream)
@@ -761,6 +816,31 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
                      "total": ev[0].elapsed_time(ev[2]) / 1e3}
     res.tile_counts = counts
     return res
+
+
+def sort_pairs(pairs: torch.Tensor) -> torch.Tensor:
+    """(n, 2) int64 device pairs → a new tensor in lexicographic (r_id, s_id)
+    order: the stable LSD radix sort of pbsm_sort_pairs over the digits that
+    vary (one small histogram read decides which)."""
+    lib = _native.load()
+    n = int(pairs.shape[0])
+    out = pairs.contiguous().clone()
+    if n <= 1:
+        return out
+    device = pairs.device
+    stream = _raw_stream(device)
+    hist = torch.empty(16 * 256, dtype=torch.int32, device=device)
+    _native.check(lib.pbsm_pair_digits(out.data_ptr(), n, hist.data_ptr(), stream),
+                  "pbsm_pair_digits")
+    full = (hist.view(16, 256) == n).any(1).cpu().tolist()  # one bucket holds every key
+    mask = sum(1 << d for d in range(16) if not full[d])
+    if mask:
+        tmp = torch.empty_like(out)
+        scratch = torch.empty(int(lib.pbsm_sort_pairs_scratch_bytes(n)), dtype=torch.uint8,
+                              device=device)
+        _native.check(lib.pbsm_sort_pairs(out.data_ptr(), n, mask, tmp.data_ptr(),
+                                          scratch.data_ptr(), stream), "pbsm_sort_pairs")
+    return out
 
 
 def _map_ids(lib, pairs, count: int, r: DeviceRects, s: DeviceRects, cur, stream) -> None:

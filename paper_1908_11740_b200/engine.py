@@ -131,12 +131,17 @@ def _require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _task_sizes_fn(r: RectBatch, s: RectBatch, kx: int, ky: int):
+def _task_sizes_fn(r: RectBatch, s: RectBatch, kx: int, ky: int, eps: float | None = None):
     """Lazy task_sizes: the report keeps references to the caller's host
     batches only; on first read their coordinates go back to the device for
-    one count pass (pbsm_count) and the join tiles' sizes come back sorted."""
+    one count pass (pbsm_count; an ε-join's squares are built first) and the
+    join tiles' sizes come back sorted."""
     def compute():
-        cr, cs = dev.tile_counts(r, s, kx, ky)
+        if eps is not None:
+            sr = squares(r, eps)
+            cr, cs = dev.tile_counts(sr, sr if s is r else squares(s, eps), kx, ky)
+        else:
+            cr, cs = dev.tile_counts(r, s, kx, ky)
         both = (cr > 0) & (cs > 0)
         sizes = (cr + cs)[both]
         return -np.sort(-sizes, kind="stable")
@@ -151,24 +156,30 @@ def join_device(r: dev.DeviceRects, s: dev.DeviceRects, cfg: JoinConfig,
     return dev.run_join(r, s, kx, ky, collect=cfg.sink_mode == "collect-pairs", timing=timing)
 
 
-def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) -> JoinReport:
+def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float,
+         eps: float | None = None) -> JoinReport:
     collect_user = cfg.sink_mode == "collect-pairs"
     if len(r) == 0 or len(s) == 0:
         return JoinReport(0, np.empty((0, 2), dtype=np.int64) if collect_user else None,
                           0.0, 0.0, 0.0, time.perf_counter() - t0,
                           task_sizes=np.empty(0, dtype=np.int64))
     device = _require_cuda()
-    # column copies on a side stream, coordinates first: the count passes
-    # start while the ids are still in flight
-    rd, sd = dev.to_device_pipelined(r, s, device)
     kx, ky = cfg.layout.grid
-    # (plain joins: the pairs come back as row indices and go home group by
-    # group as the id chunks land, dev.staged_pairs_to_host)
-    res = dev.run_join(rd, sd, kx, ky, collect=collect_user or refine is not None, timing=True,
-                       defer_map=dev.STAGED and collect_user and refine is None)
+    if eps is not None:
+        # ε-join: only the point columns cross PCIe (the squares are built
+        # in the kernels, the distance test runs inside the mini-joins)
+        rd = dev.points_to_device(r, device)
+        sd = rd if s is r else dev.points_to_device(s, device)
+        res = dev.run_join(rd, sd, kx, ky, collect=collect_user, timing=True, eps=eps)
+    else:
+        # column copies on a side stream, coordinates first: the count passes
+        # start while the ids are still in flight; the pairs come back as row
+        # indices and go home group by group as the id chunks land
+        # (dev.staged_pairs_to_host)
+        rd, sd = dev.to_device_pipelined(r, s, device)
+        res = dev.run_join(rd, sd, kx, ky, collect=collect_user, timing=True,
+                           defer_map=dev.STAGED and collect_user)
     count, pairs = res.count, res.pairs
-    if refine is not None:
-        count, pairs = refine(res.pairs)
     out = None
     if collect_user:
         if res.rows_pending:
@@ -181,7 +192,7 @@ def _run(r: RectBatch, s: RectBatch, cfg: JoinConfig, t0: float, refine=None) ->
         partition_time=t.get("partition", 0.0), sort_time=0.0,
         join_time=t.get("join", 0.0),
         total_time=time.perf_counter() - t0,
-        task_sizes=_task_sizes_fn(r, s, kx, ky))
+        task_sizes=_task_sizes_fn(r, s, kx, ky, eps))
 
 
 def join(r: RectBatch | Sequence[Rect], s: RectBatch | Sequence[Rect],
@@ -216,9 +227,12 @@ def epsilon_distance_join(p: RectBatch | Sequence[Rect], q: RectBatch | Sequence
                           eps: float, cfg: JoinConfig) -> JoinReport:
     """Point pairs within distance ``eps`` exactly once (engine.py:326-353).
 
-    Candidates come from the square join; the distance test
-    ``dx*dx + dy*dy <= eps*eps`` runs on the device without FMA contraction
-    (numpy rounds every operation, engine.py:201-206).
+    The points are the lower corners of ``p`` / ``q`` (engine.py:333-334).
+    Candidates are the pairs whose side-``eps`` squares intersect (squares
+    built in the kernels with the reference's arithmetic, engine.py:342-350);
+    the distance test ``dx*dx + dy*dy <= eps*eps`` (numpy rounding, no FMA
+    contraction, engine.py:201-206) runs inside the mini-joins, in the count
+    pass and the emit alike, so only refined pairs are ever written.
     """
     if not eps > 0.0:
         raise ConfigError(f"epsilon must be positive, got {eps!r}")
@@ -226,12 +240,4 @@ def epsilon_distance_join(p: RectBatch | Sequence[Rect], q: RectBatch | Sequence
     _resolve_policy(cfg)
     p.validate()
     q.validate()
-    t0 = time.perf_counter()
-    sp = squares(p, eps)
-    sq = sp if q is p else squares(q, eps)
-
-    def refine(cand: torch.Tensor):
-        from .refine import refine_distance
-        return refine_distance(cand, p, q, eps * eps)
-
-    return _run(sp, sq, cfg, t0, refine=refine)
+    return _run(p, q, cfg, time.perf_counter(), eps=float(eps))

@@ -222,6 +222,89 @@ def tile_rows_torch(yl, yu, k: int):
     return idx(yl), idx(yu)
 
 
+def _route_host(cols, k: int, cuts):
+    """Host mirror of pbsm_route_count / pbsm_route_pack for CPU-resident
+    slices (gloo ranks without a GPU): the same destination-major SJB1
+    records {id, x_l, y_l, x_u, y_u} and per-destination counts."""
+    import torch
+
+    ids, xl, xu, yl, yu = (c.numpy() for c in cols)
+    r0, r1 = _tile_index(yl, k), _tile_index(yu, k)
+    c = np.asarray(cuts, dtype=np.int64)
+    g0 = np.searchsorted(c, r0, side="right") - 1
+    g1 = np.searchsorted(c, r1, side="right") - 1
+    world = len(cuts) - 1
+    parts, counts = [], []
+    for g in range(world):
+        m = (g0 <= g) & (g1 >= g)
+        rec = np.stack([ids[m], xl[m].view(np.int64), yl[m].view(np.int64),
+                        xu[m].view(np.int64), yu[m].view(np.int64)], axis=1)
+        parts.append(rec)
+        counts.append(len(rec))
+    return (torch.from_numpy(np.ascontiguousarray(np.concatenate(parts))).reshape(-1),
+            counts)
+
+
+def _route_device(cols, k: int, cuts):
+    """The routing kernels (pbsm_route_count + pbsm_route_pack): one send
+    buffer of destination-major 40-byte records and the per-destination
+    counts (one small device→host read)."""
+    import torch
+
+    from . import _native
+    from .device import _ptr, _raw_stream
+
+    lib = _native.load()
+    ids, xl, xu, yl, yu = cols
+    n = len(ids)
+    world = len(cuts) - 1
+    dev = yl.device
+    stream = _raw_stream(dev)
+    cuts_d = torch.as_tensor(cuts, dtype=torch.int32).to(dev)
+    scratch = torch.empty(int(lib.pbsm_route_scratch_bytes(n, k, world)), dtype=torch.uint8,
+                          device=dev)
+    dest = torch.empty(world, dtype=torch.int64, device=dev)
+    _native.check(lib.pbsm_route_count(_ptr(yl), _ptr(yu), n, k, cuts_d.data_ptr(), world,
+                                       scratch.data_ptr(), dest.data_ptr(), stream),
+                  "pbsm_route_count")
+    counts = dest.cpu().tolist()
+    rec = torch.empty(5 * sum(counts), dtype=torch.int64, device=dev)
+    _native.check(lib.pbsm_route_pack(_ptr(ids), _ptr(xl), _ptr(xu), _ptr(yl), _ptr(yu), n, k,
+                                      cuts_d.data_ptr(), world, scratch.data_ptr(),
+                                      _ptr(rec), stream), "pbsm_route_pack")
+    return rec, counts
+
+
+def _unpack(rec):
+    """SJB1 records → (ids, xl, xu, yl, yu) columns (pbsm_unpack_records on
+    the device, a strided view on the host)."""
+    import torch
+
+    n = rec.numel() // 5
+    if not rec.is_cuda:
+        r = rec.view(n, 5)
+        f = r[:, 1:].contiguous().view(torch.float64)
+        return (r[:, 0].contiguous(), f[:, 0].contiguous(), f[:, 2].contiguous(),
+                f[:, 1].contiguous(), f[:, 3].contiguous())
+    from . import _native
+    from .device import _raw_stream
+
+    lib = _native.load()
+    cols = [torch.empty(n, dtype=torch.int64, device=rec.device)] + [
+        torch.empty(n, dtype=torch.float64, device=rec.device) for _ in range(4)]
+    bad = torch.empty(1, dtype=torch.int32, device=rec.device)
+    ids, xl, xu, yl, yu = cols
+    _native.check(lib.pbsm_unpack_records(rec.data_ptr() if n else None, n, _ptr_or0(ids),
+                                          _ptr_or0(xl), _ptr_or0(xu), _ptr_or0(yl),
+                                          _ptr_or0(yu), bad.data_ptr(), _raw_stream(rec.device)),
+                  "pbsm_unpack_records")
+    return tuple(cols)
+
+
+def _ptr_or0(t):
+    return t.data_ptr() if t.numel() else 1  # (never dereferenced when n == 0)
+
+
 def distribute(cols, k: int, cuts, group=None):
     """Device-side input distribution.
 
@@ -229,37 +312,26 @@ def distribute(cols, k: int, cuts, group=None):
     tensors; afterwards every rank holds exactly the rectangles whose tile-row
     range meets its strip [cuts[rank], cuts[rank+1]) — a rectangle spanning a
     strip boundary goes to every strip it touches, as the strip join needs.
-    One all_to_all of the per-destination counts, one all_to_all_single per
-    column (NCCL over NVLink on GPUs, gloo on CPU ranks)."""
+    The routing kernels pack the slice destination-major into one buffer of
+    40-byte records (pbsm_route_count / pbsm_route_pack); then one all_to_all
+    of the per-destination counts and ONE all_to_all_single of the packed
+    records (NCCL over NVLink on GPUs; gloo on CPU ranks, which pack with the
+    host mirror ``_route_host``), and the receiver unpacks the records into
+    columns (pbsm_unpack_records)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    ids, xl, xu, yl, yu = cols
-    r0, r1 = tile_rows_torch(yl, yu, k)
-    c = torch.as_tensor(cuts, dtype=torch.int64, device=yl.device)
-    first = torch.searchsorted(c, r0, right=True) - 1   # strip of the first row
-    last = torch.searchsorted(c, r1, right=True) - 1
-    span = (last - first + 1)
-    # one copy per (rectangle, destination), grouped by destination rank
-    rep = torch.repeat_interleave(torch.arange(len(ids), device=yl.device), span)
-    dest = torch.repeat_interleave(first, span) + (
-        torch.arange(len(rep), device=yl.device) - torch.repeat_interleave(
-            torch.cumsum(span, 0) - span, span))
-    keep = c[dest] < c[dest + 1]            # skip empty strips in a span
-    rep, dest = rep[keep], dest[keep]
-    order = torch.argsort(dest, stable=True)
-    rep, dest = rep[order], dest[order]
-    send_counts = torch.bincount(dest, minlength=world)
+    if len(cuts) != world + 1:
+        raise ValueError(f"{len(cuts) - 1} strips for {world} ranks")
+    rec, sc = (_route_device if cols[0].is_cuda else _route_host)(cols, k, cuts)
+    send_counts = torch.as_tensor(sc, dtype=torch.int64).to(rec.device)
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)
-    sc, rc = send_counts.tolist(), recv_counts.tolist()
-    out = []
-    for col in cols:
-        buf = torch.empty(sum(rc), dtype=col.dtype, device=col.device)
-        dist.all_to_all_single(buf, col[rep].contiguous(), rc, sc, group=group)
-        out.append(buf)
-    return tuple(out)
+    rc = recv_counts.tolist()
+    buf = torch.empty(5 * sum(rc), dtype=torch.int64, device=rec.device)
+    dist.all_to_all_single(buf, rec, [5 * c for c in rc], [5 * c for c in sc], group=group)
+    return _unpack(buf)
 
 
 def _cut_rows(w, k: int, world: int) -> list[int]:
@@ -334,33 +406,48 @@ def distributed_join_slices(r_cols, s_cols, k: int, collect: bool = True, group=
 
 
 def gather_pairs(pairs, exchange: dict, dst: int = 0, group=None):
-    """Pair gather: the ranks' pair shards concatenated
-    on rank `dst` in rank order (each rank's shard starts at its global pair
-    offset).  Returns the (P, 2) tensor on `dst`, None elsewhere."""
+    """Pair gather (the reference concatenates its
+    workers' chunks, engine.py:293-300): the ranks' pair shards land on rank
+    `dst` only, each at its global pair offset (the exchange's prefix), by
+    point-to-point sends straight into the output — no padding, nothing sent
+    to the other ranks.  Returns the (P, 2) tensor on `dst`, None elsewhere."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     counts = exchange["per_rank_pairs"]
-    width = max(max(counts), 1)
-    padded = torch.zeros((width, 2), dtype=torch.int64, device=pairs.device)
-    padded[:len(pairs)] = pairs
-    bufs = [torch.empty_like(padded) for _ in range(world)]
-    dist.all_gather(bufs, padded, group=group)
+    if len(pairs) != counts[rank]:
+        raise ValueError(f"rank {rank}: {len(pairs)} pairs, the exchange says {counts[rank]}")
     if rank != dst:
+        if counts[rank]:
+            dist.send(pairs.contiguous(), dist.get_global_rank(group, dst)
+                      if group is not None else dst, group=group)
         return None
-    return torch.cat([b[:n] for b, n in zip(bufs, counts)])
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    out = torch.empty((int(offs[-1]), 2), dtype=torch.int64, device=pairs.device)
+    out[offs[rank]:offs[rank + 1]] = pairs
+    ops = [dist.P2POp(dist.irecv, out[offs[g]:offs[g + 1]],
+                      dist.get_global_rank(group, g) if group is not None else g, group=group)
+           for g in range(world) if g != rank and counts[g]]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return out
 
 
 def canonical_pairs(pairs):
     """(r_id, s_id) pairs in lexicographic order (the parity form; the
-    reference's own list is unordered, engine.py:61-62) — two stable sorts."""
+    reference's own list is unordered, engine.py:61-62).  Device tensors:
+    the hand-written LSD radix sort (pbsm_sort_pairs, ``device.sort_pairs``);
+    host tensors (gloo ranks): numpy's lexsort."""
     import torch
 
     if len(pairs) == 0:
         return pairs
-    o = torch.argsort(pairs[:, 1], stable=True)
-    p = pairs[o]
-    o = torch.argsort(p[:, 0], stable=True)
-    return p[o]
+    if pairs.is_cuda:
+        from .device import sort_pairs
+
+        return sort_pairs(pairs)
+    p = pairs.numpy()
+    return torch.from_numpy(p[np.lexsort((p[:, 1], p[:, 0]))])

@@ -778,3 +778,53 @@ def test_large_tiles_mixed_sizes_and_classes(k, n, ext):
             assert h["max_huge"] == 0
         assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want), (sweep_min,
                                                                                     ordered)
+
+
+def _points(n, seed, clustered):
+    rng = np.random.default_rng(seed)
+    if clustered:
+        mu = rng.random((16, 2))
+        pick = rng.integers(0, 16, n)
+        x = np.clip(mu[pick, 0] + rng.normal(0, 1, n) * 0.01, 0, 1)
+        y = np.clip(mu[pick, 1] + rng.normal(0, 1, n) * 0.01, 0, 1)
+    else:
+        x, y = rng.random(n), rng.random(n)
+    # point rectangles: the ε-join reads the lower corners (engine.py:333-334)
+    return pb.RectBatch(np.arange(n, dtype=np.int64) + 7 * seed, x, x, y, y)
+
+
+@pytest.mark.parametrize("k", [4, 40, 400])
+def test_fused_epsilon_join_vs_oracle(k):
+    # K=4: every tile is large (brute-force work items); K=40: nested + sorted
+    # + large; K=400: nested.  The distance test runs inside the mini-joins.
+    P, Q = _points(20000, 1, False), _points(20000, 2, True)
+    eps = 3e-3
+    want = oracle.epsilon_join(P, Q, eps, k)
+    rep = pb.epsilon_distance_join(P, Q, eps, _collect("2d", k))
+    assert rep.result_count == want["count"] < want["candidates"]
+    assert np.array_equal(oracle.sorted_pairs(rep.pairs), oracle.sorted_pairs(want["pairs"]))
+    cnt = pb.epsilon_distance_join(P, Q, eps, pb.JoinConfig(pb.PartitionLayout("2d", k)))
+    assert cnt.result_count == want["count"] and cnt.pairs is None
+
+
+@pytest.mark.parametrize("nested_max", [0, 1 << 30])
+def test_fused_epsilon_every_strategy(nested_max):
+    # nested_max 0: every small tile sorted + forward-scanned; 2^30: all nested
+    P, Q = _points(6000, 3, True), _points(6000, 4, True)
+    eps, k = 5e-3, 64
+    want = oracle.epsilon_join(P, Q, eps, k)
+    res = dev.run_join(dev.points_to_device(P), dev.points_to_device(Q), k, k, eps=eps,
+                       nested_max=nested_max)
+    assert res.count == want["count"]
+    got = oracle.sorted_pairs(res.pairs.cpu().numpy())
+    assert np.array_equal(got, oracle.sorted_pairs(want["pairs"]))
+    assert res.header["n_sorted" if nested_max == 0 else "n_nested"] > 0
+
+
+def test_fused_epsilon_self_join():
+    P = _points(15000, 5, True)
+    eps, k = 2e-3, 100
+    want = oracle.epsilon_join(P, P, eps, k)
+    rep = pb.epsilon_distance_join(P, P, eps, _collect("2d", k))
+    assert rep.result_count == want["count"]
+    assert np.array_equal(oracle.sorted_pairs(rep.pairs), oracle.sorted_pairs(want["pairs"]))

@@ -131,3 +131,18 @@ def test_full_truth_is_consistent_with_fixtures():
         spec = CONFIGS[int(name[3:])]
         assert (t["count"], t["a_r"], t["a_s"]) == (spec.pairs, spec.a_r, spec.a_s), name
         assert (t["n_r"], t["n_s"], t["k"]) == (spec.n_r, spec.n_s, spec.k), name
+
+
+def test_oracle_epsilon_join_matches_reference(golden):
+    # the CPU restatement of epsilon_distance_join (engine.py:326-353) vs the
+    # reference's own outputs
+    g = golden["epsilon"]
+    for i in range(3):
+        x, y = g[f"e{i}_p"]
+        x2, y2 = g[f"e{i}_q"]
+        n = len(x)
+        P = (np.arange(n, dtype=np.int64), x, x, y, y)
+        Q = (np.arange(n, dtype=np.int64) + 5000, x2, x2, y2, y2)
+        res = oracle.epsilon_join(P, Q, float(g[f"e{i}_eps"]), int(g[f"e{i}_k"]))
+        assert np.array_equal(oracle.sorted_pairs(res["pairs"]), g[f"e{i}_pairs"])
+        assert res["candidates"] >= res["count"]
