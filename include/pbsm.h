@@ -404,6 +404,27 @@ int pbsm_pair_digits(const int64_t* pairs, int64_t n, uint32_t* hist, void* stre
 int pbsm_sort_pairs(int64_t* pairs, int64_t n, uint32_t pass_mask, void* tmp, void* scratch,
                     void* stream);
 
+/* ======================================================================
+ * partition() — the reference's public two-pass partitioning
+ * (partition.py:243-263 → PartitionedDataset, partition.py:75-111) for the
+ * kx × ky grid (1D stripes: kx × 1 or 1 × ky).  pbsm_partition_count puts
+ * the total assignments A (Σ over rectangles of the tiles they overlap,
+ * = PartitionedDataset.total_assigned) in *total (device int64);
+ * pbsm_partition_write (same n, same scratch; keys / keys_tmp: 16*A bytes,
+ * sort_scratch: pbsm_sort_pairs_scratch_bytes(A)) writes the A entries
+ * tile-major, rows ascending inside a tile — the reference's order for any
+ * writer count m — as SoA columns, and offsets (device int64[kx*ky+1], the
+ * CSR array).  ids may be NULL (row indices). */
+int64_t pbsm_partition_scratch_bytes(int64_t n, int32_t kx, int32_t ky);
+int pbsm_partition_count(const double* xl, const double* xu, const double* yl, const double* yu,
+                         int64_t n, int32_t kx, int32_t ky, void* scratch, int64_t* total,
+                         void* stream);
+int pbsm_partition_write(const int64_t* ids, const double* xl, const double* xu,
+                         const double* yl, const double* yu, int64_t n, int32_t kx, int32_t ky,
+                         void* scratch, int64_t total, void* keys, void* keys_tmp,
+                         void* sort_scratch, int64_t* out_ids, double* out_xl, double* out_xu,
+                         double* out_yl, double* out_yu, int64_t* offsets, void* stream);
+
 /* ABI version / build identification */
 int32_t pbsm_abi_version(void);
 const char* pbsm_build_info(void);

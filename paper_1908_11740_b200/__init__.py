@@ -7,7 +7,17 @@ hand-written sm_100a CUDA kernels (``csrc/pbsm.cu``) behind the C ABI in
 ``include/pbsm.h``.  There is no CPU fallback.
 """
 
-from .engine import JoinConfig, JoinReport, epsilon_distance_join, join, join_device, squares
+from .engine import (
+    JoinConfig,
+    JoinReport,
+    JoinTask,
+    SortTask,
+    build_task_queue,
+    epsilon_distance_join,
+    join,
+    join_device,
+    squares,
+)
 from .errors import (
     ConfigError,
     DatasetError,
@@ -29,7 +39,16 @@ from .geometry import (
     intersects,
     tile_boundary,
 )
-from .partition import DEFAULT_K_MAX, PartitionLayout, recommend_k, tiles_overlapping
+from .partition import (
+    DEFAULT_K_MAX,
+    PartitionedDataset,
+    PartitionLayout,
+    count_pass,
+    partition,
+    recommend_k,
+    tiles_overlapping,
+    write_pass,
+)
 
 __version__ = "0.1.0"
 

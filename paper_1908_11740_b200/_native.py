@@ -33,6 +33,7 @@ EXPORTED = (
     "pbsm_count_points", "pbsm_scatter_points", "pbsm_join_count_eps", "pbsm_join_emit_eps",
     "pbsm_route_scratch_bytes", "pbsm_route_count", "pbsm_route_pack",
     "pbsm_sort_pairs_scratch_bytes", "pbsm_pair_digits", "pbsm_sort_pairs",
+    "pbsm_partition_scratch_bytes", "pbsm_partition_count", "pbsm_partition_write",
     "pbsm_unit_supported", "pbsm_unit_workspace_bytes", "pbsm_unit_bin_bytes",
     "pbsm_unit_scratch_bytes", "pbsm_unit_init", "pbsm_unit_count", "pbsm_unit_map",
     "pbsm_unit_bin", "pbsm_unit_join", "pbsm_read_uheader",
@@ -125,6 +126,10 @@ _SIGNATURES = {
     "pbsm_sort_pairs_scratch_bytes": (_I64, [_I64]),
     "pbsm_pair_digits": (C.c_int, [_P, _I64, _P, _P]),
     "pbsm_sort_pairs": (C.c_int, [_P, _I64, C.c_uint32, _P, _P, _P]),
+    "pbsm_partition_scratch_bytes": (_I64, [_I64, _I32, _I32]),
+    "pbsm_partition_count": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P]),
+    "pbsm_partition_write": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _I64, _P, _P,
+                                       _P, _P, _P, _P, _P, _P, _P, _P]),
     "pbsm_unit_supported": (_I32, [_I32, _I32, _I32, _I32]),
     "pbsm_unit_workspace_bytes": (_I64, [_I32, _I32, _I32, _I32]),
     "pbsm_unit_bin_bytes": (_I64, [_I64]),

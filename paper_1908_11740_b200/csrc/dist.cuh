@@ -220,3 +220,86 @@ inline PairSortLayout pair_sort_layout(i64 n) {
   L.total = o;
   return L;
 }
+
+// ---------------------------------------------------------------- public partition()
+// partition() / PartitionedDataset (partition.py:75-111, 243-263) on the
+// device: every (tile, rectangle) assignment as a (tile, row) key pair, the
+// keys radix-sorted (stable: rows ascending inside a tile — exactly the
+// reference's order, whose writers own contiguous input slices in slice order,
+// partition.py:130-133, 201-227), the coordinates gathered in that order and
+// the CSR offsets found at the tile boundaries of the sorted keys.
+template <typename F>
+__device__ __forceinline__ void rect_tiles(double a, double b, double c, double d, int kx, int ky,
+                                           const double* bx, const double* by, F&& f) {
+  const int c0 = tile_of(a, kx, bx), c1 = tile_of(b, kx, bx);
+  const int r0 = tile_of(c, ky, by), r1 = tile_of(d, ky, by);
+  // tiles_overlapping (partition.py:114-127): rows ascending, then columns
+  for (int row = r0; row <= r1; ++row)
+    for (int col = c0; col <= c1; ++col) f((u64)row * (u64)kx + (u64)col);
+}
+
+__global__ void k_assign_count(const double* __restrict__ xl, const double* __restrict__ xu,
+                               const double* __restrict__ yl, const double* __restrict__ yu,
+                               i64 n, int kx, int ky, const double* __restrict__ bx,
+                               const double* __restrict__ by, u32* __restrict__ per) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const int c0 = tile_of(xl[i], kx, bx), c1 = tile_of(xu[i], kx, bx);
+    const int r0 = tile_of(yl[i], ky, by), r1 = tile_of(yu[i], ky, by);
+    per[i] = (u32)((c1 - c0 + 1) * (r1 - r0 + 1));
+  }
+}
+
+__global__ void k_assign_write(const double* __restrict__ xl, const double* __restrict__ xu,
+                               const double* __restrict__ yl, const double* __restrict__ yu,
+                               i64 n, int kx, int ky, const double* __restrict__ bx,
+                               const double* __restrict__ by, const u64* __restrict__ start,
+                               ulonglong2* __restrict__ keys) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    u64 o = start[i];
+    rect_tiles(xl[i], xu[i], yl[i], yu[i], kx, ky, bx, by,
+               [&](u64 t) { keys[o++] = make_ulonglong2(t, (u64)i); });
+  }
+}
+
+// sorted (tile, row) keys → SoA copies + offsets[t] = first position of tile t
+__global__ void k_assign_gather(const ulonglong2* __restrict__ keys, i64 a, u64 tiles,
+                                const i64* __restrict__ ids, const double* __restrict__ xl,
+                                const double* __restrict__ xu, const double* __restrict__ yl,
+                                const double* __restrict__ yu, i64* __restrict__ o_ids,
+                                double* __restrict__ o_xl, double* __restrict__ o_xu,
+                                double* __restrict__ o_yl, double* __restrict__ o_yu,
+                                i64* __restrict__ offsets) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i <= a;
+       i += (i64)gridDim.x * blockDim.x) {
+    const u64 t = i < a ? keys[i].x : tiles;
+    const u64 prev = i > 0 ? keys[i - 1].x + 1 : 0;  // tiles (prev, t] start here
+    for (u64 q = prev; q <= t; ++q) offsets[q] = i;
+    if (i < a) {
+      const i64 r = (i64)keys[i].y;
+      o_ids[i] = ids ? ids[r] : r;
+      o_xl[i] = xl[r];
+      o_xu[i] = xu[r];
+      o_yl[i] = yl[r];
+      o_yu[i] = yu[r];
+    }
+  }
+}
+
+struct AssignLayout {
+  size_t bx, by, per, start, part, total;
+  u64 nb;
+};
+inline AssignLayout assign_layout(i64 n, int kx, int ky) {
+  AssignLayout L;
+  L.nb = ((u64)n + kScanTile - 1) / kScanTile;
+  size_t o = 0;
+  L.bx = o; o = align_up(o + 8 * ((size_t)kx + 1), 256);
+  L.by = o; o = align_up(o + 8 * ((size_t)ky + 1), 256);
+  L.per = o; o = align_up(o + 4 * ((size_t)n + 1), 256);
+  L.start = o; o = align_up(o + 8 * ((size_t)n + 1), 256);
+  L.part = o; o = align_up(o + 8 * (L.nb + 1), 256);
+  L.total = o;
+  return L;
+}

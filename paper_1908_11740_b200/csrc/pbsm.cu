@@ -477,6 +477,78 @@ int pbsm_sort_pairs(int64_t* pairs, int64_t n, uint32_t pass_mask, void* tmp, vo
   return launch_status();
 }
 
+// ------------------------------------------------------------ partition()
+int64_t pbsm_partition_scratch_bytes(int64_t n, int32_t kx, int32_t ky) {
+  if (n < 0 || kx < 1 || ky < 1 || kx > 65535 || ky > 65535) return PBSM_E_ARG;
+  return (int64_t)assign_layout(n, kx, ky).total;
+}
+
+int pbsm_partition_count(const double* xl, const double* xu, const double* yl, const double* yu,
+                         int64_t n, int32_t kx, int32_t ky, void* scratch, int64_t* total,
+                         void* stream) {
+  if (n < 0 || kx < 1 || ky < 1 || kx > 65535 || ky > 65535 || !scratch || !total)
+    return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  const AssignLayout L = assign_layout(n, kx, ky);
+  char* b = (char*)scratch;
+  double* bx = (double*)(b + L.bx);
+  double* by = (double*)(b + L.by);
+  u32* per = (u32*)(b + L.per);
+  u64* start = (u64*)(b + L.start);
+  k_bounds<<<(unsigned)((kx + 256) / 256), 256, 0, s>>>(bx, kx);
+  k_bounds<<<(unsigned)((ky + 256) / 256), 256, 0, s>>>(by, ky);
+  if (n == 0) {
+    cudaMemsetAsync(total, 0, 8, s);
+    return launch_status();
+  }
+  if (!xl || !xu || !yl || !yu) return PBSM_E_ARG;
+  const unsigned blocks = (unsigned)std::min<i64>((n + 255) / 256, (i64)num_sms() * 8);
+  k_assign_count<<<blocks, 256, 0, s>>>(xl, xu, yl, yu, n, kx, ky, bx, by, per);
+  k_scan_reduce<<<(unsigned)L.nb, kScanThreads, 0, s>>>(per, (u64)n, (u64*)(b + L.part));
+  k_scan_partials<<<1, 1024, 0, s>>>((u64*)(b + L.part), L.nb, start, (u64)n);
+  k_scan_apply<<<(unsigned)L.nb, kScanThreads, 0, s>>>(per, (u64)n, (u64*)(b + L.part), start);
+  cudaMemcpyAsync(total, start + n, 8, cudaMemcpyDeviceToDevice, s);
+  return launch_status();
+}
+
+int pbsm_partition_write(const int64_t* ids, const double* xl, const double* xu,
+                         const double* yl, const double* yu, int64_t n, int32_t kx, int32_t ky,
+                         void* scratch, int64_t total, void* keys, void* keys_tmp,
+                         void* sort_scratch, int64_t* out_ids, double* out_xl, double* out_xu,
+                         double* out_yl, double* out_yu, int64_t* offsets, void* stream) {
+  if (n < 0 || kx < 1 || ky < 1 || kx > 65535 || ky > 65535 || !scratch || total < 0 ||
+      !offsets)
+    return PBSM_E_ARG;
+  cudaStream_t s = as_stream(stream);
+  const AssignLayout L = assign_layout(n, kx, ky);
+  char* b = (char*)scratch;
+  const double* bx = (const double*)(b + L.bx);
+  const double* by = (const double*)(b + L.by);
+  const u64 tiles = (u64)kx * (u64)ky;
+  if (total > 0) {
+    if (!xl || !xu || !yl || !yu || !keys || !keys_tmp || !sort_scratch || !out_ids || !out_xl ||
+        !out_xu || !out_yl || !out_yu)
+      return PBSM_E_ARG;
+    const unsigned blocks = (unsigned)std::min<i64>((n + 255) / 256, (i64)num_sms() * 8);
+    k_assign_write<<<blocks, 256, 0, s>>>(xl, xu, yl, yu, n, kx, ky, bx, by,
+                                          (const u64*)(b + L.start), (ulonglong2*)keys);
+    // digits that can vary: rows < n (low word), tiles < kx*ky (high word)
+    u32 mask = 0;
+    for (int d = 0; d < 7; ++d) {
+      if (((u64)(n - 1) >> (8 * d)) != 0) mask |= 1u << d;
+      if (((tiles - 1) >> (8 * d)) != 0) mask |= 1u << (8 + d);
+    }
+    int rc = pbsm_sort_pairs((int64_t*)keys, total, mask, keys_tmp, sort_scratch, stream);
+    if (rc) return rc;
+  }
+  const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((total + 256) / 256,
+                                                               (i64)num_sms() * 8));
+  k_assign_gather<<<gb, 256, 0, s>>>((const ulonglong2*)keys, total, tiles, (const i64*)ids, xl,
+                                     xu, yl, yu, (i64*)out_ids, out_xl, out_xu, out_yl, out_yu,
+                                     (i64*)offsets);
+  return launch_status();
+}
+
 // ------------------------------------------------------------ unit pipeline
 static int unit_nb() { return std::min(num_sms(), 1024); }
 

@@ -26,7 +26,8 @@ from . import _native
 from .errors import KernelError
 
 __all__ = ["DeviceRects", "DeviceJoinResult", "PhaseProbe", "release_buffers", "run_join",
-           "points_to_device", "to_device", "to_device_pipelined"]
+           "partition_columns", "points_to_device", "sort_pairs", "tile_counts", "to_device",
+           "to_device_pipelined"]
 
 
 @dataclass
@@ -953,6 +954,40 @@ def tile_counts(r, s, kx: int, ky: int, row_lo: int = 0, row_hi: int | None = No
     out = (cr.cpu().numpy(), cs.cpu().numpy())
     _read_header(lib, ws, stream)  # validation bits → ValueError
     return out
+
+
+def partition_columns(batch, kx: int, ky: int, device=None):
+    """partition() on the device (partition.py:243-263): every rectangle of
+    ``batch`` (RectBatch / 5-tuple) copied into each tile of the ``kx × ky``
+    grid it overlaps, tile-major and in input order inside a tile (the
+    reference's order for every writer count).  Returns host numpy arrays
+    (offsets int64[kx*ky+1], ids, xl, xu, yl, yu) — PartitionedDataset's
+    fields (partition.py:75-111).  RectBatch.validate's errors are the
+    caller's (the reference validates in as_batch / join)."""
+    lib = _native.load()
+    dv = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    b = batch if isinstance(batch, DeviceRects) else to_device(batch, dv)
+    n = len(b)
+    stream = _raw_stream(b.device)
+    scratch = torch.empty(int(lib.pbsm_partition_scratch_bytes(n, kx, ky)), dtype=torch.uint8,
+                          device=b.device)
+    total_d = torch.empty(1, dtype=torch.int64, device=b.device)
+    _native.check(lib.pbsm_partition_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), n, kx,
+                                           ky, scratch.data_ptr(), total_d.data_ptr(), stream),
+                  "pbsm_partition_count")
+    a = int(total_d.item())
+    keys = torch.empty((max(a, 1), 2), dtype=torch.int64, device=b.device)
+    tmp = torch.empty_like(keys)
+    sort_scratch = torch.empty(int(lib.pbsm_sort_pairs_scratch_bytes(a)), dtype=torch.uint8,
+                               device=b.device)
+    out = [torch.empty(max(a, 1), dtype=torch.int64, device=b.device)] + [
+        torch.empty(max(a, 1), dtype=torch.float64, device=b.device) for _ in range(4)]
+    offsets = torch.empty(kx * ky + 1, dtype=torch.int64, device=b.device)
+    _native.check(lib.pbsm_partition_write(
+        _ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), n, kx, ky,
+        scratch.data_ptr(), a, keys.data_ptr(), tmp.data_ptr(), sort_scratch.data_ptr(),
+        *(t.data_ptr() for t in out), offsets.data_ptr(), stream), "pbsm_partition_write")
+    return (offsets.cpu().numpy(),) + tuple(t[:a].cpu().numpy() for t in out)
 
 
 def _align(v: int, a: int = 256) -> int:

@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import time
 from dataclasses import dataclass, field
-from typing import Literal, Sequence
+from typing import Literal, NamedTuple, Sequence
 
 import numpy as np
 import torch
@@ -21,12 +21,12 @@ import torch
 from . import device as dev
 from .errors import ConfigError, KernelError
 from .geometry import Rect, RectBatch, as_batch
-from .partition import MAX_DEVICE_K, PartitionLayout
+from .partition import MAX_DEVICE_K, PartitionedDataset, PartitionLayout
 
 AxisPolicyName = Literal["x", "y", "adaptive", "auto"]
 
-__all__ = ["JoinConfig", "JoinReport", "epsilon_distance_join", "join", "join_device",
-           "squares"]
+__all__ = ["JoinConfig", "JoinReport", "JoinTask", "SortTask", "build_task_queue",
+           "epsilon_distance_join", "join", "join_device", "squares"]
 
 
 @dataclass
@@ -87,6 +87,37 @@ class JoinReport:
     join_time: float
     total_time: float
     task_sizes: np.ndarray | None = field(default=_Lazy(), repr=False)
+
+
+class SortTask(NamedTuple):
+    """One per-tile sort (engine.py:73-76); ``which`` 0 = first input, 1 = second."""
+
+    which: int
+    tile: int
+    size: int
+
+
+class JoinTask(NamedTuple):
+    """One per-tile join (engine.py:79-81)."""
+
+    tile: int
+    size: int
+
+
+def build_task_queue(partitioned_r: PartitionedDataset, partitioned_s: PartitionedDataset,
+                     ) -> tuple[list[SortTask], list[JoinTask]]:
+    """The reference's work lists, largest first (engine.py:84-100): one sort
+    task per non-empty (tile, input), one join task per tile where both
+    inputs are non-empty.  (The device join builds the same join set and its
+    own CTA work units inside pbsm_plan; this is the host view of it.)"""
+    cr, cs = partitioned_r.counts, partitioned_s.counts
+    sort_tasks = [SortTask(0, int(t), int(cr[t])) for t in np.nonzero(cr)[0]]
+    sort_tasks += [SortTask(1, int(t), int(cs[t])) for t in np.nonzero(cs)[0]]
+    sort_tasks.sort(key=lambda task: -task.size)
+    both = np.nonzero((cr > 0) & (cs > 0))[0]
+    join_tasks = [JoinTask(int(t), int(cr[t] + cs[t])) for t in both]
+    join_tasks.sort(key=lambda task: -task.size)
+    return sort_tasks, join_tasks
 
 
 def _resolve_policy(cfg: JoinConfig) -> str:

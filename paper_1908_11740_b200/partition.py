@@ -15,19 +15,21 @@ the reference uses (``_kernels.pyx:91``).
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Literal
+from typing import Literal, Sequence
 
 import numpy as np
 
-from .errors import InvalidStatisticsError
-from .geometry import Axis, Rect, TileExtent, axis_tile_index, tile_boundary
+from .errors import ConfigError, InvalidStatisticsError
+from .geometry import Axis, Rect, RectBatch, TileExtent, as_batch, axis_tile_index, tile_boundary
 
 DEFAULT_K_MAX = 20000
 MAX_DEVICE_K = 65535
 
 PartitionKind = Literal["1d", "2d"]
 
-__all__ = ["DEFAULT_K_MAX", "PartitionLayout", "recommend_k", "tiles_overlapping"]
+__all__ = ["DEFAULT_K_MAX", "PartitionLayout", "PartitionedDataset", "compute_segment_offsets",
+           "count_pass", "partition", "recommend_k", "split_slices", "tiles_overlapping",
+           "write_pass"]
 
 
 @dataclass(frozen=True)
@@ -95,3 +97,126 @@ def recommend_k(avg_extent_split_axis: float, kind: PartitionKind = "1d",
         raise InvalidStatisticsError(
             f"average extent must be positive, got {avg_extent_split_axis!r}")
     return int(np.clip(round(1.0 / (10.0 * avg_extent_split_axis)), 1, k_max))
+
+
+# ---------------------------------------------------------------- public partitioning
+# The reference's two-pass partitioning API (partition.py:75-263), on the
+# device: the count pass is pbsm_count (the join's k_count), the write pass
+# pbsm_partition_write (assignment keys, stable radix sort, gather).  The
+# reference's writers m and executor only choose how the CPU work is split;
+# the buffers they produce are identical for every m (criterion 9,
+# tests/test_acceptance.py:291-313), and so are these.
+
+@dataclass
+class PartitionedDataset:
+    """Per-tile contiguous rectangle buffers of one input (partition.py:75-111):
+    tile ``t`` owns rows [offsets[t], offsets[t+1]) of the coordinate arrays.
+    ``hist_x`` / ``hist_y`` (the adaptive axis model's sampled histograms) are
+    always None here: that model is out of scope (result-invariant)."""
+
+    layout: PartitionLayout
+    offsets: np.ndarray
+    ids: np.ndarray
+    xl: np.ndarray
+    xu: np.ndarray
+    yl: np.ndarray
+    yu: np.ndarray
+    source_count: int
+    hist_x: np.ndarray | None = None
+    hist_y: np.ndarray | None = None
+
+    @property
+    def counts(self) -> np.ndarray:
+        return np.diff(self.offsets)
+
+    @property
+    def total_assigned(self) -> int:
+        return int(self.offsets[-1])
+
+    def tile_bounds(self, t: int) -> tuple[int, int]:
+        return int(self.offsets[t]), int(self.offsets[t + 1])
+
+    def tile_batch(self, t: int) -> RectBatch:
+        lo, hi = self.tile_bounds(t)
+        return RectBatch(self.ids[lo:hi], self.xl[lo:hi], self.xu[lo:hi],
+                         self.yl[lo:hi], self.yu[lo:hi])
+
+
+def split_slices(n: int, m: int) -> list[tuple[int, int]]:
+    """range(n) in m near-equal contiguous [start, stop) slices (partition.py:130-133)."""
+    bounds = np.linspace(0, n, m + 1).astype(np.int64)
+    return [(int(bounds[i]), int(bounds[i + 1])) for i in range(m)]
+
+
+def compute_segment_offsets(per_slice_counts: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """(m, n_tiles) counts → (CSR tile offsets, each writer's start per tile)
+    (partition.py:151-164)."""
+    per_slice_counts = np.atleast_2d(np.asarray(per_slice_counts, dtype=np.int64))
+    totals = per_slice_counts.sum(axis=0)
+    tile_offsets = np.zeros(len(totals) + 1, dtype=np.int64)
+    np.cumsum(totals, out=tile_offsets[1:])
+    within = np.zeros_like(per_slice_counts)
+    np.cumsum(per_slice_counts[:-1], axis=0, out=within[1:])
+    return tile_offsets, within + tile_offsets[:-1]
+
+
+def _check_hist(hist) -> None:
+    if hist is not None:
+        raise ConfigError("per-tile axis histograms belong to the adaptive axis model, "
+                          "which this build does not implement (result-invariant)")
+
+
+def count_pass(rects: RectBatch | Sequence[Rect], layout: PartitionLayout,
+               start: int = 0, stop: int | None = None, kernels=None) -> np.ndarray:
+    """Per-tile assignment counts of rows [start, stop) (partition.py:136-148),
+    by the device count pass (pbsm_count).  ``kernels`` is accepted for
+    signature compatibility; there is one backend."""
+    from . import device as dev
+
+    batch = as_batch(rects)
+    if stop is None:
+        stop = len(batch)
+    kx, ky = layout.grid
+    if stop <= start:
+        return np.zeros(layout.n_tiles, dtype=np.int64)
+    sl = tuple(np.ascontiguousarray(a[start:stop])
+               for a in (batch.ids, batch.xl, batch.xu, batch.yl, batch.yu))
+    return dev.tile_counts(sl, sl, kx, ky)[0]
+
+
+def _device_dataset(batch: RectBatch, layout: PartitionLayout) -> PartitionedDataset:
+    from . import device as dev
+
+    kx, ky = layout.grid
+    offsets, ids, xl, xu, yl, yu = dev.partition_columns(
+        (batch.ids, batch.xl, batch.xu, batch.yl, batch.yu), kx, ky)
+    return PartitionedDataset(layout, offsets, ids, xl, xu, yl, yu, source_count=len(batch))
+
+
+def write_pass(rects: RectBatch | Sequence[Rect], layout: PartitionLayout,
+               counts: np.ndarray, segment_offsets: np.ndarray,
+               executor=None, kernels=None, hist=None) -> PartitionedDataset:
+    """Fill the per-tile buffers (partition.py:176-240) on the device.  The
+    reference's guard (:229-233) is kept: writer i (input slice i of m) must
+    end exactly at writer i+1's start, the last at the tile's end, or
+    RuntimeError — checked against the device count of each slice."""
+    _check_hist(hist)
+    batch = as_batch(rects)
+    seg = np.atleast_2d(np.asarray(segment_offsets, dtype=np.int64))
+    m = seg.shape[0]
+    tile_offsets = np.zeros(layout.n_tiles + 1, dtype=np.int64)
+    np.cumsum(np.asarray(counts, dtype=np.int64), out=tile_offsets[1:])
+    final = np.vstack([seg[i] + count_pass(batch, layout, a, b)
+                       for i, (a, b) in enumerate(split_slices(len(batch), m))])
+    expected = np.vstack([seg[1:], tile_offsets[1:].reshape(1, -1)])
+    if not np.array_equal(final, expected):
+        raise RuntimeError("partition write overflow: count and write passes disagree")
+    return _device_dataset(batch, layout)
+
+
+def partition(rects: RectBatch | Sequence[Rect], layout: PartitionLayout,
+              m: int = 1, executor=None, kernels=None, hist=None) -> PartitionedDataset:
+    """Two-pass partitioning (partition.py:243-263): count, offsets, write —
+    one device pass each; the result is the reference's for every ``m``."""
+    _check_hist(hist)
+    return _device_dataset(as_batch(rects), layout)

@@ -19,4 +19,4 @@ def golden():
 
     g = ROOT / "tests" / "golden"
     return {name: np.load(g / f"{name}.npz") for name in
-            ("instances", "configs", "tile_of", "epsilon", "synthetic")}
+            ("instances", "configs", "tile_of", "epsilon", "synthetic", "partition")}

@@ -17,7 +17,10 @@ scratch copy and records the reference's own outputs on seeded inputs:
 * ``tile_of.npz``    — axis_tile_index known answers at and around i/k;
 * ``epsilon.npz``    — epsilon_distance_join known answers;
 * ``synthetic.npz``  — generate_synthetic outputs, a join of two of them and
-  the acceptance criterion-3 count (``python make_golden.py synthetic``).
+  the acceptance criterion-3 count (``python make_golden.py synthetic``);
+* ``partition.npz``  — partition() PartitionedDataset arrays (offsets, ids,
+  coordinates) for 1D x / 1D y / 2D layouts at m = 1 and m = 3, and
+  build_task_queue's sort/join task lists (``python make_golden.py partition``).
 
 Nothing here runs on the GPU box; the .npz files are committed.
 """
@@ -212,13 +215,57 @@ def make_synthetic(sj):
     np.savez_compressed(HERE / "synthetic.npz", **out)
 
 
+PART_LAYOUTS = [("1d", 7, 0), ("1d", 6, 1), ("2d", 5, 0), ("2d", 23, 0)]
+
+
+def make_partition(sj):
+    """partition() (partition.py:243-263) and build_task_queue
+    (engine.py:84-100) known answers on seeded mixed-extent inputs."""
+    from sweepjoin.partition import partition
+    rng = np.random.default_rng(2024)
+    out = {}
+    for i in range(2):
+        n = 600 + 200 * i
+        xl, yl = rng.random(n), rng.random(n)
+        w = np.where(rng.random(n) < 0.2, rng.random(n) * 0.5, rng.random(n) * 0.02)
+        h = np.where(rng.random(n) < 0.2, rng.random(n) * 0.5, rng.random(n) * 0.02)
+        xl[:20] = np.round(xl[:20] * 5) / 5   # on tile boundaries of K=5
+        batch = sj.RectBatch(np.arange(n, dtype=np.int64) * 3 + 1, xl, np.minimum(xl + w, 1.0),
+                             yl, np.minimum(yl + h, 1.0))
+        for c in ("ids", "xl", "xu", "yl", "yu"):
+            out[f"p{i}_{c}"] = getattr(batch, c)
+        for j, (kind, k, axis) in enumerate(PART_LAYOUTS):
+            layout = sj.PartitionLayout(kind, k, sj.Axis(axis))
+            for m in (1, 3):
+                pd = partition(batch, layout, m=m)
+                tag = f"p{i}_l{j}_m{m}"
+                out[f"{tag}_offsets"] = pd.offsets
+                for c in ("ids", "xl", "xu", "yl", "yu"):
+                    out[f"{tag}_{c}"] = getattr(pd, c)
+        # task queue of input 0 vs input 1 on the 2D K=5 layout
+    layout = sj.PartitionLayout("2d", 5)
+    pr = partition(sj.RectBatch(*(out[f"p0_{c}"] for c in ("ids", "xl", "xu", "yl", "yu"))),
+                   layout)
+    ps = partition(sj.RectBatch(*(out[f"p1_{c}"] for c in ("ids", "xl", "xu", "yl", "yu"))),
+                   layout)
+    sort_tasks, join_tasks = sj.build_task_queue(pr, ps)
+    out["tq_sort"] = np.array([tuple(t) for t in sort_tasks], dtype=np.int64)
+    out["tq_join"] = np.array([tuple(t) for t in join_tasks], dtype=np.int64)
+    out["layouts"] = np.array([f"{a},{b},{c}" for a, b, c in PART_LAYOUTS])
+    np.savez_compressed(HERE / "partition.npz", **out)
+
+
 if __name__ == "__main__":
     sj = import_reference()
     if sys.argv[1:] == ["synthetic"]:
         make_synthetic(sj)
+        sys.exit(0)
+    if sys.argv[1:] == ["partition"]:
+        make_partition(sj)
         sys.exit(0)
     make_tile_of(sj)
     make_instances(sj)
     make_epsilon(sj)
     make_configs(sj)
     make_synthetic(sj)
+    make_partition(sj)
