@@ -144,6 +144,11 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
 
 /* Copy the device header to *out and synchronise the stream. */
 int pbsm_read_header(void* ws, pbsm_header* out, void* stream);
+/* Enqueue only: a tiny kernel stores the device header into *out, which must
+ * be page-locked host memory (device-mapped); the caller synchronises later.
+ * Capturable in a CUDA graph (the repeated-shape path replays init → count →
+ * plan → scatter → bounded emit → this publish as one graph). */
+int pbsm_publish_header(void* ws, pbsm_header* out, void* stream);
 
 /* write_tiles (_kernels.pyx:61-98) for ALL n rectangles of one input:
  * scatter each rectangle into the list of every JOIN tile it overlaps (tiles

@@ -26,7 +26,8 @@ ERR_INTERNAL = 256
 
 EXPORTED = (
     "pbsm_abi_version", "pbsm_build_info", "pbsm_workspace_bytes", "pbsm_init",
-    "pbsm_count", "pbsm_plan", "pbsm_read_header", "pbsm_scatter", "pbsm_bin",
+    "pbsm_count", "pbsm_plan", "pbsm_read_header", "pbsm_publish_header", "pbsm_scatter",
+    "pbsm_bin",
     "pbsm_scatter_banded",
     "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit", "pbsm_join_emit_bounded",
     "pbsm_unpack_records", "pbsm_map_ids", "pbsm_group_pairs",
@@ -98,6 +99,7 @@ _SIGNATURES = {
     "pbsm_count": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P]),
     "pbsm_plan": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _I64, _P]),
     "pbsm_read_header": (C.c_int, [_P, C.POINTER(Header), _P]),
+    "pbsm_publish_header": (C.c_int, [_P, _P, _P]),
     "pbsm_scatter": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32,
                                _P, _I64, _P]),
     "pbsm_bin": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P, _P]),

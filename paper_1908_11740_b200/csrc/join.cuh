@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(kNT, EPS ? 4 : PBSM_NESTED_MINB) k_join_nested
   if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
     bool bad = false;
     for (u64 t = blockIdx.x * (u64)kNT + threadIdx.x; t < A.g_tiles; t += (u64)gridDim.x * kNT)
-      bad |= (A.g_cur_r[t] != A.g_end_r[t]) || (A.g_cur_s[t] != A.g_end_s[t]);
+      bad |= !cursor_done(A.g_cur_r[t], A.g_end_r[t]) || !cursor_done(A.g_cur_s[t], A.g_end_s[t]);
     if (bad) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
   }
   __shared__ int s_unit;

@@ -185,6 +185,12 @@ int pbsm_read_header(void* ws, pbsm_header* out, void* stream) {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
+int pbsm_publish_header(void* ws, pbsm_header* out, void* stream) {
+  if (!ws || !out) return PBSM_E_ARG;
+  k_publish_header<<<1, 32, 0, as_stream(stream)>>>(reinterpret_cast<const pbsm_header*>(ws), out);
+  return launch_status();
+}
+
 static int scatter_impl(const int64_t* ids, const double* xl, const double* xu,
                         const double* yl, const double* yu, const void* band, int64_t n,
                         int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,

@@ -828,3 +828,26 @@ def test_fused_epsilon_self_join():
     rep = pb.epsilon_distance_join(P, P, eps, _collect("2d", k))
     assert rep.result_count == want["count"]
     assert np.array_equal(oracle.sorted_pairs(rep.pairs), oracle.sorted_pairs(want["pairs"]))
+
+
+def test_graph_replay_bit_exact_and_miss_fallback():
+    # the repeated-shape path as a CUDA graph: same pair set as the eager
+    # path; a different input with the same shape but larger lists misses
+    # the captured sizes and falls back to the exact path
+    r, s, k = make_config(2, 0.02)
+    R, S = dev.to_device(r), dev.to_device(s)
+    want = oracle.sorted_pairs(dev.run_join(R, S, k, k).pairs.cpu().numpy())
+    for _ in range(3):
+        res = dev.run_join(R, S, k, k, graph=True)
+        assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+    assert dev._graph_cache, "the graph path did not run"
+    # same sizes and grid, every rectangle 3x wider: longer lists, more pairs
+    wide = (r[0], r[1], np.minimum(r[2] + 2 * (r[2] - r[1]) + 1e-4, 1.0), r[3],
+            np.minimum(r[4] + 2 * (r[4] - r[3]) + 1e-4, 1.0))
+    W = dev.to_device(wide)
+    got = dev.run_join(W, S, k, k, graph=True)
+    ref = oracle.join(wide, s, "2d", k)
+    assert got.count == ref["count"]
+    assert np.array_equal(oracle.sorted_pairs(got.pairs.cpu().numpy()),
+                          oracle.sorted_pairs(ref["pairs"]))
+    dev.release_buffers()

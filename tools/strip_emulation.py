@@ -36,12 +36,12 @@ for n in a.ns:
         rd = dev.to_device(rr, "cuda")
         sd = rd if self_join else dev.to_device(ss, "cuda")
         for _ in range(3):
-            res = dev.run_join(rd, sd, k, k, collect=True, row_lo=lo, row_hi=hi)
+            res = dev.run_join(rd, sd, k, k, collect=True, row_lo=lo, row_hi=hi, graph=True)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(a.steps):
-            res = dev.run_join(rd, sd, k, k, collect=True, row_lo=lo, row_hi=hi)
+            res = dev.run_join(rd, sd, k, k, collect=True, row_lo=lo, row_hi=hi, graph=True)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.steps
@@ -55,6 +55,7 @@ for n in a.ns:
                     "pairs": res.count, "a_r": res.header["a_r"], "a_s": res.header["a_s"],
                     "max_tile": res.header.get("max_tile"), "phases_ms": ph})
         del rd, sd, res
+        dev.release_buffers()
     t = max(p["ms"] for p in per)
     print(json.dumps({"config": a.config, "n": n, "projected_ms": t,
                       "projected_rects_per_s": n_tot / (t / 1e3),
