@@ -26,6 +26,7 @@ sorted pair list, tests/golden/full_truth.json); a mismatch exits 1.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -404,7 +405,10 @@ def main():
         if shared:
             dist.init_process_group("gloo")
         else:
-            dist.init_process_group("nccl", device_id=device)
+            # a stuck collective must fail the run, not hang the box
+            os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+            dist.init_process_group("nccl", device_id=device,
+                                    timeout=datetime.timedelta(seconds=120))
 
     spec = CONFIGS[args.config]
     r, s, k = make_config(args.config)
@@ -422,12 +426,10 @@ def main():
     def step(probe=None):
         # (repeated joins of the same resident inputs replay one CUDA graph;
         # the phase-probe pass runs the same launches eagerly)
+        # world > 1: the join's one collective (all_gather {pairs, A_R, A_S} →
+        # global pair offset) — inside the graph, from the device header
         res = dev.run_join(rd, sd, k, k, collect=True, row_lo=row_lo, row_hi=row_hi,
-                           probe=probe, graph=True)
-        if world > 1:
-            # the one collective: all_gather {pairs, A_R, A_S} → global pair offset
-            res.header["exchange"] = parallel.exchange_counts(
-                res.count, res.header["a_r"], res.header["a_s"], device=device)
+                           probe=probe, graph=True, exchange=world > 1)
         return res
 
     def barrier():

@@ -554,13 +554,29 @@ def _run_units(lib, r: DeviceRects, s: DeviceRects, kx: int, ky: int, row_lo: in
     return res
 
 
+def _with_exchange(res: DeviceJoinResult, exchange: bool) -> DeviceJoinResult:
+    """The eager path's count exchange (after its own header read)."""
+    if exchange and "exchange" not in res.header:
+        from .parallel import exchange_counts
+
+        res.header["exchange"] = exchange_counts(res.count, res.header["a_r"],
+                                                 res.header["a_s"], device=res_device(res))
+    return res
+
+
+def res_device(res: DeviceJoinResult):
+    return res.pairs.device if res.pairs is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+
+
 def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool = True,
              row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
              keep_counts: bool = False, probe: PhaseProbe | None = None,
              ordered: bool = False, nested_max: int = -1,
              bin_bytes: int | None = None, defer_map: bool = False,
              pipeline: str | None = None, sweep_min: int = -1,
-             eps: float | None = None, graph: bool = False) -> DeviceJoinResult:
+             eps: float | None = None, graph: bool = False,
+             exchange: bool = False) -> DeviceJoinResult:
     """Join two device-resident inputs over a ``kx × ky`` grid (rows [row_lo, row_hi)).
 
     Two device pipelines compute the same pair set: the tile-list pipeline
@@ -584,11 +600,33 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     scatters, bounded emit, header publish — as one CUDA graph, then one
     host sync; the returned ``pairs`` is then a view of the graph's output
     buffer, valid until the next graphed join of the same inputs.
+    ``exchange`` (strip-sharded joins, torch.distributed initialised): the
+    one collective of the join — every rank's {pair_count, A_R, A_S} — lands
+    in ``header["exchange"]`` (parallel.exchange_counts' dict).  On the graph
+    path it is an all_gather of the device header inside the graph, before
+    the single host read (no host round trip in between).
     ``eps``: ε-distance join (epsilon_distance_join, engine.py:326-353) —
     ``r``/``s`` hold points (``points_to_device``: xl, yl = px, py), each
     standing for its side-eps square; candidates are refined inside the
     mini-joins (pbsm_join_emit_eps), so the count is the refined count.
     """
+    res = _run_join_impl(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
+                         timing=timing, keep_counts=keep_counts, probe=probe, ordered=ordered,
+                         nested_max=nested_max, bin_bytes=bin_bytes, defer_map=defer_map,
+                         pipeline=pipeline, sweep_min=sweep_min, eps=eps, graph=graph,
+                         exchange=exchange)
+    return _with_exchange(res, exchange)
+
+
+def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool = True,
+             row_lo: int = 0, row_hi: int | None = None, timing: bool = False,
+             keep_counts: bool = False, probe: PhaseProbe | None = None,
+             ordered: bool = False, nested_max: int = -1,
+             bin_bytes: int | None = None, defer_map: bool = False,
+             pipeline: str | None = None, sweep_min: int = -1,
+             eps: float | None = None, graph: bool = False,
+             exchange: bool = False) -> DeviceJoinResult:
+    """run_join without the eager count exchange (see run_join)."""
     mark = probe.mark if probe is not None else (lambda name: None)
     lib = _native.load()
     if row_hi is None:
@@ -618,7 +656,7 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
         if guess is not None and not (_binned(guess["list_r"], len(r), bin_bytes)
                                       or _binned(guess["list_s"], len(s), bin_bytes)):
             res = _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max,
-                               sweep_min, stream)
+                               sweep_min, stream, exchange)
             if res is not None:
                 return res
     ws = _workspace(lib, device, kx, ky, row_lo, row_hi, stream)
@@ -869,6 +907,9 @@ def sort_pairs(pairs: torch.Tensor) -> torch.Tensor:
 # the ~12 launches and their host work (~100 µs of Python + driver calls per
 # join, the whole cost of a near-empty join) become one graph launch.
 GRAPHS = os.environ.get("PBSM_GRAPHS", "1") != "0"
+# tests: capture the header all_gather even on a one-rank group (the
+# collective path of a multi-GPU run, exercised on one GPU)
+GRAPH_EXCHANGE_ALWAYS = os.environ.get("PBSM_GRAPH_EXCHANGE_ALWAYS") == "1"
 _graph_cache: dict = {}
 
 
@@ -878,6 +919,26 @@ class _Graphed:
         self.hdr = None      # page-locked header the graph's last kernel writes
         self.pairs = None
         self.keep = []       # buffers the graph's kernels address
+        self.gathered = None  # page-locked (world, HDR_WORDS + 5): every rank's header + caps
+        self.world = 1
+
+
+HDR_WORDS = C.sizeof(_native.Header) // 8
+_CAPS = ("list_r", "list_s", "nested", "other", "pairs")
+
+
+def _guess_missed(h: dict, caps) -> bool:
+    """Did a join sized from the speculative ``caps`` (list_r, list_s, nested
+    chunks, other units, pairs) miss its true plan ``h``?"""
+    return bool(h["list_r"] > caps[0] or h["list_s"] > caps[1] or h["chunks_nested"] > caps[2]
+                or h["chunks_sorted"] + h["n_items"] > caps[3] or h["pairs"] > caps[4]
+                or h["error"] & (_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW))
+
+
+def _header_row(row) -> dict:
+    """An int64 row of HDR_WORDS header words → the header dict."""
+    h = _native.Header.from_buffer_copy(bytes(memoryview(row[:HDR_WORDS].copy())))
+    return h.as_dict()
 
 
 def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess,
@@ -929,14 +990,38 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
                                              scratch.data_ptr(), g.pairs.data_ptr(), cap, stream),
                   "pbsm_join_emit_bounded")
     _native.check(lib.pbsm_publish_header(wsp, g.hdr.data_ptr(), stream), "pbsm_publish_header")
+    if g.gathered is not None:
+        # the join's one collective, from the device header (no host round
+        # trip): every rank's header words + the caps its graph was sized
+        # with, so every rank can tell whether ANY rank's sizes missed
+        import torch.distributed as dist
+
+        mine = torch.cat([ws[:8 * HDR_WORDS].view(torch.int64), g.caps])
+        allv = torch.empty((g.world, HDR_WORDS + len(_CAPS)), dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(allv, mine)
+        g.gathered.copy_(allv, non_blocking=True)
+        g.keep += [mine, allv]
 
 
 def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, sweep_min,
-                 stream) -> DeviceJoinResult | None:
+                 stream, exchange: bool = False) -> DeviceJoinResult | None:
     """run_join's repeated-shape path as a graph replay + one host sync.
     Returns None when the speculative sizes missed (the caller runs the
-    exact path, which refreshes the sizes)."""
+    exact path, which refreshes the sizes).  With ``exchange`` on several
+    ranks the graph also all-gathers the headers; then a miss on any rank is
+    handled here, identically on every rank: the ranks that missed re-run
+    their join exactly, and all ranks exchange their counts eagerly."""
     device = r.device
+    world, rank = 1, 0
+    if exchange:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            world, rank = dist.get_world_size(), dist.get_rank()
+    # (NCCL only: a gloo collective cannot be captured in a CUDA graph — the
+    # eager exchange after the read serves those groups)
+    gathered = exchange and dist.is_initialized() and dist.get_backend() == "nccl" and (
+        world > 1 or GRAPH_EXCHANGE_ALWAYS)
     gkey = key + tuple(t.data_ptr() for t in r.columns() + s.columns()) + (
         tuple(sorted(guess.items())),)
     with _state_lock:
@@ -946,7 +1031,12 @@ def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, swee
             for k_ in [k_ for k_ in _graph_cache if k_[:2] == key[:2]]:
                 del _graph_cache[k_]
         g = _Graphed()
+        g.world = world
         g.hdr = torch.zeros(C.sizeof(_native.Header), dtype=torch.uint8, pin_memory=True)
+        if gathered:
+            g.gathered = torch.zeros((world, HDR_WORDS + len(_CAPS)), dtype=torch.int64,
+                                     pin_memory=True)
+            g.caps = torch.tensor([guess[c] for c in _CAPS], dtype=torch.int64).to(device)
         g.graph = torch.cuda.CUDAGraph()
         cap_stream = torch.cuda.Stream(device)
         side_st = torch.cuda.Stream(device)
@@ -964,14 +1054,29 @@ def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, swee
     for bit, msg in _VALIDATION:
         if h2.error & bit:
             raise ValueError(msg)
-    miss = (h2.list_r > guess["list_r"] or h2.list_s > guess["list_s"]
-            or h2.chunks_nested > guess["nested"]
-            or h2.chunks_sorted + h2.n_items > guess["other"] or h2.pairs > guess["pairs"]
-            or h2.error & (_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW))
+    miss = _guess_missed(h2.as_dict(), [guess[c] for c in _CAPS])
     if miss:
         with _state_lock:
             _graph_cache.pop(gkey, None)
             _plan_cache.pop(key, None)
+    if g.gathered is not None:
+        rows = g.gathered.numpy().copy()
+        misses = [_guess_missed(_header_row(rw), rw[HDR_WORDS:]) for rw in rows]
+        if any(misses):  # (every rank sees the same rows: the same branch everywhere)
+            if miss:
+                res = run_join(r, s, kx, ky, row_lo=row_lo, row_hi=row_hi,
+                               nested_max=nested_max, sweep_min=sweep_min)
+            else:
+                res = DeviceJoinResult(int(h2.pairs), g.pairs[:int(h2.pairs)],
+                                       header=h2.as_dict())
+            return _with_exchange(res, True)
+        from .parallel import exchange_from_rows
+
+        res = DeviceJoinResult(int(h2.pairs), g.pairs[:int(h2.pairs)], header=h2.as_dict())
+        res.header["exchange"] = exchange_from_rows(
+            [(int(rw[12]), int(rw[0]), int(rw[1])) for rw in rows], rank)
+        return res
+    if miss:
         return None
     bad = h2.error & ~_VALIDATION_BITS
     if bad:

@@ -139,7 +139,13 @@ def exchange_counts(count: int, a_r: int, a_s: int, device=None, group=None) -> 
         else:  # gloo (CPU ranks) has no all_gather_into_tensor
             dist.all_gather(list(allv.unbind(0)), mine, group=group)
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    v = allv.cpu().numpy()
+    return exchange_from_rows(allv.cpu().numpy().tolist(), rank)
+
+
+def exchange_from_rows(rows, rank: int) -> dict:
+    """Every rank's (pair_count, A_R, A_S) → this rank's global pair offset
+    and the totals (the exclusive prefix of the pair counts)."""
+    v = np.asarray(rows, dtype=np.int64).reshape(-1, 3)
     offs = np.concatenate([[0], np.cumsum(v[:, 0])])
     return {"pair_offset": int(offs[rank]), "pairs": int(offs[-1]),
             "a_r": int(v[:, 1].sum()), "a_s": int(v[:, 2].sum()),
@@ -419,21 +425,25 @@ def gather_pairs(pairs, exchange: dict, dst: int = 0, group=None):
     counts = exchange["per_rank_pairs"]
     if len(pairs) != counts[rank]:
         raise ValueError(f"rank {rank}: {len(pairs)} pairs, the exchange says {counts[rank]}")
+    # (gloo moves host memory only: device shards go through the host there)
+    via_host = pairs.is_cuda and dist.get_backend(group) != "nccl"
     if rank != dst:
         if counts[rank]:
-            dist.send(pairs.contiguous(), dist.get_global_rank(group, dst)
-                      if group is not None else dst, group=group)
+            dist.send(pairs.contiguous().cpu() if via_host else pairs.contiguous(),
+                      dist.get_global_rank(group, dst) if group is not None else dst,
+                      group=group)
         return None
     offs = np.concatenate([[0], np.cumsum(counts)])
-    out = torch.empty((int(offs[-1]), 2), dtype=torch.int64, device=pairs.device)
-    out[offs[rank]:offs[rank + 1]] = pairs
+    out = torch.empty((int(offs[-1]), 2), dtype=torch.int64,
+                      device="cpu" if via_host else pairs.device)
+    out[offs[rank]:offs[rank + 1]] = pairs.cpu() if via_host else pairs
     ops = [dist.P2POp(dist.irecv, out[offs[g]:offs[g + 1]],
                       dist.get_global_rank(group, g) if group is not None else g, group=group)
            for g in range(world) if g != rank and counts[g]]
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
-    return out
+    return out.to(pairs.device) if via_host else out
 
 
 def canonical_pairs(pairs):
