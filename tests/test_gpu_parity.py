@@ -851,3 +851,27 @@ def test_graph_replay_bit_exact_and_miss_fallback():
     assert np.array_equal(oracle.sorted_pairs(got.pairs.cpu().numpy()),
                           oracle.sorted_pairs(ref["pairs"]))
     dev.release_buffers()
+
+
+def test_cli_bench_grid_csv(tmp_path, golden, capsys):
+    """`python -m paper_1908_11740_b200 bench` (cli.py:161-193 in the
+    reference): one CSV row per (layout, k, axis, threads, rep), every row
+    with the reference's result_count; an unknown layout is an error."""
+    from paper_1908_11740_b200 import cli
+    from paper_1908_11740_b200 import io as pio
+
+    g = golden["configs"]
+    r, s, k = make_config(1, float(g["cfg1_scale"]))
+    pio.save_mbr_binary(pb.RectBatch(*r), tmp_path / "r.bin")
+    pio.save_mbr_binary(pb.RectBatch(*s), tmp_path / "s.bin")
+    args = ["bench", "--left", str(tmp_path / "r.bin"), "--right", str(tmp_path / "s.bin"),
+            "--layout-list", "1d,2d", "--k-list", f"{k},auto", "--axis-list", "x,adaptive",
+            "--threads-list", "1,4", "--reps", "2"]
+    assert cli.main(args) == 0
+    lines = capsys.readouterr().out.strip().splitlines()
+    assert lines[0] == cli.CSV_HEADER
+    rows = [dict(zip(cli.CSV_HEADER.split(","), ln.split(","))) for ln in lines[1:]]
+    assert len(rows) == 2 * 2 * 2 * 2 * 2  # layouts x ks x axes x threads x reps
+    assert {int(rw["result_count"]) for rw in rows} == {int(g["cfg1_count"])}
+    assert {rw["layout"] for rw in rows} == {"1d", "2d"}
+    assert cli.main(args[:5] + ["--layout-list", "3d"]) == 1
