@@ -61,7 +61,7 @@ def parse():
                     help="cpu_baseline runs of the reference join: axis x|a(daptive) + "
                          "threads (N = physical cores), e.g. x1,xN,a1,aN")
     ap.add_argument("--sub-configs", default="5,3,4",
-                    help="other BASELINE configs timed in the same run (N=1), '' for none")
+                    help="other BASELINE configs timed in the same run (N=1), '' or none for none")
     ap.add_argument("--sub-steps", type=int, default=5)
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
@@ -594,11 +594,13 @@ def main():
                       "row_lo, row_hi) per rank (host strip split outside the timed region)"}
 
     subs = {}
-    if rank == 0 and world == 1 and args.sub_configs.strip():
+    sub_list = [x.strip() for x in args.sub_configs.split(",")
+                if x.strip() and x.strip().lower() != "none"]
+    if rank == 0 and world == 1 and sub_list:
         del rd, sd
         dev.release_buffers()
         torch.cuda.empty_cache()
-        for c in [int(x) for x in args.sub_configs.split(",") if x.strip()]:
+        for c in [int(x) for x in sub_list]:
             if c == args.config:
                 continue
             subs[f"cfg{c}"] = time_sub_config(c, args.sub_steps, device, hbm, args.no_parity)
