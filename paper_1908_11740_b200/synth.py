@@ -185,3 +185,17 @@ def make_config(cfg: int, scale: float = 1.0):
     r = make_side(cfg, "r", nr)
     s = r if spec.self_join else make_side(cfg, "s", ns)
     return r, s, spec.k
+
+
+def cfg4_points(n: int, seed: int, clustered: bool):
+    """The points cfg4's squares are built from: R uniform
+    (seed 0), S a 128-cluster mixture (seed 1) — as (ids, px, py) for the
+    ε-distance join (which takes the points, engine.py:326-353)."""
+    rng = np.random.default_rng(seed)
+    if clustered:
+        px, py = _mix(rng, 128, n, 0.005, 0.05)
+    else:
+        px = rng.random(n)
+        py = rng.random(n)
+    return (np.arange(n, dtype=np.int64), np.ascontiguousarray(px, dtype=np.float64),
+            np.ascontiguousarray(py, dtype=np.float64))
