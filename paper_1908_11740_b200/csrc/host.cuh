@@ -96,6 +96,20 @@ int set_smem_attrs() {
   e = cudaFuncSetAttribute(k_lsort_win, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kSortWindow * 12);
   if (e != cudaSuccess) return (int)e;
+#if PBSM_NESTED_PIPE
+  {
+    const int b = (int)sizeof(PipeSmem);
+    if ((e = cudaFuncSetAttribute(k_join_nested_pipe<true, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<true, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)))
+      return (int)e;
+  }
+#endif
   done.fetch_or(bit, std::memory_order_release);
   return 0;
 }
@@ -156,6 +170,22 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.g_tiles = fused_guard ? L.tiles : 0;
   A.eps = eps;
   A.eps_sq = eps_sq;
+#if PBSM_NESTED_PIPE
+  if (cn > 0 && !ordered) {
+    // persistent CTAs, two per SM, TMA-staged chunks (k_join_nested_pipe)
+    const unsigned g =
+        (unsigned)std::max<i64>(1, std::min<i64>(cn, (i64)num_sms() * PBSM_PIPE_CTAS));
+    const size_t sm = sizeof(PipeSmem);
+    if (eps) {
+      if (emit) k_join_nested_pipe<true, true><<<g, kNT, sm, s>>>(A, cn);
+      else k_join_nested_pipe<false, true><<<g, kNT, sm, s>>>(A, cn);
+    } else if (emit) {
+      k_join_nested_pipe<true, false><<<g, kNT, sm, s>>>(A, cn);
+    } else {
+      k_join_nested_pipe<false, false><<<g, kNT, sm, s>>>(A, cn);
+    }
+  } else
+#endif
   if (cn > 0) {
     // one CTA per chunk (the ordered look-back takes tickets in launch order)
     if (eps) {

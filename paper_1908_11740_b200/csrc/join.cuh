@@ -613,9 +613,36 @@ struct NestedSmem {
   u64 base;
 };
 
+// Staged-entry views for the nested tests: the cp.async-staged SoA buffer
+// (k_join_nested: {xl|label, xu}, {yl, yu}, id arrays + the ε-join's points)
+// or the raw 64-byte records a TMA bulk copy landed (k_join_nested_pipe).
+struct SoaView {
+  const NestedBuf& B;
+  const double2* ap;
+  __device__ __forceinline__ ulonglong2 ax(int i) const { return B.ax[i]; }
+  __device__ __forceinline__ double2 ay(int i) const { return B.ay[i]; }
+  __device__ __forceinline__ i64 id(int i) const { return B.aid[i]; }
+  __device__ __forceinline__ double2 pt(int i) const { return ap[i]; }
+  __device__ __forceinline__ uint4 jr(int t) const { return B.jr[t]; }
+};
+struct RecView {
+  const Rec* r;
+  const uint4* j;
+  __device__ __forceinline__ ulonglong2 ax(int i) const {
+    return *reinterpret_cast<const ulonglong2*>(&r[i].xl_key);
+  }
+  __device__ __forceinline__ double2 ay(int i) const {
+    return *reinterpret_cast<const double2*>(&r[i].yl);
+  }
+  __device__ __forceinline__ i64 id(int i) const { return r[i].id; }
+  __device__ __forceinline__ double2 pt(int i) const { return rec_point(r[i]); }
+  __device__ __forceinline__ uint4 jr(int t) const { return j[t]; }
+};
+
 // first tile of pair q0: binary search over the boundaries (the same
 // addresses in every lane: broadcast reads)
-__device__ __forceinline__ int nested_tile_of(const NestedSmem& S, int nt, u32 q0) {
+template <typename Smem>
+__device__ __forceinline__ int nested_tile_of(const Smem& S, int nt, u32 q0) {
   int lo = 0, hi = nt;  // last lt with tb[lt] <= q0
   while (hi - lo > 1) {
     const int m = (lo + hi) >> 1;
@@ -628,7 +655,8 @@ __device__ __forceinline__ int nested_tile_of(const NestedSmem& S, int nt, u32 q
 // boundaries (at most 31: tiles hold >= 1 pair and tb[lt] <= q0) become a
 // position bitmask, and lane L's tile is lt + (boundaries at positions <= L).
 // Returns lane's tile; advances lt to the tile of the step's last pair.
-__device__ __forceinline__ int nested_step_tile(const NestedSmem& S, int nt, u32 q0, int& lt,
+template <typename Smem>
+__device__ __forceinline__ int nested_step_tile(const Smem& S, int nt, u32 q0, int& lt,
                                                 int lane) {
   const int j = lt + 1 + lane;
   const u32 d = S.tb[j] - q0;  // tb[nt + 1 ..] = ~0
@@ -640,7 +668,8 @@ __device__ __forceinline__ int nested_step_tile(const NestedSmem& S, int nt, u32
 }
 
 // pair q (in tile t) → chunk-local positions of its r and s entries
-__device__ __forceinline__ void nested_pair(const NestedSmem& S, int t, u32 q, int& pr, int& ps) {
+template <typename Smem>
+__device__ __forceinline__ void nested_pair(const Smem& S, int t, u32 q, int& pr, int& ps) {
   const TileInfo ti = S.ti[t];
   const u32 local = q - ti.p0;
   // local / ns: local < 2^16 and |local/ns - integer| >= 0.5/ns, so the
@@ -650,9 +679,10 @@ __device__ __forceinline__ void nested_pair(const NestedSmem& S, int t, u32 q, i
   ps = (int)(ti.rs0 >> 16) + (int)(local - r * ti.ns);
 }
 
-__device__ __forceinline__ bool nested_hit(const NestedBuf& B, int pr, int ps) {
-  const ulonglong2 rx = B.ax[pr], sx = B.ax[ps];
-  const double2 ry = B.ay[pr], sy = B.ay[ps];
+template <typename View>
+__device__ __forceinline__ bool nested_hit(const View& B, int pr, int ps) {
+  const ulonglong2 rx = B.ax(pr), sx = B.ax(ps);
+  const double2 ry = B.ay(pr), sy = B.ay(ps);
   return pair_ok(rx.x, __longlong_as_double((long long)rx.y), ry.x, ry.y, sx.x,
                  __longlong_as_double((long long)sx.y), sy.x, sy.y);
 }
@@ -708,29 +738,29 @@ __device__ __forceinline__ void nested_stage(NestedBuf& B, double2* ap, const Jo
 // |R_T|*|S_T| <= 1024; <= 64 for any nested tile, |R_T|+|S_T| <= 128).  No per-pair index arithmetic; a warp runs max(|other|)
 // steps over its 32 lead entries.  body(hit, pr, ps, ballot) is called by
 // every lane of every step.
-template <bool EPS, typename Body>
-__device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf& B,
-                                            const double2* ap, double eps_sq, u32 e_beg,
-                                            u32 e_end, u32 e_step, int lane, Body&& body) {
+template <bool EPS, typename Smem, typename View, typename Body>
+__device__ __forceinline__ void nested_rows(const Smem& S, const View& B, double eps_sq,
+                                            u32 e_beg, u32 e_end, u32 e_step, int lane,
+                                            Body&& body) {
   for (u32 g = e_beg; g < e_end; g += e_step) {
     const u32 ei = g + lane;
     const bool valid = ei < e_end;
     const u32 d = valid ? S.lead[ei] : 0u;
     const u32 pos = d & 511u, o0 = (d >> 9) & 511u, nO = valid ? (d >> 18) & 127u : 0u;
     const bool lr = (d >> 25) & 1u;
-    const ulonglong2 mx = B.ax[pos];
-    const double2 my = B.ay[pos];
+    const ulonglong2 mx = B.ax(pos);
+    const double2 my = B.ay(pos);
     const double mxu = __longlong_as_double((long long)mx.y);
-    const double2 mp = EPS ? ap[pos] : make_double2(0.0, 0.0);
+    const double2 mp = EPS ? B.pt(pos) : make_double2(0.0, 0.0);
     const u32 steps = __reduce_max_sync(0xffffffffu, nO);
     for (u32 j = 0; j < steps; ++j) {
       bool hit = false;
       if (j < nO) {
-        const ulonglong2 ox = B.ax[o0 + j];
-        const double2 oy = B.ay[o0 + j];
+        const ulonglong2 ox = B.ax(o0 + j);
+        const double2 oy = B.ay(o0 + j);
         hit = pair_ok(mx.x, mxu, my.x, my.y, ox.x, __longlong_as_double((long long)ox.y), oy.x,
                       oy.y);
-        if (EPS) hit = hit && within_eps(mp, ap[o0 + j], eps_sq);
+        if (EPS) hit = hit && within_eps(mp, B.pt(o0 + j), eps_sq);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       body(hit, lr ? pos : o0 + j, lr ? o0 + j : pos, m);
@@ -740,10 +770,9 @@ __device__ __forceinline__ void nested_rows(const NestedSmem& S, const NestedBuf
 
 // Pair-flattened form (PBSM_NESTED_ROWS=0): every (r, s) pair of every tile
 // gets an index (tile-major, then r, then s); lane q of a warp-step tests pair q.
-template <bool EPS, typename Body>
-__device__ __forceinline__ void nested_flat(const NestedSmem& S, const NestedBuf& B,
-                                            const double2* ap, double eps_sq, int nt,
-                                            u32 q_beg, u32 q_end, int lt, int lane,
+template <bool EPS, typename Smem, typename View, typename Body>
+__device__ __forceinline__ void nested_flat(const Smem& S, const View& B, double eps_sq,
+                                            int nt, u32 q_beg, u32 q_end, int lt, int lane,
                                             Body&& body) {
   for (u32 q0 = q_beg; q0 < q_end; q0 += 32u) {
     const u32 q = q0 + lane;
@@ -753,16 +782,15 @@ __device__ __forceinline__ void nested_flat(const NestedSmem& S, const NestedBuf
     if (q < q_end) {
       nested_pair(S, t, q, pr, ps);
       hit = nested_hit(B, pr, ps);
-      if (EPS) hit = hit && within_eps(ap[pr], ap[ps], eps_sq);
+      if (EPS) hit = hit && within_eps(B.pt(pr), B.pt(ps), eps_sq);
     }
     body(hit, (u32)pr, (u32)ps, __ballot_sync(0xffffffffu, hit));
   }
 }
 
 // One staged chunk (B landed and visible): tables, count, reserve, emit.
-template <bool EMIT, bool EPS>
-__device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
-                                             const double2* ap, const JoinArgs& A,
+template <bool EMIT, bool EPS, typename Smem, typename View>
+__device__ __forceinline__ void nested_chunk(Smem& S, const View& B, const JoinArgs& A,
                                              const NestedChunk& k, i64 c) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = k.nt, NR = k.NR;
@@ -775,7 +803,7 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
 #pragma unroll
   for (int h = 0; h < kTPT; ++h) {
     const int t = kTPT * tid + h;
-    tr[h] = t < nt ? B.jr[t] : make_uint4(0, 0, 0, 0);
+    tr[h] = t < nt ? B.jr(t) : make_uint4(0, 0, 0, 0);
     w += PBSM_NESTED_ROWS ? max(tr[h].z, tr[h].w) : tr[h].z * tr[h].w;
   }
   u32 W;  // rows: lead entries of the chunk; flat: pairs of the chunk
@@ -822,8 +850,8 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     }
     wcnt += __popc(m);
   };
-  if (PBSM_NESTED_ROWS) nested_rows<EPS>(S, B, ap, A.eps_sq, w_beg, w_end, 32u * kW, lane, count);
-  else nested_flat<EPS>(S, B, ap, A.eps_sq, nt, w_beg, w_end, lt_beg, lane, count);
+  if (PBSM_NESTED_ROWS) nested_rows<EPS>(S, B, A.eps_sq, w_beg, w_end, 32u * kW, lane, count);
+  else nested_flat<EPS>(S, B, A.eps_sq, nt, w_beg, w_end, lt_beg, lane, count);
   if (lane == 0) S.wtot[warp] = wcnt;
   __syncthreads();
   if (tid == 0) {
@@ -854,19 +882,19 @@ __device__ __forceinline__ void nested_chunk(NestedSmem& S, const NestedBuf& B,
     for (u32 i = lane; i < wcnt; i += 32u) {
       const u32 v = S.hits[warp][i];
       *reinterpret_cast<longlong2*>(out + 2 * (i64)i) =
-          make_longlong2(B.aid[v & 0xffffu], B.aid[v >> 16]);
+          make_longlong2(B.id(v & 0xffffu), B.id(v >> 16));
     }
     return;
   }
   auto emit = [&](bool hit, u32 pr, u32 ps, unsigned m) {
     if (hit) {
       const i64 o = __popc(m & lt_mask);
-      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(B.aid[pr], B.aid[ps]);
+      *reinterpret_cast<longlong2*>(out + 2 * o) = make_longlong2(B.id(pr), B.id(ps));
     }
     out += 2 * (i64)__popc(m);
   };
-  if (PBSM_NESTED_ROWS) nested_rows<EPS>(S, B, ap, A.eps_sq, w_beg, w_end, 32u * kW, lane, emit);
-  else nested_flat<EPS>(S, B, ap, A.eps_sq, nt, w_beg, w_end, lt_beg, lane, emit);
+  if (PBSM_NESTED_ROWS) nested_rows<EPS>(S, B, A.eps_sq, w_beg, w_end, 32u * kW, lane, emit);
+  else nested_flat<EPS>(S, B, A.eps_sq, nt, w_beg, w_end, lt_beg, lane, emit);
 }
 
 // One CTA per chunk (chunks handed out by ticket in the ordered mode, whose
@@ -904,7 +932,104 @@ __global__ void __launch_bounds__(kNT, EPS ? 4 : PBSM_NESTED_MINB) k_join_nested
   nested_stage<EPS>(S.buf, s_pt, A, k);
   cp_async_wait_all();
   __syncthreads();
-  nested_chunk<EMIT, EPS>(S, S.buf, s_pt, A, k, c);
+  nested_chunk<EMIT, EPS>(S, SoaView{S.buf, s_pt}, A, k, c);
+}
+
+// ---- nested mini-joins, persistent + TMA-staged (the default for the
+// unordered emit): each CTA takes chunks blockIdx.x, + gridDim.x, ...
+// (static: no ticket).  A chunk's R range, S range and tile records are three
+// contiguous byte ranges (k_plan_apply), so one thread stages it with three
+// cp.async.bulk copies on a stage's mbarrier — no per-entry copies through the
+// load/store units (k_join_nested's 3 cp.async per entry: ~39 M lane
+// operations on cfg2) and no CTA launch per chunk — and the tests read the
+// 64-byte records in place (RecView).  Measured (r02z2, bench.py 10 steps):
+// 1 stage x 5 CTAs per SM beats the per-chunk kernel (cfg2 join 368 -> 333 µs,
+// cfg5 262 -> 231, cfg3 3.15 -> 2.93 ms); 2-3 stages at 1-2 CTAs per SM and
+// smaller buckets at 6-7 CTAs per SM were slower — resident CTAs hide the
+// staging latency better than a deeper pipeline.
+#ifndef PBSM_NESTED_PIPE
+#define PBSM_NESTED_PIPE 1
+#endif
+#ifndef PBSM_PIPE_STAGES
+#define PBSM_PIPE_STAGES 1
+#endif
+#ifndef PBSM_PIPE_CTAS
+#define PBSM_PIPE_CTAS 5  // resident CTAs per SM (the grid: this many per SM)
+#endif
+constexpr int kPipeStages = PBSM_PIPE_STAGES;
+struct PipeStage {
+  Rec recs[kCapN];         // R range, then S range
+  uint4 jr[kMaxTilesN];    // tile records
+};
+struct PipeSmem {
+  PipeStage st[kPipeStages];
+  u64 bar[kPipeStages];
+  NestedChunk k[kPipeStages];
+  // nested_chunk's working set (the names of NestedSmem)
+  u32 lead[PBSM_NESTED_ROWS ? kCapN : 1];
+  TileInfo ti[PBSM_NESTED_ROWS ? 1 : kMaxTilesN];
+  u32 tb[PBSM_NESTED_ROWS ? 1 : kMaxTilesN + 33];
+  u64 wtot[kNT / 32 + 1];
+  u32 scan32[kNT / 32 + 1];
+  u32 hits[kNT / 32][kHitCap];
+  u64 base;
+};
+
+// thread 0: chunk c's descriptors → stage s, its three bulk copies
+__device__ __forceinline__ void pipe_issue(PipeSmem& S, const JoinArgs& A, int s, i64 c) {
+  NestedChunk k = nested_desc(A, c);
+  if (!k.ok) {
+    atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
+    k.nt = k.NR = k.NS = 0;
+  }
+  S.k[s] = k;
+  const u32 rb = (u32)k.NR * (u32)sizeof(Rec), sb = (u32)k.NS * (u32)sizeof(Rec);
+  const u32 tb = (u32)k.nt * 16u;
+  mbar_expect_tx(&S.bar[s], rb + sb + tb);
+  if (rb) bulk_g2s(&S.st[s].recs[0], A.rl + k.d0.y, rb, &S.bar[s]);
+  if (sb) bulk_g2s(&S.st[s].recs[k.NR], A.sl + k.d0.z, sb, &S.bar[s]);
+  if (tb) bulk_g2s(&S.st[s].jr[0], A.jrec[0] + k.d0.x, tb, &S.bar[s]);
+}
+
+template <bool EMIT, bool EPS>
+__global__ void __launch_bounds__(kNT, PBSM_PIPE_CTAS) k_join_nested_pipe(JoinArgs A,
+                                                                          i64 n_chunks) {
+  extern __shared__ __align__(128) unsigned char pipe_raw[];
+  PipeSmem& S = *reinterpret_cast<PipeSmem*>(pipe_raw);
+  const int tid = threadIdx.x;
+  const i64 n_plan = A.bounded ? (i64)A.hdr->chunks_nested : n_chunks;
+  const bool over = A.bounded && lists_overflow(A);
+  if (tid == 0) {
+    for (int q = 0; q < kPipeStages; ++q) mbar_init(&S.bar[q], 1);
+    if (!over)
+      for (int q = 0; q < kPipeStages; ++q) {
+        const i64 c = blockIdx.x + (i64)q * gridDim.x;
+        if (c < n_plan) pipe_issue(S, A, q, c);
+      }
+  }
+  if (A.g_tiles) {  // the write guard, a grid-stride slice per CTA (all CTAs)
+    bool bad = false;
+    for (u64 t = blockIdx.x * (u64)kNT + tid; t < A.g_tiles; t += (u64)gridDim.x * kNT)
+      bad |= !cursor_done(A.g_cur_r[t], A.g_end_r[t]) || !cursor_done(A.g_cur_s[t], A.g_end_s[t]);
+    if (bad) atomicOr(&A.hdr->error, PBSM_ERR_OFFSET_MISMATCH);
+  }
+  __syncthreads();
+  if (over) return;
+  u32 phase = 0;  // bit q: the parity stage q waits for next
+  for (i64 it = 0;; ++it) {
+    const i64 c = blockIdx.x + it * gridDim.x;
+    if (c >= n_plan) break;
+    const int q = (int)(it % kPipeStages);
+    mbar_wait(&S.bar[q], (phase >> q) & 1u);
+    phase ^= 1u << q;
+    const NestedChunk k = S.k[q];
+    nested_chunk<EMIT, EPS>(S, RecView{S.st[q].recs, S.st[q].jr}, A, k, c);
+    __syncthreads();  // stage q consumed
+    if (tid == 0) {
+      const i64 cn = c + (i64)kPipeStages * gridDim.x;
+      if (cn < n_plan) pipe_issue(S, A, q, cn);
+    }
+  }
 }
 
 template <bool EMIT>
