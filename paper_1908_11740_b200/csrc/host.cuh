@@ -217,6 +217,25 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
     // the sorted/large launch keeps its own ticket (the look-back ids follow
     // the nested chunks', whose kernel has finished by then)
     if (ordered) cudaMemsetAsync(scratch, 0, 4, s);
+#if PBSM_JOIN_PDL && PBSM_NESTED_PIPE
+    // right behind the persistent nested kernel (nothing between them: no
+    // huge-tile sort, no ordered ticket reset): start while it drains
+    if (!ordered && cn > 0 && !(lcap > 0 && mtile > 0)) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)rest);
+      cfg.blockDim = dim3(kJoinThreads);
+      cfg.dynamicSmemBytes = sizeof(JoinSmem);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = emit ? cudaLaunchKernelEx(&cfg, k_join<true>, A)
+                                 : cudaLaunchKernelEx(&cfg, k_join<false>, A);
+      return e == cudaSuccess ? launch_status() : (int)e;
+    }
+#endif
     if (emit)
       k_join<true><<<(unsigned)rest, kJoinThreads, sizeof(JoinSmem), s>>>(A);
     else

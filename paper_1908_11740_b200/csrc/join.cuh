@@ -997,6 +997,12 @@ __global__ void __launch_bounds__(kNT, PBSM_PIPE_CTAS) k_join_nested_pipe(JoinAr
   extern __shared__ __align__(128) unsigned char pipe_raw[];
   PipeSmem& S = *reinterpret_cast<PipeSmem*>(pipe_raw);
   const int tid = threadIdx.x;
+#if PBSM_JOIN_PDL
+  // the sorted / large units (k_join, launched with programmatic stream
+  // serialization) do not read anything this kernel writes: let them start
+  // as soon as SM slots free up, filling this kernel's tail
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   const i64 n_plan = A.bounded ? (i64)A.hdr->chunks_nested : n_chunks;
   const bool over = A.bounded && lists_overflow(A);
   if (tid == 0) {
@@ -1032,11 +1038,25 @@ __global__ void __launch_bounds__(kNT, PBSM_PIPE_CTAS) k_join_nested_pipe(JoinAr
   }
 }
 
-template <bool EMIT>
 #ifndef PBSM_JOIN_MINB
 #define PBSM_JOIN_MINB 2
 #endif
+template <bool EMIT>
+__device__ __forceinline__ void k_join_body(JoinArgs& A);
+
+// PBSM_JOIN_PDL (common.cuh): k_join may start while the nested-chunk kernel
+// still runs (programmatic dependent launch); every CTA waits for that grid
+// before it exits, so the work after k_join in the stream sees both done
+template <bool EMIT>
 __global__ void __launch_bounds__(kJoinThreads, PBSM_JOIN_MINB) k_join(JoinArgs A) {
+  k_join_body<EMIT>(A);
+#if PBSM_JOIN_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <bool EMIT>
+__device__ __forceinline__ void k_join_body(JoinArgs& A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   JoinSmem& U = *reinterpret_cast<JoinSmem*>(smem_raw);
   // ordered mode hands out units by ticket (launch order, for the look-back);
