@@ -132,7 +132,11 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   const i64 mtile = bounded ? max_tile : plan->max_huge;
   // the write guard (reads the cursors the scatter left behind) runs inside
   // the nested join when there is one, else as its own kernel
-  const bool fused_guard = cn > 0;
+  // (fused only when the nested grid is large enough that its grid-stride
+  // slice stays short: a small join over a large strip runs k_guard instead)
+  const i64 nested_ctas =
+      PBSM_NESTED_PIPE && !ordered ? std::min<i64>(cn, (i64)num_sms() * PBSM_PIPE_CTAS) : cn;
+  const bool fused_guard = cn > 0 && (i64)L.tiles <= nested_ctas * (i64)kNT * 32;
   if (!fused_guard) {
     const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
                                                                   (i64)num_sms() * 8));
