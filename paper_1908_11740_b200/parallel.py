@@ -293,22 +293,19 @@ def _unpack(rec):
         return (r[:, 0].contiguous(), f[:, 0].contiguous(), f[:, 2].contiguous(),
                 f[:, 1].contiguous(), f[:, 3].contiguous())
     from . import _native
-    from .device import _raw_stream
+    from .device import _ptr, _raw_stream
+    from .errors import DatasetError
 
     lib = _native.load()
     cols = [torch.empty(n, dtype=torch.int64, device=rec.device)] + [
         torch.empty(n, dtype=torch.float64, device=rec.device) for _ in range(4)]
     bad = torch.empty(1, dtype=torch.int32, device=rec.device)
-    ids, xl, xu, yl, yu = cols
-    _native.check(lib.pbsm_unpack_records(rec.data_ptr() if n else None, n, _ptr_or0(ids),
-                                          _ptr_or0(xl), _ptr_or0(xu), _ptr_or0(yl),
-                                          _ptr_or0(yu), bad.data_ptr(), _raw_stream(rec.device)),
+    _native.check(lib.pbsm_unpack_records(_ptr(rec), n, *(_ptr(c) for c in cols),
+                                          bad.data_ptr(), _raw_stream(rec.device)),
                   "pbsm_unpack_records")
+    if n and int(bad.item()):  # (routed records were validated rectangles: a bug guard)
+        raise DatasetError("distribute: a received record has a lower bound above its upper")
     return tuple(cols)
-
-
-def _ptr_or0(t):
-    return t.data_ptr() if t.numel() else 1  # (never dereferenced when n == 0)
 
 
 def distribute(cols, k: int, cuts, group=None):
