@@ -461,6 +461,7 @@ def main():
     t_local = start.elapsed_time(end) / 1e3
     # per-phase device times: the same K steps again, outside the timed
     # region (the phase events add host work between the launches)
+    step(dev.PhaseProbe())  # (the eager path's own buffers, allocated untimed)
     probe = dev.PhaseProbe()
     for _ in range(args.steps):
         step(probe)
@@ -496,7 +497,8 @@ def main():
     B_alg = 40 * (n_r + n_s) + 80 * (A_R + A_S) + 16 * P
     step_gbs = B_alg / step_s / 1e9
     # dominant kernel: the longest device phase
-    dev_phases = {k_: v for k_, v in phases.items() if not k_.startswith("header")}
+    dev_phases = {k_: v for k_, v in phases.items()
+                  if not k_.startswith("header") and k_ not in ("alloc", "start")}
     dom = max(dev_phases, key=dev_phases.get)
     h = res.header
     # algorithmic bytes of each phase, per SURVEY §8(d)'s per-unit figures

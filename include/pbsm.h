@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define PBSM_ABI_VERSION 9
+#define PBSM_ABI_VERSION 10
 
 /* library error codes (negative) */
 #define PBSM_E_ARG        (-1)  /* bad argument (null pointer, k out of range, ...) */
@@ -113,6 +113,8 @@ typedef struct pbsm_header {
   int64_t sweep_min;      /* large tiles with |R_T|*|S_T| above this are sorted +   */
                           /* swept, the others brute-forced (pbsm_plan)             */
   int64_t max_huge;       /* largest side of a sorted + swept tile                  */
+  int64_t nested_r;       /* R entries in nested tiles: the nested region of R's    */
+  int64_t nested_s;       /* list is positions [0, nested_r); same for S            */
   uint32_t error;         /* PBSM_ERR_* bits                                        */
   uint32_t pad;
 } pbsm_header;
@@ -183,6 +185,33 @@ int pbsm_scatter_points(const int64_t* ids, const double* px, const double* py, 
                         int32_t side, double half, void* ws, int32_t kx, int32_t ky,
                         int32_t row_lo, int32_t row_hi, pbsm_entry* out, int64_t capacity,
                         void* stream);
+
+/* Compact nested entries (the shipped driver's default where it applies):
+ * the NESTED region of each tile list (positions [0, header.nested_r /
+ * nested_s), every entry of a tile the nested mini-join tests) is written as
+ * one 32-byte sector per entry {xl | label, xu, yl, yu32 | row << 32} into
+ * rec32 — yu rounded toward zero to float32 and the entry's row index — and
+ * the sorted / large regions as 64-byte entries into out (ids, or rows if ids
+ * is NULL).  The scatter then stores one sector per nested entry instead of
+ * two.  pbsm_join_emit_split reads the compact entries: a y-test is decided by
+ * yu32 and the next float32 except inside that gap, where the exact yu is read
+ * from r_yu / s_yu (the input columns, by row); hit ids come from r_ids /
+ * s_ids by row (both NULL: the pairs hold row indices, map them with
+ * pbsm_map_ids).  Takes the host plan (exact grids) or plan = NULL and the
+ * bounds of pbsm_join_emit_bounded.  Unordered placement; not for ε-joins or
+ * the binned scatter; n < 2^32. */
+int pbsm_scatter_split(const int64_t* ids, const double* xl, const double* xu, const double* yl,
+                       const double* yu, int64_t n, int32_t side, void* ws, int32_t kx,
+                       int32_t ky, int32_t row_lo, int32_t row_hi, pbsm_entry* out,
+                       int64_t capacity, void* rec32, int64_t capacity32, void* stream);
+int pbsm_join_emit_split(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                         const pbsm_entry* r_list, int64_t r_capacity, const void* r32,
+                         int64_t r32_capacity, const double* r_yu, const int64_t* r_ids,
+                         const pbsm_entry* s_list, int64_t s_capacity, const void* s32,
+                         int64_t s32_capacity, const double* s_yu, const int64_t* s_ids,
+                         const pbsm_header* plan, int64_t max_nested_chunks,
+                         int64_t max_other_units, int64_t large_capacity, int64_t max_tile,
+                         void* scratch, int64_t* pairs, int64_t capacity, void* stream);
 
 /* Binned scatter (worth it when an input's tile lists are large, e.g. > 1 GB).
  * pbsm_bin copies the input's rectangles into row-band order — 256 bands of

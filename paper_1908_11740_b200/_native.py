@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 from .errors import KernelError
 
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 # error bits of pbsm_header.error (include/pbsm.h)
 ERR_SCATTER_OVERFLOW = 1
@@ -32,6 +32,7 @@ EXPORTED = (
     "pbsm_join_scratch_bytes", "pbsm_join_count", "pbsm_join_emit", "pbsm_join_emit_bounded",
     "pbsm_unpack_records", "pbsm_map_ids", "pbsm_group_pairs",
     "pbsm_count_points", "pbsm_scatter_points", "pbsm_join_count_eps", "pbsm_join_emit_eps",
+    "pbsm_scatter_split", "pbsm_join_emit_split",
     "pbsm_route_scratch_bytes", "pbsm_route_count", "pbsm_route_pack",
     "pbsm_sort_pairs_scratch_bytes", "pbsm_pair_digits", "pbsm_sort_pairs",
     "pbsm_partition_scratch_bytes", "pbsm_partition_count", "pbsm_partition_write",
@@ -51,6 +52,7 @@ class Header(C.Structure):
         ("chunks_sorted", C.c_int64), ("n_items", C.c_int64), ("pairs", C.c_int64),
         ("pair_bound", C.c_int64), ("max_tile", C.c_int64), ("large_r", C.c_int64),
         ("large_s", C.c_int64), ("sweep_min", C.c_int64), ("max_huge", C.c_int64),
+        ("nested_r", C.c_int64), ("nested_s", C.c_int64),
         ("error", C.c_uint32), ("pad", C.c_uint32),
     ]
 
@@ -122,6 +124,11 @@ _SIGNATURES = {
                                       C.c_double, _P]),
     "pbsm_join_emit_eps": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, C.POINTER(Header), _P,
                                      _P, _I64, _I32, C.c_double, _P]),
+    "pbsm_scatter_split": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _I32, _I32, _I32,
+                                     _P, _I64, _P, _I64, _P]),
+    "pbsm_join_emit_split": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P,
+                                       _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _I64, _I64,
+                                       _P, _P, _I64, _P]),
     "pbsm_route_scratch_bytes": (_I64, [_I64, _I32, _I32]),
     "pbsm_route_count": (C.c_int, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
     "pbsm_route_pack": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),

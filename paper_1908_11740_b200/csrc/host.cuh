@@ -98,15 +98,14 @@ int set_smem_attrs() {
   if (e != cudaSuccess) return (int)e;
 #if PBSM_NESTED_PIPE
   {
-    const int b = (int)sizeof(PipeSmem);
-    if ((e = cudaFuncSetAttribute(k_join_nested_pipe<true, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)) ||
-        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)) ||
-        (e = cudaFuncSetAttribute(k_join_nested_pipe<true, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)) ||
-        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b)))
+    const int b = (int)sizeof(PipeSmem<Rec>), b32 = (int)sizeof(PipeSmem<Half>);
+    const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if ((e = cudaFuncSetAttribute(k_join_nested_pipe<true, 0>, A, b)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 0>, A, b)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<true, 1>, A, b)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 1>, A, b)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<true, 2>, A, b32)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 2>, A, b32)))
       return (int)e;
   }
 #endif
@@ -114,11 +113,24 @@ int set_smem_attrs() {
   return 0;
 }
 
+// compact nested entries (SplitOut): the nested regions, their capacities,
+// the exact yu columns and the id columns (null: the pairs hold rows)
+struct SplitLists {
+  const void* r32;
+  const void* s32;
+  i64 cap_r, cap_s;
+  const double* r_yu;
+  const double* s_yu;
+  const i64* r_ids;
+  const i64* s_ids;
+};
+
 int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, int row_hi,
                 const pbsm_entry* r_list, const pbsm_entry* s_list, const pbsm_header* plan,
                 void* scratch, int64_t* pairs, i64 capacity, cudaStream_t s,
                 i64 max_nested = -1, i64 max_other = -1, i64 cap_r = -1, i64 cap_s = -1,
-                i64 large_cap = 0, i64 max_tile = 0, int eps = 0, double eps_sq = 0.0) {
+                i64 large_cap = 0, i64 max_tile = 0, int eps = 0, double eps_sq = 0.0,
+                const SplitLists* split = nullptr) {
   int rc = set_smem_attrs();
   if (rc) return rc;
   const WsLayout L = ws_layout(kx, ky, row_lo, row_hi);
@@ -174,19 +186,30 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.g_tiles = fused_guard ? L.tiles : 0;
   A.eps = eps;
   A.eps_sq = eps_sq;
+  A.r32 = split ? reinterpret_cast<const Half*>(split->r32) : nullptr;
+  A.s32 = split ? reinterpret_cast<const Half*>(split->s32) : nullptr;
+  A.cap32_r = split ? split->cap_r : 0;
+  A.cap32_s = split ? split->cap_s : 0;
+  A.r_yu = split ? split->r_yu : nullptr;
+  A.s_yu = split ? split->s_yu : nullptr;
+  A.r_ids = split ? split->r_ids : nullptr;
+  A.s_ids = split ? split->s_ids : nullptr;
 #if PBSM_NESTED_PIPE
   if (cn > 0 && !ordered) {
     // persistent CTAs, two per SM, TMA-staged chunks (k_join_nested_pipe)
     const unsigned g =
         (unsigned)std::max<i64>(1, std::min<i64>(cn, (i64)num_sms() * PBSM_PIPE_CTAS));
-    const size_t sm = sizeof(PipeSmem);
+    const size_t sm = sizeof(PipeSmem<Rec>), sm32 = sizeof(PipeSmem<Half>);
     if (eps) {
-      if (emit) k_join_nested_pipe<true, true><<<g, kNT, sm, s>>>(A, cn);
-      else k_join_nested_pipe<false, true><<<g, kNT, sm, s>>>(A, cn);
+      if (emit) k_join_nested_pipe<true, 1><<<g, kNT, sm, s>>>(A, cn);
+      else k_join_nested_pipe<false, 1><<<g, kNT, sm, s>>>(A, cn);
+    } else if (split) {
+      if (emit) k_join_nested_pipe<true, 2><<<g, kNT, sm32, s>>>(A, cn);
+      else k_join_nested_pipe<false, 2><<<g, kNT, sm32, s>>>(A, cn);
     } else if (emit) {
-      k_join_nested_pipe<true, false><<<g, kNT, sm, s>>>(A, cn);
+      k_join_nested_pipe<true, 0><<<g, kNT, sm, s>>>(A, cn);
     } else {
-      k_join_nested_pipe<false, false><<<g, kNT, sm, s>>>(A, cn);
+      k_join_nested_pipe<false, 0><<<g, kNT, sm, s>>>(A, cn);
     }
   } else
 #endif

@@ -34,6 +34,16 @@ struct JoinArgs {
   // are within sqrt(eps_sq); eps = 0: plain join
   int eps;
   double eps_sq;
+  // compact nested entries (SplitOut, partition.cuh): the nested region of
+  // each list as 32-byte sectors; the exact yu columns (for a y-test inside
+  // yu32's float32 gap) and the id columns (ids of the hits; null: rows)
+  const Half* r32;
+  const Half* s32;
+  i64 cap32_r, cap32_s;
+  const double* r_yu;
+  const double* s_yu;
+  const i64* r_ids;
+  const i64* s_ids;
 };
 
 // _refine_pairs (engine.py:201-206): dx*dx + dy*dy <= eps^2, every operation
@@ -125,7 +135,8 @@ __device__ u64 lookback_thread(u64* status, i64 unit, u64 count, pbsm_header* hd
 // sized from a previous plan — the scatter stopped at the capacity, so no unit
 // may stage entries: flag it (the caller re-runs with the exact plan) and exit.
 __device__ __forceinline__ bool lists_overflow(const JoinArgs& A) {
-  const bool over = A.hdr->list_r > A.list_cap_r || A.hdr->list_s > A.list_cap_s;
+  const bool over = A.hdr->list_r > A.list_cap_r || A.hdr->list_s > A.list_cap_s ||
+                    (A.r32 && (A.hdr->nested_r > A.cap32_r || A.hdr->nested_s > A.cap32_s));
   if (over && threadIdx.x == 0) atomicOr(&A.hdr->error, PBSM_ERR_SCATTER_OVERFLOW);
   return over;
 }
@@ -617,6 +628,7 @@ struct NestedSmem {
 // (k_join_nested: {xl|label, xu}, {yl, yu}, id arrays + the ε-join's points)
 // or the raw 64-byte records a TMA bulk copy landed (k_join_nested_pipe).
 struct SoaView {
+  static constexpr bool kRZ = false;
   const NestedBuf& B;
   const double2* ap;
   __device__ __forceinline__ ulonglong2 ax(int i) const { return B.ax[i]; }
@@ -626,6 +638,7 @@ struct SoaView {
   __device__ __forceinline__ uint4 jr(int t) const { return B.jr[t]; }
 };
 struct RecView {
+  static constexpr bool kRZ = false;
   const Rec* r;
   const uint4* j;
   __device__ __forceinline__ ulonglong2 ax(int i) const {
@@ -638,6 +651,63 @@ struct RecView {
   __device__ __forceinline__ double2 pt(int i) const { return rec_point(r[i]); }
   __device__ __forceinline__ uint4 jr(int t) const { return j[t]; }
 };
+// compact nested entries: {xl | label, xu, yl, yu32 | row << 32}; ay() gives
+// {yl, yu32}, yu32 <= yu < the next float32 (y-tests: rz_le)
+struct RecView32 {
+  static constexpr bool kRZ = true;
+  const Half* r;
+  const uint4* j;
+  int NR;  // entries [0, NR) are R's, the rest S's
+  const double* yu_r;
+  const double* yu_s;
+  const i64* ids_r;
+  const i64* ids_s;
+  __device__ __forceinline__ ulonglong2 ax(int i) const {
+    return *reinterpret_cast<const ulonglong2*>(&r[i].xl_key);
+  }
+  __device__ __forceinline__ u64 w3(int i) const {
+    return (u64)__double_as_longlong(r[i].yu);
+  }
+  __device__ __forceinline__ double2 ay(int i) const {
+    return make_double2(r[i].yl, (double)__uint_as_float((u32)w3(i)));
+  }
+  __device__ __forceinline__ double yl(int i) const { return r[i].yl; }
+  __device__ __forceinline__ double yu_exact(int i) const {
+    return __ldg((i < NR ? yu_r : yu_s) + (w3(i) >> 32));
+  }
+  __device__ __forceinline__ i64 id(int i) const {
+    const i64 row = (i64)(w3(i) >> 32);
+    const i64* ids = i < NR ? ids_r : ids_s;
+    return ids ? __ldg(ids + row) : row;
+  }
+  __device__ __forceinline__ double2 pt(int) const { return make_double2(0.0, 0.0); }
+  __device__ __forceinline__ uint4 jr(int t) const { return j[t]; }
+};
+
+// lo <= yu for an entry known by yu32 = RZ_float(yu): decided by yu32 and the
+// next float32 except inside that gap, where the exact yu is read (rare)
+template <typename View>
+__device__ __forceinline__ bool rz_le(double lo, double yu32, const View& B, int e) {
+  if (lo <= yu32) return true;
+  if (lo >= (double)__uint_as_float(__float_as_uint((float)yu32) + 1u)) return false;
+  return lo <= B.yu_exact(e);
+}
+
+// the full pair test (pair_ok) on two staged entries of any view
+template <typename View>
+__device__ __forceinline__ bool view_pair(const View& B, int a, int b) {
+  const ulonglong2 ax = B.ax(a), bx = B.ax(b);
+  const double2 ay = B.ay(a), by = B.ay(b);
+  if constexpr (!View::kRZ) {
+    return pair_ok(ax.x, __longlong_as_double((long long)ax.y), ay.x, ay.y, bx.x,
+                   __longlong_as_double((long long)bx.y), by.x, by.y);
+  } else {
+    const bool xy = (key_x(ax.x) <= __longlong_as_double((long long)bx.y)) &
+                    (key_x(bx.x) <= __longlong_as_double((long long)ax.y)) &
+                    (((ax.x & bx.x) & kLabelMask) == 0ull);
+    return xy && rz_le(ay.x, by.y, B, b) && rz_le(by.x, ay.y, B, a);
+  }
+}
 
 // first tile of pair q0: binary search over the boundaries (the same
 // addresses in every lane: broadcast reads)
@@ -681,6 +751,7 @@ __device__ __forceinline__ void nested_pair(const Smem& S, int t, u32 q, int& pr
 
 template <typename View>
 __device__ __forceinline__ bool nested_hit(const View& B, int pr, int ps) {
+  if constexpr (View::kRZ) return view_pair(B, pr, ps);
   const ulonglong2 rx = B.ax(pr), sx = B.ax(ps);
   const double2 ry = B.ay(pr), sy = B.ay(ps);
   return pair_ok(rx.x, __longlong_as_double((long long)rx.y), ry.x, ry.y, sx.x,
@@ -752,14 +823,41 @@ __device__ __forceinline__ void nested_rows(const Smem& S, const View& B, double
     const double2 my = B.ay(pos);
     const double mxu = __longlong_as_double((long long)mx.y);
     const double2 mp = EPS ? B.pt(pos) : make_double2(0.0, 0.0);
+    // compact entries: the lead's yl bracketed by float32 (tested against the
+    // partners' float32 yu), its yu32 and the next float32 as doubles (the
+    // partners' yl are tested against those) — no conversion per step
+    float l_dn = 0.f, l_up = 0.f;
+    double l_yu = 0.0, l_yu_next = 0.0;
+    if constexpr (View::kRZ) {
+      l_dn = __double2float_rd(my.x);
+      l_up = __double2float_ru(my.x);
+      const float v = __uint_as_float((u32)B.w3(pos));
+      l_yu = (double)v;
+      l_yu_next = (double)__uint_as_float(__float_as_uint(v) + 1u);
+    }
     const u32 steps = __reduce_max_sync(0xffffffffu, nO);
     for (u32 j = 0; j < steps; ++j) {
       bool hit = false;
       if (j < nO) {
         const ulonglong2 ox = B.ax(o0 + j);
-        const double2 oy = B.ay(o0 + j);
-        hit = pair_ok(mx.x, mxu, my.x, my.y, ox.x, __longlong_as_double((long long)ox.y), oy.x,
-                      oy.y);
+        if constexpr (View::kRZ) {
+          const double o_yl = B.yl(o0 + j);
+          const float o_yu = __uint_as_float((u32)B.w3(o0 + j));
+          hit = (key_x(mx.x) <= __longlong_as_double((long long)ox.y)) & (key_x(ox.x) <= mxu) &
+                (((mx.x & ox.x) & kLabelMask) == 0ull);
+          if (hit) {  // lead.yl <= other.yu and other.yu's float32 gap
+            if (l_dn > o_yu) hit = false;
+            else if (!(l_up <= o_yu)) hit = my.x <= B.yu_exact((int)(o0 + j));
+          }
+          if (hit) {  // other.yl <= lead.yu
+            if (o_yl >= l_yu_next) hit = false;
+            else if (!(o_yl <= l_yu)) hit = o_yl <= B.yu_exact((int)pos);
+          }
+        } else {
+          const double2 oy = B.ay(o0 + j);
+          hit = pair_ok(mx.x, mxu, my.x, my.y, ox.x, __longlong_as_double((long long)ox.y),
+                        oy.x, oy.y);
+        }
         if (EPS) hit = hit && within_eps(mp, B.pt(o0 + j), eps_sq);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
@@ -957,12 +1055,14 @@ __global__ void __launch_bounds__(kNT, EPS ? 4 : PBSM_NESTED_MINB) k_join_nested
 #define PBSM_PIPE_CTAS 5  // resident CTAs per SM (the grid: this many per SM)
 #endif
 constexpr int kPipeStages = PBSM_PIPE_STAGES;
+template <typename RecT>
 struct PipeStage {
-  Rec recs[kCapN];         // R range, then S range
+  RecT recs[kCapN];        // R range, then S range (64-byte records or compact sectors)
   uint4 jr[kMaxTilesN];    // tile records
 };
+template <typename RecT>
 struct PipeSmem {
-  PipeStage st[kPipeStages];
+  PipeStage<RecT> st[kPipeStages];
   u64 bar[kPipeStages];
   NestedChunk k[kPipeStages];
   // nested_chunk's working set (the names of NestedSmem)
@@ -976,26 +1076,41 @@ struct PipeSmem {
 };
 
 // thread 0: chunk c's descriptors → stage s, its three bulk copies
-__device__ __forceinline__ void pipe_issue(PipeSmem& S, const JoinArgs& A, int s, i64 c) {
+template <typename RecT>
+__device__ __forceinline__ void pipe_issue(PipeSmem<RecT>& S, const JoinArgs& A, int s, i64 c) {
   NestedChunk k = nested_desc(A, c);
   if (!k.ok) {
     atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
     k.nt = k.NR = k.NS = 0;
   }
   S.k[s] = k;
-  const u32 rb = (u32)k.NR * (u32)sizeof(Rec), sb = (u32)k.NS * (u32)sizeof(Rec);
+  const u32 rb = (u32)k.NR * (u32)sizeof(RecT), sb = (u32)k.NS * (u32)sizeof(RecT);
   const u32 tb = (u32)k.nt * 16u;
+  const RecT* rsrc;
+  const RecT* ssrc;
+  if constexpr (sizeof(RecT) == sizeof(Rec)) {
+    rsrc = A.rl + k.d0.y;
+    ssrc = A.sl + k.d0.z;
+  } else {
+    rsrc = A.r32 + k.d0.y;
+    ssrc = A.s32 + k.d0.z;
+  }
   mbar_expect_tx(&S.bar[s], rb + sb + tb);
-  if (rb) bulk_g2s(&S.st[s].recs[0], A.rl + k.d0.y, rb, &S.bar[s]);
-  if (sb) bulk_g2s(&S.st[s].recs[k.NR], A.sl + k.d0.z, sb, &S.bar[s]);
+  if (rb) bulk_g2s(&S.st[s].recs[0], rsrc, rb, &S.bar[s]);
+  if (sb) bulk_g2s(&S.st[s].recs[k.NR], ssrc, sb, &S.bar[s]);
   if (tb) bulk_g2s(&S.st[s].jr[0], A.jrec[0] + k.d0.x, tb, &S.bar[s]);
 }
 
-template <bool EMIT, bool EPS>
+// MODE 0: 64-byte records; 1: ε-join (64-byte records carrying the point);
+// 2: compact nested entries (RecView32)
+template <int MODE>
+using PipeRec = std::conditional_t<MODE == 2, Half, Rec>;
+template <bool EMIT, int MODE>
 __global__ void __launch_bounds__(kNT, PBSM_PIPE_CTAS) k_join_nested_pipe(JoinArgs A,
                                                                           i64 n_chunks) {
+  constexpr bool EPS = MODE == 1;
   extern __shared__ __align__(128) unsigned char pipe_raw[];
-  PipeSmem& S = *reinterpret_cast<PipeSmem*>(pipe_raw);
+  PipeSmem<PipeRec<MODE>>& S = *reinterpret_cast<PipeSmem<PipeRec<MODE>>*>(pipe_raw);
   const int tid = threadIdx.x;
 #if PBSM_JOIN_PDL
   // the sorted / large units (k_join, launched with programmatic stream
@@ -1029,7 +1144,11 @@ __global__ void __launch_bounds__(kNT, PBSM_PIPE_CTAS) k_join_nested_pipe(JoinAr
     mbar_wait(&S.bar[q], (phase >> q) & 1u);
     phase ^= 1u << q;
     const NestedChunk k = S.k[q];
-    nested_chunk<EMIT, EPS>(S, RecView{S.st[q].recs, S.st[q].jr}, A, k, c);
+    if constexpr (MODE == 2)
+      nested_chunk<EMIT, false>(S, RecView32{S.st[q].recs, S.st[q].jr, k.NR, A.r_yu, A.s_yu,
+                                             A.r_ids, A.s_ids}, A, k, c);
+    else
+      nested_chunk<EMIT, EPS>(S, RecView{S.st[q].recs, S.st[q].jr}, A, k, c);
     __syncthreads();  // stage q consumed
     if (tid == 0) {
       const i64 cn = c + (i64)kPipeStages * gridDim.x;

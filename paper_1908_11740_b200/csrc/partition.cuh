@@ -361,6 +361,43 @@ __device__ __forceinline__ void write_rec(Rec* r, u64 key, double xu, double yl,
   st256_hint(&r->id, (u64)id, 0ull, pt.x, pt.y, pol);
 }
 
+// Compact nested entries (the shipped driver's default where it applies):
+// the NESTED region of a tile list — positions [0, nested_end), every entry of
+// a tile the nested mini-join tests — is written as ONE 32-byte sector
+// {xl | label, xu, yl, yu32 | row << 32}: yu rounded toward zero to float32
+// (yu32 <= yu < next float32) and the entry's row index.  The scatter then
+// stores one sector per nested entry instead of two (the scatter is bound by
+// its scattered per-lane memory operations); the nested join
+// decides a y-test against yu32 and reads the exact yu from the input column
+// in the rare case it falls inside yu32's float32 gap, and looks the hit's id
+// up by row at the emit.  Sorted / large tiles keep the 64-byte record.
+struct SplitOut {
+  Half* rec32;            // null: one 64-byte format for every entry
+  i64 cap32;              // entries rec32 holds
+  const i64* nested_end;  // &hdr->nested_r / nested_s (written by the plan)
+};
+
+__device__ __forceinline__ u64 yu_row_word(double yu, i64 row) {
+  return ((u64)(u32)row << 32) | (u64)__float_as_uint(__double2float_rz(yu));
+}
+
+// one list entry at position p: a compact 32-byte sector in the nested
+// region (split format), else the 64-byte record; past a capacity → error bit
+__device__ __forceinline__ void put_entry(Rec* out, i64 capacity, const SplitOut& sp, u64 nend,
+                                          u32 p, u64 key, double xu, double yl, double yu,
+                                          i64 id, i64 row, u64 pol, ulonglong2 pt, u32& bad) {
+  if (sp.rec32 && (u64)p < nend) {
+    if ((i64)p < sp.cap32)
+      st256_hint(sp.rec32 + p, key, (u64)__double_as_longlong(xu),
+                 (u64)__double_as_longlong(yl), yu_row_word(yu, row), pol);
+    else
+      bad |= PBSM_ERR_SCATTER_OVERFLOW;
+    return;
+  }
+  if ((i64)p < capacity) write_rec(out + p, key, xu, yl, yu, id, pol, pt);
+  else bad |= PBSM_ERR_SCATTER_OVERFLOW;
+}
+
 // write_tiles (_kernels.pyx:61-98): copy each rectangle into every tile it
 // overlaps, labelled with its class there.  Only tiles where both inputs are
 // non-empty get a list (the others cannot produce a pair: build_task_queue
@@ -372,6 +409,7 @@ struct ScatterIn {
   const double *xl, *xu, *yl, *yu;
   const BRec* band;  // non-null: read the row-band copy instead
   double half;       // points mode: square half-side (see load_mbr)
+  SplitOut split;
   template <bool BANDED, bool PTS>
   __device__ __forceinline__ void load(i64 i, double& a, double& b, double& c, double& d,
                                        i64& id, ulonglong2& pt) const {
@@ -414,6 +452,7 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
                                                  i64 capacity, pbsm_header* hdr) {
   u32 bad = 0;
   const u64 pol = l2_evict_first_policy();
+  const u64 nend = in.split.rec32 ? (u64)__ldcg(in.split.nested_end) : 0ull;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   double pa = 0, pb = 0, pc = 0, pd = 0;
@@ -435,10 +474,9 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
     const int nc = c1 - c0 + 1, nr = r1 - r0 + 1;
     if (nc * nr == 1) {  // one tile: most rectangles
       const u32 p = cur_inc(cursor + (size_t)(r0 - row_lo) * kx + c0);
-      if (p < kSkip) {
-        if ((i64)p < capacity) write_rec(out + p, xk | ((r0 != rr0) ? kYOut : 0ull), b, c, d, id, pol, pt);
-        else bad |= PBSM_ERR_SCATTER_OVERFLOW;
-      }
+      if (p < kSkip)
+        put_entry(out, capacity, in.split, nend, p, xk | ((r0 != rr0) ? kYOut : 0ull), b, c, d,
+                  id, i, pol, pt, bad);
       continue;
     }
     if (nc <= 2 && nr <= 2) {
@@ -471,12 +509,8 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (q >= ns || pos[q] >= kSkip) continue;  // absent / not a join tile
-        if ((i64)pos[q] >= capacity) {
-          bad |= PBSM_ERR_SCATTER_OVERFLOW;
-          continue;
-        }
         const u64 key = xk | ((rows[q] != rr0) ? kYOut : 0ull) | ((cols[q] != c0) ? kXOut : 0ull);
-        write_rec(out + pos[q], key, b, c, d, id, pol, pt);
+        put_entry(out, capacity, in.split, nend, pos[q], key, b, c, d, id, i, pol, pt, bad);
       }
       continue;
     }
@@ -486,11 +520,8 @@ __global__ void __launch_bounds__(256, BANDED ? 4 : PBSM_SCAT_MINB) k_scatter(Sc
       for (int col = c0; col <= c1; ++col) {
         const u32 p = cur_inc(rowp + col);
         if (p >= kSkip) continue;  // not a join tile
-        if ((i64)p >= capacity) {
-          bad |= PBSM_ERR_SCATTER_OVERFLOW;
-          continue;
-        }
-        write_rec(out + p, xk | ylab | ((col != c0) ? kXOut : 0ull), b, c, d, id, pol, pt);
+        put_entry(out, capacity, in.split, nend, p, xk | ylab | ((col != c0) ? kXOut : 0ull), b,
+                  c, d, id, i, pol, pt, bad);
       }
     }
   }
@@ -719,6 +750,8 @@ __global__ void __launch_bounds__(kPartThreads) k_plan_partials(u64* __restrict_
     hdr->list_s = (i64)ls;
     hdr->large_r = (i64)c[L_LA];
     hdr->large_s = (i64)c[L_LB];
+    hdr->nested_r = (i64)c[L_NA];
+    hdr->nested_s = (i64)c[L_NB];
     // chunk counts and the closing descriptors (see k_plan_apply)
     const u64 wn = c[L_NA] + c[L_NB], ws = c[L_SA] + c[L_SB];
     const u64 chn = wn ? (wn - 1) / kChunkBN + 1 : 0, chs = ws ? (ws - 1) / kChunkB + 1 : 0;

@@ -195,13 +195,15 @@ static int scatter_impl(const int64_t* ids, const double* xl, const double* xu,
                         const double* yl, const double* yu, const void* band, int64_t n,
                         int32_t side, void* ws, int32_t kx, int32_t ky, int32_t row_lo,
                         int32_t row_hi, pbsm_entry* out, int64_t capacity, void* stream,
-                        double half = 0.0) {
+                        double half = 0.0, void* rec32 = nullptr, int64_t cap32 = 0) {
   Ws w = ws_bind(ws, ws_layout(kx, ky, row_lo, row_hi));
 #ifndef PBSM_SCAT_GRID
 #define PBSM_SCAT_GRID 32  // blocks per SM (swept 8-1000 on cfg2/cfg3: 32 best)
 #endif
   const i64 blocks = std::min<i64>((n + 255) / 256, (i64)num_sms() * PBSM_SCAT_GRID);
-  ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band), half};
+  const SplitOut sp{reinterpret_cast<Half*>(rec32), cap32,
+                    reinterpret_cast<const i64*>(side ? &w.hdr->nested_s : &w.hdr->nested_r)};
+  ScatterIn in{(const i64*)ids, xl, xu, yl, yu, reinterpret_cast<const BRec*>(band), half, sp};
   u32* cur = side ? w.cur_s : w.cur_r;
   Rec* o = reinterpret_cast<Rec*>(out);
   cudaStream_t s = as_stream(stream);
@@ -228,6 +230,19 @@ int pbsm_scatter(const int64_t* ids, const double* xl, const double* xu, const d
   if (!xl || !xu || !yl || !yu || (!out && capacity > 0)) return PBSM_E_ARG;
   return scatter_impl(ids, xl, xu, yl, yu, nullptr, n, side, ws, kx, ky, row_lo, row_hi, out,
                       capacity, stream);
+}
+
+int pbsm_scatter_split(const int64_t* ids, const double* xl, const double* xu, const double* yl,
+                       const double* yu, int64_t n, int32_t side, void* ws, int32_t kx,
+                       int32_t ky, int32_t row_lo, int32_t row_hi, pbsm_entry* out,
+                       int64_t capacity, void* rec32, int64_t capacity32, void* stream) {
+  if (!ws || !grid_ok(kx, ky, row_lo, row_hi) || n < 0 || (side != 0 && side != 1) ||
+      capacity < 0 || capacity32 < 0 || n > 0xffffffffll)
+    return PBSM_E_ARG;
+  if (n == 0) return 0;
+  if (!xl || !xu || !yl || !yu || (!out && capacity > 0) || !rec32) return PBSM_E_ARG;
+  return scatter_impl(ids, xl, xu, yl, yu, nullptr, n, side, ws, kx, ky, row_lo, row_hi, out,
+                      capacity, stream, 0.0, rec32, capacity32);
 }
 
 int pbsm_scatter_points(const int64_t* ids, const double* px, const double* py, int64_t n,
@@ -297,6 +312,35 @@ int pbsm_join_emit(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row
     return PBSM_E_ARG;
   return launch_join(true, ordered != 0, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan,
                      scratch, pairs, capacity, as_stream(stream));
+}
+
+int pbsm_join_emit_split(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
+                         const pbsm_entry* r_list, int64_t r_capacity, const void* r32,
+                         int64_t r32_capacity, const double* r_yu, const int64_t* r_ids,
+                         const pbsm_entry* s_list, int64_t s_capacity, const void* s32,
+                         int64_t s32_capacity, const double* s_yu, const int64_t* s_ids,
+                         const pbsm_header* plan, int64_t max_nested_chunks,
+                         int64_t max_other_units, int64_t large_capacity, int64_t max_tile,
+                         void* scratch, int64_t* pairs, int64_t capacity, void* stream) {
+#if !PBSM_NESTED_PIPE
+  return PBSM_E_ARG;  // the compact nested entries are read by the persistent nested join
+#endif
+  if (!ws || !scratch || !grid_ok(kx, ky, row_lo, row_hi) || capacity < 0 ||
+      (capacity > 0 && !pairs) || !r32 || !s32 || !r_yu || !s_yu || r32_capacity < 0 ||
+      s32_capacity < 0 || r_capacity < 0 || s_capacity < 0 || (!r_ids) != (!s_ids))
+    return PBSM_E_ARG;
+  if (!plan && (max_nested_chunks < 0 || max_other_units < 0 || max_nested_chunks > 0x7fffffff ||
+                max_other_units > 0x7fffffff || large_capacity < 0 || max_tile < 0))
+    return PBSM_E_ARG;
+  SplitLists sp{r32, s32, r32_capacity, s32_capacity, r_yu, s_yu,
+                reinterpret_cast<const i64*>(r_ids), reinterpret_cast<const i64*>(s_ids)};
+  if (plan)
+    return launch_join(true, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan, scratch,
+                       pairs, capacity, as_stream(stream), -1, -1, r_capacity, s_capacity, 0, 0,
+                       0, 0.0, &sp);
+  return launch_join(true, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, nullptr, scratch,
+                     pairs, capacity, as_stream(stream), max_nested_chunks, max_other_units,
+                     r_capacity, s_capacity, large_capacity, max_tile, 0, 0.0, &sp);
 }
 
 int pbsm_join_emit_bounded(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,

@@ -372,6 +372,26 @@ def _side_stream(device, stream: int):
         return st
 
 SPECULATE = os.environ.get("PBSM_SPECULATE", "1") != "0"
+# compact nested entries (pbsm_scatter_split / pbsm_join_emit_split): one
+# 32-byte sector per nested-tile entry instead of a 64-byte record.  The
+# scatter saves one scattered store per nested entry (cfg2: 545 -> 444 µs,
+# cfg3 4.76 -> 3.92 ms) but each emitted pair then gathers its two ids by row
+# (cfg2 join +35 µs, cfg3 +0.6 ms) — so it is used when the pairs are at most
+# SPLIT_PAIR_RATIO per nested entry (the previous join of the shape tells:
+# speculative sizes), or when the ids are still in flight anyway (every pair
+# is mapped afterwards).
+SPLIT = os.environ.get("PBSM_SPLIT", "1") != "0"
+SPLIT_PAIR_RATIO = float(os.environ.get("PBSM_SPLIT_PAIR_RATIO", 1.0))
+
+
+def _split_ok(collect, eps, binned, ordered, nest_r, nest_s, n_r, n_s, pairs_hint,
+              late) -> bool:
+    if not (SPLIT and collect and eps is None and not binned and not ordered
+            and nest_r + nest_s > 0 and max(n_r, n_s) < (1 << 32)):
+        return False
+    if late:
+        return True
+    return pairs_hint is not None and pairs_hint <= SPLIT_PAIR_RATIO * (nest_r + nest_s)
 # The unit pipeline (units.cuh) is parity-green but measured slower than the
 # tile-list pipeline on every BASELINE config: opt-in only.
 UNITS = os.environ.get("PBSM_UNITS", "0") == "1"
@@ -716,12 +736,18 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
         h = _read_header(lib, ws, stream)
         mark("header")
         list_r, list_s = h.list_r, h.list_s
+        nest_r, nest_s = h.nested_r, h.nested_s
     else:
         h = None
         list_r, list_s = guess["list_r"], guess["list_s"]
+        nest_r, nest_s = guess["nested_r"], guess["nested_s"]
 
     lists = []
-    dual_sc = DUAL and not (_binned(list_r, len(r), bin_bytes) or _binned(list_s, len(s), bin_bytes))
+    binned = _binned(list_r, len(r), bin_bytes) or _binned(list_s, len(s), bin_bytes)
+    dual_sc = DUAL and not binned
+    split = _split_ok(collect, eps, binned, ordered, nest_r, nest_s, len(r), len(s),
+                      guess["count"] if guess is not None else None, late)
+    split_bufs = []
     if dual_sc:
         fork = torch.cuda.Event()
         fork.record(main_st)
@@ -735,6 +761,23 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
                                                   half, wsp, *grid, ent.data_ptr(), total,
                                                   side_st.cuda_stream if (dual_sc and side)
                                                   else stream), "pbsm_scatter_points")
+            if dual_sc and side == 1:
+                join_ev = torch.cuda.Event()
+                join_ev.record(side_st)
+                main_st.wait_event(join_ev)
+            if side == 1:
+                mark("scatter")
+            lists.append(ent)
+            continue
+        if split:
+            n32 = max(nest_s if side else nest_r, 1)
+            rec32 = _buffer(device, f"rec32_{side}", (n32, 4), torch.int64, stream)
+            split_bufs.append((rec32, n32))
+            _native.check(lib.pbsm_scatter_split(ids_p, _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
+                                                 _ptr(b.yu), len(b), side, wsp, *grid,
+                                                 ent.data_ptr(), total, rec32.data_ptr(), n32,
+                                                 side_st.cuda_stream if (dual_sc and side)
+                                                 else stream), "pbsm_scatter_split")
             if dual_sc and side == 1:
                 join_ev = torch.cuda.Event()
                 join_ev.record(side_st)
@@ -780,16 +823,21 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
                           torch.uint8, stream)
         pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
         mark("alloc")
-        _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), list_r,
-                                                 sl.data_ptr(), list_s, cn, rest, lcap, mtile,
-                                                 scratch.data_ptr(), pairs.data_ptr(), cap,
-                                                 stream), "pbsm_join_emit_bounded")
+        if split:
+            _emit_split(lib, wsp, grid, rl, list_r, sl, list_s, split_bufs, r, s, late, None,
+                        (cn, rest, lcap, mtile), scratch, pairs, cap, stream)
+        else:
+            _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), list_r,
+                                                     sl.data_ptr(), list_s, cn, rest, lcap,
+                                                     mtile, scratch.data_ptr(), pairs.data_ptr(),
+                                                     cap, stream), "pbsm_join_emit_bounded")
         mark("join")
         h2 = _read_header(lib, ws, stream,
                           allow=_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW)
         mark("header2")
         if (h2.list_r > list_r or h2.list_s > list_s or h2.chunks_nested > cn
                 or h2.chunks_sorted + h2.n_items > rest or h2.pairs > cap
+                or (split and (h2.nested_r > nest_r or h2.nested_s > nest_s))
                 or h2.error & (_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW)):
             # another input behind the same shape: redo it with the exact plan
             with _state_lock:
@@ -839,6 +887,9 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
                                                      C.byref(h), scratch.data_ptr(),
                                                      pairs.data_ptr(), cap, int(ordered), eps_sq,
                                                      stream), "pbsm_join_emit_eps")
+            elif split:
+                _emit_split(lib, wsp, grid, rl, list_r, sl, list_s, split_bufs, r, s, late,
+                            C.byref(h), (-1, -1, 0, 0), scratch, pairs, cap, stream)
             else:
                 _native.check(lib.pbsm_join_emit(wsp, *grid, rl.data_ptr(), sl.data_ptr(),
                                                  C.byref(h), scratch.data_ptr(), pairs.data_ptr(),
@@ -861,7 +912,9 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
                                 "nested": h.chunks_nested,
                                 "other": h.chunks_sorted + h.n_items,
                                 "large": int(h.large_r + h.large_s),
-                                "max_huge": int(h.max_huge)}
+                                "max_huge": int(h.max_huge),
+                                "nested_r": int(h.nested_r), "nested_s": int(h.nested_s),
+                                "count": count}
     if ev:
         ev[2].record()
         ev[2].synchronize()
@@ -924,7 +977,7 @@ class _Graphed:
 
 
 HDR_WORDS = C.sizeof(_native.Header) // 8
-_CAPS = ("list_r", "list_s", "nested", "other", "pairs")
+_CAPS = ("list_r", "list_s", "nested", "other", "pairs", "nested_r", "nested_s")
 
 
 def _guess_missed(h: dict, caps) -> bool:
@@ -932,6 +985,7 @@ def _guess_missed(h: dict, caps) -> bool:
     chunks, other units, pairs) miss its true plan ``h``?"""
     return bool(h["list_r"] > caps[0] or h["list_s"] > caps[1] or h["chunks_nested"] > caps[2]
                 or h["chunks_sorted"] + h["n_items"] > caps[3] or h["pairs"] > caps[4]
+                or h["nested_r"] > caps[5] or h["nested_s"] > caps[6]
                 or h["error"] & (_native.ERR_PAIR_OVERFLOW | _native.ERR_SCATTER_OVERFLOW))
 
 
@@ -959,6 +1013,14 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
                           device=device)
     g.pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=device)
     g.keep += [ws, lists, scratch]
+    nest = (guess["nested_r"], guess["nested_s"])
+    split = _split_ok(True, None, False, False, nest[0], nest[1], len(r), len(s),
+                      guess["count"], False)
+    split_bufs = []
+    if split:
+        split_bufs = [(torch.empty((max(nest[q], 1), 4), dtype=torch.int64, device=device),
+                       max(nest[q], 1)) for q in range(2)]
+        g.keep.append(split_bufs)
 
     def fork():
         e = torch.cuda.Event()
@@ -980,15 +1042,26 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
     _native.check(lib.pbsm_plan(wsp, *grid, nested_max, sweep_min, stream), "pbsm_plan")
     fork()
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
-        _native.check(lib.pbsm_scatter(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
-                                       _ptr(b.yu), len(b), side, wsp, *grid,
-                                       lists[side].data_ptr(), total,
-                                       side_st.cuda_stream if side else stream), "pbsm_scatter")
+        st_ = side_st.cuda_stream if side else stream
+        if split:
+            rec32, n32 = split_bufs[side]
+            _native.check(lib.pbsm_scatter_split(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
+                                                 _ptr(b.yu), len(b), side, wsp, *grid,
+                                                 lists[side].data_ptr(), total, rec32.data_ptr(),
+                                                 n32, st_), "pbsm_scatter_split")
+        else:
+            _native.check(lib.pbsm_scatter(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
+                                           _ptr(b.yu), len(b), side, wsp, *grid,
+                                           lists[side].data_ptr(), total, st_), "pbsm_scatter")
     join()
-    _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, lists[0].data_ptr(), list_r,
-                                             lists[1].data_ptr(), list_s, cn, rest, lcap, mtile,
-                                             scratch.data_ptr(), g.pairs.data_ptr(), cap, stream),
-                  "pbsm_join_emit_bounded")
+    if split:
+        _emit_split(lib, wsp, grid, lists[0], list_r, lists[1], list_s, split_bufs, r, s, False,
+                    None, (cn, rest, lcap, mtile), scratch, g.pairs, cap, stream)
+    else:
+        _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, lists[0].data_ptr(), list_r,
+                                                 lists[1].data_ptr(), list_s, cn, rest, lcap,
+                                                 mtile, scratch.data_ptr(), g.pairs.data_ptr(),
+                                                 cap, stream), "pbsm_join_emit_bounded")
     _native.check(lib.pbsm_publish_header(wsp, g.hdr.data_ptr(), stream), "pbsm_publish_header")
     if g.gathered is not None:
         # the join's one collective, from the device header (no host round
@@ -1084,6 +1157,20 @@ def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, swee
                           "(partition write overflow check, partition.py:229-233)")
     count = int(h2.pairs)
     return DeviceJoinResult(count, g.pairs[:count], header=h2.as_dict())
+
+
+def _emit_split(lib, wsp, grid, rl, list_r, sl, list_s, split_bufs, r, s, late, plan, bounds,
+                scratch, pairs, cap, stream) -> None:
+    """pbsm_join_emit_split over the compact nested entries: the exact yu
+    columns by row, ids looked up at the emit (rows while the id columns are
+    still in flight: mapped after the join)."""
+    (r32, c32r), (s32, c32s) = split_bufs
+    cn, rest, lcap, mtile = bounds
+    _native.check(lib.pbsm_join_emit_split(
+        wsp, *grid, rl.data_ptr(), list_r, r32.data_ptr(), c32r, _ptr(r.yu),
+        None if late else _ptr(r.ids), sl.data_ptr(), list_s, s32.data_ptr(), c32s, _ptr(s.yu),
+        None if late else _ptr(s.ids), plan, cn, rest, lcap, mtile, scratch.data_ptr(),
+        pairs.data_ptr(), cap, stream), "pbsm_join_emit_split")
 
 
 def _map_ids(lib, pairs, count: int, r: DeviceRects, s: DeviceRects, cur, stream) -> None:

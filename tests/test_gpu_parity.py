@@ -875,3 +875,56 @@ def test_cli_bench_grid_csv(tmp_path, golden, capsys):
     assert {int(rw["result_count"]) for rw in rows} == {int(g["cfg1_count"])}
     assert {rw["layout"] for rw in rows} == {"1d", "2d"}
     assert cli.main(args[:5] + ["--layout-list", "3d"]) == 1
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 5])
+def test_compact_nested_entries_match_full_records(cfg):
+    # the compact 32-byte nested entries (yu as float32 + row; exact yu read in
+    # the float32 gap, ids looked up at the emit) vs the one-format pipeline,
+    # through the exact, speculative and graph paths
+    r, s, k = make_config(cfg, 0.03)
+    R = dev.to_device(r)
+    S = R if s is r else dev.to_device(s)
+    old = dev.SPLIT, dev.SPLIT_PAIR_RATIO
+    try:
+        dev.SPLIT = False
+        want = oracle.sorted_pairs(dev.run_join(R, S, k, k).pairs.cpu().numpy())
+        dev.release_buffers()
+        dev.SPLIT, dev.SPLIT_PAIR_RATIO = True, 1e9  # (every speculative join: compact)
+        for _ in range(3):
+            res = dev.run_join(R, S, k, k, graph=True)
+            assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+        assert res.header["nested_r"] > 0
+    finally:
+        dev.SPLIT, dev.SPLIT_PAIR_RATIO = old
+        dev.release_buffers()
+
+
+def test_compact_entries_float32_gap_ties():
+    # y bounds inside one float32 gap: yu and the partner's yl differ only in
+    # the low mantissa bits that float32 drops, both ways, so every y-test
+    # falls in the gap and must read the exact yu
+    n = 4000
+    rng = np.random.default_rng(9)
+    base = np.float32(0.3) + rng.integers(0, 1000, n).astype(np.float32) * np.float32(1e-4)
+    yu = base.astype(np.float64) + rng.integers(1, 1 << 20, n) * 2.0 ** -50
+    xl = rng.random(n) * 0.9
+    r = (np.arange(n, dtype=np.int64), xl, xl + 0.05, yu - 1e-3, yu)
+    # S starts exactly at, just above or just below R's yu (inside the gap)
+    d = rng.integers(-3, 4, n) * 2.0 ** -52
+    yl2 = np.clip(yu[rng.permutation(n)] + d, 0, 1)
+    xs = rng.random(n) * 0.9
+    s = (np.arange(n, dtype=np.int64) + 10 ** 6, xs, xs + 0.05, yl2, np.minimum(yl2 + 1e-3, 1))
+    want = oracle.join(r, s, "2d", 50)
+    R, S = dev.to_device(r), dev.to_device(s)
+    old = dev.SPLIT_PAIR_RATIO
+    try:
+        dev.SPLIT_PAIR_RATIO = 1e9
+        for _ in range(2):  # exact (64-byte), then speculative (compact)
+            res = dev.run_join(R, S, 50, 50)
+            assert res.count == want["count"]
+            assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()),
+                                  oracle.sorted_pairs(want["pairs"]))
+    finally:
+        dev.SPLIT_PAIR_RATIO = old
+        dev.release_buffers()
