@@ -198,8 +198,10 @@ int pbsm_scatter_points(const int64_t* ids, const double* px, const double* py, 
  * from r_yu / s_yu (the input columns, by row); hit ids come from r_ids /
  * s_ids by row (both NULL: the pairs hold row indices, map them with
  * pbsm_map_ids).  Takes the host plan (exact grids) or plan = NULL and the
- * bounds of pbsm_join_emit_bounded.  Unordered placement; not for ε-joins or
- * the binned scatter; n < 2^32. */
+ * bounds of pbsm_join_emit_bounded.  few_pairs != 0 (an occupancy hint: the
+ * join is expected to emit well under one pair per 4 entries) runs the
+ * nested join at 8 CTAs per SM instead of 6.  Unordered placement; not for
+ * ε-joins or the binned scatter; n < 2^32. */
 int pbsm_scatter_split(const int64_t* ids, const double* xl, const double* xu, const double* yl,
                        const double* yu, int64_t n, int32_t side, void* ws, int32_t kx,
                        int32_t ky, int32_t row_lo, int32_t row_hi, pbsm_entry* out,
@@ -211,7 +213,8 @@ int pbsm_join_emit_split(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32
                          int64_t s32_capacity, const double* s_yu, const int64_t* s_ids,
                          const pbsm_header* plan, int64_t max_nested_chunks,
                          int64_t max_other_units, int64_t large_capacity, int64_t max_tile,
-                         void* scratch, int64_t* pairs, int64_t capacity, void* stream);
+                         void* scratch, int64_t* pairs, int64_t capacity, int32_t few_pairs,
+                         void* stream);
 
 /* Binned scatter (worth it when an input's tile lists are large, e.g. > 1 GB).
  * pbsm_bin copies the input's rectangles into row-band order — 256 bands of

@@ -128,7 +128,7 @@ _SIGNATURES = {
                                      _P, _I64, _P, _I64, _P]),
     "pbsm_join_emit_split": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _P, _I64, _P, _P,
                                        _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _I64, _I64,
-                                       _P, _P, _I64, _P]),
+                                       _P, _P, _I64, _I32, _P]),
     "pbsm_route_scratch_bytes": (_I64, [_I64, _I32, _I32]),
     "pbsm_route_count": (C.c_int, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
     "pbsm_route_pack": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),

@@ -98,14 +98,16 @@ int set_smem_attrs() {
   if (e != cudaSuccess) return (int)e;
 #if PBSM_NESTED_PIPE
   {
-    const int b = (int)sizeof(PipeSmem<Rec>), b32 = (int)sizeof(PipeSmem<Half>);
+    const int b = (int)sizeof(PipeSmemM<0>), b32 = (int)sizeof(PipeSmemM<2>);
     const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
     if ((e = cudaFuncSetAttribute(k_join_nested_pipe<true, 0>, A, b)) ||
         (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 0>, A, b)) ||
         (e = cudaFuncSetAttribute(k_join_nested_pipe<true, 1>, A, b)) ||
         (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 1>, A, b)) ||
         (e = cudaFuncSetAttribute(k_join_nested_pipe<true, 2>, A, b32)) ||
-        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 2>, A, b32)))
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 2>, A, b32)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<true, 3>, A, b32)) ||
+        (e = cudaFuncSetAttribute(k_join_nested_pipe<false, 3>, A, b32)))
       return (int)e;
   }
 #endif
@@ -123,6 +125,7 @@ struct SplitLists {
   const double* s_yu;
   const i64* r_ids;
   const i64* s_ids;
+  int few_pairs;  // occupancy hint: the join emits few pairs per entry
 };
 
 int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, int row_hi,
@@ -147,7 +150,10 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   // (fused only when the nested grid is large enough that its grid-stride
   // slice stays short: a small join over a large strip runs k_guard instead)
   const i64 nested_ctas =
-      PBSM_NESTED_PIPE && !ordered ? std::min<i64>(cn, (i64)num_sms() * PBSM_PIPE_CTAS) : cn;
+      PBSM_NESTED_PIPE && !ordered
+          ? std::min<i64>(cn, (i64)num_sms() *
+                                  pipe_ctas(split ? (split->few_pairs ? 3 : 2) : eps ? 1 : 0))
+          : cn;
   const bool fused_guard = cn > 0 && (i64)L.tiles <= nested_ctas * (i64)kNT * 32;
   if (!fused_guard) {
     const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
@@ -197,15 +203,21 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
 #if PBSM_NESTED_PIPE
   if (cn > 0 && !ordered) {
     // persistent CTAs, two per SM, TMA-staged chunks (k_join_nested_pipe)
+    const int mode = split ? (split->few_pairs ? 3 : 2) : eps ? 1 : 0;
     const unsigned g =
-        (unsigned)std::max<i64>(1, std::min<i64>(cn, (i64)num_sms() * PBSM_PIPE_CTAS));
-    const size_t sm = sizeof(PipeSmem<Rec>), sm32 = sizeof(PipeSmem<Half>);
+        (unsigned)std::max<i64>(1, std::min<i64>(cn, (i64)num_sms() * pipe_ctas(mode)));
+    const size_t sm = sizeof(PipeSmemM<0>), sm32 = sizeof(PipeSmemM<2>);
     if (eps) {
       if (emit) k_join_nested_pipe<true, 1><<<g, kNT, sm, s>>>(A, cn);
       else k_join_nested_pipe<false, 1><<<g, kNT, sm, s>>>(A, cn);
     } else if (split) {
-      if (emit) k_join_nested_pipe<true, 2><<<g, kNT, sm32, s>>>(A, cn);
-      else k_join_nested_pipe<false, 2><<<g, kNT, sm32, s>>>(A, cn);
+      if (mode == 3) {
+        if (emit) k_join_nested_pipe<true, 3><<<g, kNT, sm32, s>>>(A, cn);
+        else k_join_nested_pipe<false, 3><<<g, kNT, sm32, s>>>(A, cn);
+      } else {
+        if (emit) k_join_nested_pipe<true, 2><<<g, kNT, sm32, s>>>(A, cn);
+        else k_join_nested_pipe<false, 2><<<g, kNT, sm32, s>>>(A, cn);
+      }
     } else if (emit) {
       k_join_nested_pipe<true, 0><<<g, kNT, sm, s>>>(A, cn);
     } else {

@@ -1054,13 +1054,32 @@ __global__ void __launch_bounds__(kNT, EPS ? 4 : PBSM_NESTED_MINB) k_join_nested
 #ifndef PBSM_PIPE_CTAS
 #define PBSM_PIPE_CTAS 5  // resident CTAs per SM (the grid: this many per SM)
 #endif
-constexpr int kPipeStages = PBSM_PIPE_STAGES;
+// the compact-entry instance (MODE 2: 32-byte sectors, half the staging)
+#ifndef PBSM_PIPE_STAGES32
+#define PBSM_PIPE_STAGES32 1
+#endif
+// MODE 2: 6 CTAs per SM (40 registers, no spills); MODE 3, the same kernel
+// for joins with few pairs per entry: 8 CTAs per SM (32 registers) — measured
+// (r02zr): cfg2 (0.17 pairs / entry) 1.124 -> 1.091 ms at 8, but cfg3 (0.37)
+// and cfg5 (0.48), whose emits do more, are faster at 6
+#ifndef PBSM_PIPE_CTAS32
+#define PBSM_PIPE_CTAS32 6
+#endif
+#ifndef PBSM_PIPE_CTAS32_FEW
+#define PBSM_PIPE_CTAS32_FEW 8
+#endif
+__host__ __device__ constexpr int pipe_stages(int mode) {
+  return mode >= 2 ? PBSM_PIPE_STAGES32 : PBSM_PIPE_STAGES;
+}
+__host__ __device__ constexpr int pipe_ctas(int mode) {
+  return mode == 3 ? PBSM_PIPE_CTAS32_FEW : mode == 2 ? PBSM_PIPE_CTAS32 : PBSM_PIPE_CTAS;
+}
 template <typename RecT>
 struct PipeStage {
   RecT recs[kCapN];        // R range, then S range (64-byte records or compact sectors)
   uint4 jr[kMaxTilesN];    // tile records
 };
-template <typename RecT>
+template <typename RecT, int kPipeStages>
 struct PipeSmem {
   PipeStage<RecT> st[kPipeStages];
   u64 bar[kPipeStages];
@@ -1076,8 +1095,9 @@ struct PipeSmem {
 };
 
 // thread 0: chunk c's descriptors → stage s, its three bulk copies
-template <typename RecT>
-__device__ __forceinline__ void pipe_issue(PipeSmem<RecT>& S, const JoinArgs& A, int s, i64 c) {
+template <typename RecT, int ST>
+__device__ __forceinline__ void pipe_issue(PipeSmem<RecT, ST>& S, const JoinArgs& A, int s,
+                                           i64 c) {
   NestedChunk k = nested_desc(A, c);
   if (!k.ok) {
     atomicOr(&A.hdr->error, PBSM_ERR_INTERNAL);
@@ -1102,15 +1122,18 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<RecT>& S, const JoinArgs& A,
 }
 
 // MODE 0: 64-byte records; 1: ε-join (64-byte records carrying the point);
-// 2: compact nested entries (RecView32)
+// 2, 3: compact nested entries (RecView32) at two occupancies
 template <int MODE>
-using PipeRec = std::conditional_t<MODE == 2, Half, Rec>;
+using PipeRec = std::conditional_t<MODE >= 2, Half, Rec>;
+template <int MODE>
+using PipeSmemM = PipeSmem<PipeRec<MODE>, pipe_stages(MODE)>;
 template <bool EMIT, int MODE>
-__global__ void __launch_bounds__(kNT, PBSM_PIPE_CTAS) k_join_nested_pipe(JoinArgs A,
-                                                                          i64 n_chunks) {
+__global__ void __launch_bounds__(kNT, pipe_ctas(MODE)) k_join_nested_pipe(JoinArgs A,
+                                                                           i64 n_chunks) {
   constexpr bool EPS = MODE == 1;
+  constexpr int kPipeStages = pipe_stages(MODE);
   extern __shared__ __align__(128) unsigned char pipe_raw[];
-  PipeSmem<PipeRec<MODE>>& S = *reinterpret_cast<PipeSmem<PipeRec<MODE>>*>(pipe_raw);
+  PipeSmemM<MODE>& S = *reinterpret_cast<PipeSmemM<MODE>*>(pipe_raw);
   const int tid = threadIdx.x;
 #if PBSM_JOIN_PDL
   // the sorted / large units (k_join, launched with programmatic stream
@@ -1144,7 +1167,7 @@ __global__ void __launch_bounds__(kNT, PBSM_PIPE_CTAS) k_join_nested_pipe(JoinAr
     mbar_wait(&S.bar[q], (phase >> q) & 1u);
     phase ^= 1u << q;
     const NestedChunk k = S.k[q];
-    if constexpr (MODE == 2)
+    if constexpr (MODE >= 2)
       nested_chunk<EMIT, false>(S, RecView32{S.st[q].recs, S.st[q].jr, k.NR, A.r_yu, A.s_yu,
                                              A.r_ids, A.s_ids}, A, k, c);
     else

@@ -321,7 +321,8 @@ int pbsm_join_emit_split(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32
                          int64_t s32_capacity, const double* s_yu, const int64_t* s_ids,
                          const pbsm_header* plan, int64_t max_nested_chunks,
                          int64_t max_other_units, int64_t large_capacity, int64_t max_tile,
-                         void* scratch, int64_t* pairs, int64_t capacity, void* stream) {
+                         void* scratch, int64_t* pairs, int64_t capacity, int32_t few_pairs,
+                         void* stream) {
 #if !PBSM_NESTED_PIPE
   return PBSM_E_ARG;  // the compact nested entries are read by the persistent nested join
 #endif
@@ -333,7 +334,8 @@ int pbsm_join_emit_split(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32
                 max_other_units > 0x7fffffff || large_capacity < 0 || max_tile < 0))
     return PBSM_E_ARG;
   SplitLists sp{r32, s32, r32_capacity, s32_capacity, r_yu, s_yu,
-                reinterpret_cast<const i64*>(r_ids), reinterpret_cast<const i64*>(s_ids)};
+                reinterpret_cast<const i64*>(r_ids), reinterpret_cast<const i64*>(s_ids),
+                few_pairs != 0};
   if (plan)
     return launch_join(true, false, ws, kx, ky, row_lo, row_hi, r_list, s_list, plan, scratch,
                        pairs, capacity, as_stream(stream), -1, -1, r_capacity, s_capacity, 0, 0,

@@ -825,7 +825,7 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
         mark("alloc")
         if split:
             _emit_split(lib, wsp, grid, rl, list_r, sl, list_s, split_bufs, r, s, late, None,
-                        (cn, rest, lcap, mtile), scratch, pairs, cap, stream)
+                        (cn, rest, lcap, mtile), scratch, pairs, cap, stream, guess["count"])
         else:
             _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, rl.data_ptr(), list_r,
                                                      sl.data_ptr(), list_s, cn, rest, lcap,
@@ -1056,7 +1056,7 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
     join()
     if split:
         _emit_split(lib, wsp, grid, lists[0], list_r, lists[1], list_s, split_bufs, r, s, False,
-                    None, (cn, rest, lcap, mtile), scratch, g.pairs, cap, stream)
+                    None, (cn, rest, lcap, mtile), scratch, g.pairs, cap, stream, guess["count"])
     else:
         _native.check(lib.pbsm_join_emit_bounded(wsp, *grid, lists[0].data_ptr(), list_r,
                                                  lists[1].data_ptr(), list_s, cn, rest, lcap,
@@ -1160,17 +1160,19 @@ def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, swee
 
 
 def _emit_split(lib, wsp, grid, rl, list_r, sl, list_s, split_bufs, r, s, late, plan, bounds,
-                scratch, pairs, cap, stream) -> None:
+                scratch, pairs, cap, stream, pairs_hint=None) -> None:
     """pbsm_join_emit_split over the compact nested entries: the exact yu
     columns by row, ids looked up at the emit (rows while the id columns are
     still in flight: mapped after the join)."""
     (r32, c32r), (s32, c32s) = split_bufs
     cn, rest, lcap, mtile = bounds
+    # occupancy hint: few pairs per entry (the previous join of the shape)
+    few = 1 if pairs_hint is not None and pairs_hint <= 0.25 * (c32r + c32s) else 0
     _native.check(lib.pbsm_join_emit_split(
         wsp, *grid, rl.data_ptr(), list_r, r32.data_ptr(), c32r, _ptr(r.yu),
         None if late else _ptr(r.ids), sl.data_ptr(), list_s, s32.data_ptr(), c32s, _ptr(s.yu),
         None if late else _ptr(s.ids), plan, cn, rest, lcap, mtile, scratch.data_ptr(),
-        pairs.data_ptr(), cap, stream), "pbsm_join_emit_split")
+        pairs.data_ptr(), cap, few, stream), "pbsm_join_emit_split")
 
 
 def _map_ids(lib, pairs, count: int, r: DeviceRects, s: DeviceRects, cur, stream) -> None:
