@@ -343,6 +343,18 @@ def _binned(total: int, n: int, bin_bytes: int | None) -> bool:
     return 64 * total > thresh and (bin_bytes == 0 or total >= 1.6 * n)
 
 
+def _binned_pair(list_r: int, list_s: int, n_r: int, n_s: int, bin_bytes: int | None,
+                 split: bool) -> bool:
+    """Whether either input goes through the row-band copy.  Compact nested
+    entries (``split``) halve the scattered bytes without the copy: with
+    BIN_LIST_BYTES' default they replace it (cfg4: 13.99 -> 12.94 ms,
+    profiles/r02zx_cfg4_bin_split_ab.txt); an explicit ``bin_bytes`` keeps
+    the row-band copy."""
+    if not (_binned(list_r, n_r, bin_bytes) or _binned(list_s, n_s, bin_bytes)):
+        return False
+    return not (split and bin_bytes is None)
+
+
 def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream, ids_p) -> torch.Tensor:
     """Row-band copy of one input: n 40-byte records {id (or row), xl, xu, yl, yu}."""
     band = torch.empty((len(b), 5), dtype=torch.int64, device=b.device)
@@ -673,8 +685,10 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
         key = (str(device), stream, kx, ky, row_lo, row_hi, len(r), len(s), s is r, nested_max,
                bin_bytes, sweep_min)
         guess = _plan_cache.get(key)
-        if guess is not None and not (_binned(guess["list_r"], len(r), bin_bytes)
-                                      or _binned(guess["list_s"], len(s), bin_bytes)):
+        if guess is not None and not _binned_pair(
+                guess["list_r"], guess["list_s"], len(r), len(s), bin_bytes,
+                _split_ok(True, None, False, False, guess["nested_r"], guess["nested_s"],
+                          len(r), len(s), guess["count"], False)):
             res = _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max,
                                sweep_min, stream, exchange)
             if res is not None:
@@ -743,10 +757,11 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
         nest_r, nest_s = guess["nested_r"], guess["nested_s"]
 
     lists = []
-    binned = _binned(list_r, len(r), bin_bytes) or _binned(list_s, len(s), bin_bytes)
-    dual_sc = DUAL and not binned
-    split = _split_ok(collect, eps, binned, ordered, nest_r, nest_s, len(r), len(s),
+    split = _split_ok(collect, eps, False, ordered, nest_r, nest_s, len(r), len(s),
                       guess["count"] if guess is not None else None, late)
+    binned = _binned_pair(list_r, list_s, len(r), len(s), bin_bytes, split)
+    split = split and not binned
+    dual_sc = DUAL and not binned
     split_bufs = []
     if dual_sc:
         fork = torch.cuda.Event()
