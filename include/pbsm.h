@@ -272,7 +272,9 @@ int pbsm_join_emit_eps(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t
 /* pbsm_join_emit without the host copy of the plan: the kernels read the
  * unit counts from the device header and the grids are the caller's upper
  * bounds (e.g. the previous join's counts), so the pipeline needs no host
- * sync between pbsm_plan and the emit.  Unordered placement only.
+ * sync between pbsm_plan and the emit.  Unordered placement only, and ONE
+ * bounded emit per pbsm_plan (the plan zeroes header.pairs; the bounded emit
+ * does not reset it).
  * r_capacity / s_capacity are the entries the tile-list buffers hold (the
  * capacities given to pbsm_scatter): if the plan's lists are longer, no unit
  * reads them and PBSM_ERR_SCATTER_OVERFLOW is set; likewise large_capacity

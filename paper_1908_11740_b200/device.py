@@ -260,6 +260,7 @@ def release_buffers() -> None:
         _ws_cache.clear()
         _plan_cache.clear()
         _graph_cache.clear()
+        _fast.clear()
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -642,6 +643,13 @@ def run_join(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect: bool 
     standing for its side-eps square; candidates are refined inside the
     mini-joins (pbsm_join_emit_eps), so the count is the refined count.
     """
+    if graph and _fast and FAST_REPLAY and collect and not (timing or keep_counts or ordered or defer_map
+                                            or exchange) \
+            and probe is None and pipeline is None and eps is None and len(r) and len(s):
+        res = _fast_replay(r, s, kx, ky, row_lo, ky if row_hi is None else row_hi, nested_max,
+                           bin_bytes, sweep_min)
+        if res is not None:
+            return res
     res = _run_join_impl(r, s, kx, ky, collect=collect, row_lo=row_lo, row_hi=row_hi,
                          timing=timing, keep_counts=keep_counts, probe=probe, ordered=ordered,
                          nested_max=nested_max, bin_bytes=bin_bytes, defer_map=defer_map,
@@ -989,6 +997,14 @@ class _Graphed:
         self.keep = []       # buffers the graph's kernels address
         self.gathered = None  # page-locked (world, HDR_WORDS + 5): every rank's header + caps
         self.world = 1
+        # fast replay (_fast_replay): the inputs this graph reads (kept alive:
+        # their ids key the lookup), their addresses, the header as int64
+        # words, the speculative caps, the last result's pair view
+        self.inputs = None
+        self.ptrs = ()
+        self.hdr_words = None
+        self.cap_list = ()
+        self.view = (-1, None)
 
 
 HDR_WORDS = C.sizeof(_native.Header) // 8
@@ -1121,6 +1137,10 @@ def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, swee
         g = _Graphed()
         g.world = world
         g.hdr = torch.zeros(C.sizeof(_native.Header), dtype=torch.uint8, pin_memory=True)
+        g.hdr_words = g.hdr.numpy().view(np.int64)
+        g.cap_list = [int(guess[c]) for c in _CAPS]
+        g.inputs = (r, s)
+        g.ptrs = tuple(t.data_ptr() for t in r.columns() + s.columns())
         if gathered:
             g.gathered = torch.zeros((world, HDR_WORDS + len(_CAPS)), dtype=torch.int64,
                                      pin_memory=True)
@@ -1147,6 +1167,7 @@ def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, swee
         with _state_lock:
             _graph_cache.pop(gkey, None)
             _plan_cache.pop(key, None)
+            _fast.pop(key[:2], None)
     if g.gathered is not None:
         rows = g.gathered.numpy().copy()
         misses = [_guess_missed(_header_row(rw), rw[HDR_WORDS:]) for rw in rows]
@@ -1171,7 +1192,62 @@ def _run_graphed(lib, r, s, kx, ky, row_lo, row_hi, key, guess, nested_max, swee
         raise KernelError(f"device guard: {_native.describe_error(bad)} "
                           "(partition write overflow check, partition.py:229-233)")
     count = int(h2.pairs)
+    if g.gathered is None:
+        with _state_lock:  # the next join of these inputs replays without the lookups above
+            _fast[key[:2]] = (_fast_key(r, s, key), g)
     return DeviceJoinResult(count, g.pairs[:count], header=h2.as_dict())
+
+
+# Fast replay.  Between two joins of a repeated shape the GPU idles while the
+# host works (tools/timeline.py: ~40 µs per join, a fifth of an 8-way strip's
+# step): the result of join i is decoded, run_join returns, is called again,
+# rebuilds its cache keys and launches the graph.  The last graphed join of a
+# (device, stream) is therefore remembered under a key of object identities;
+# a repeat skips every lookup and decodes the page-locked header straight
+# from its int64 words.  Anything unusual — an error bit, a size miss, other
+# options — drops the entry and takes the general path.
+_fast: dict = {}
+FAST_REPLAY = os.environ.get("PBSM_FAST_REPLAY", "1") != "0"
+_HDR_NAMES = tuple(n for n, _ in _native.Header._fields_ if n not in ("error", "pad"))
+_HDR_IX = {n: i for i, n in enumerate(_HDR_NAMES)}
+_MISS_IX = tuple(_HDR_IX[n] for n in ("list_r", "list_s", "chunks_nested", "chunks_sorted",
+                                      "n_items", "pairs", "nested_r", "nested_s"))
+
+
+def _fast_key(r, s, key) -> tuple:
+    return (id(r), id(s)) + key[2:]
+
+
+def _fast_replay(r, s, kx, ky, row_lo, row_hi, nested_max, bin_bytes, sweep_min):
+    device = r.device
+    ent = _fast.get((str(device), _raw_stream(device)))
+    if ent is None:
+        return None
+    fkey, g = ent
+    if fkey != (id(r), id(s), kx, ky, row_lo, row_hi, len(r), len(s), s is r, nested_max,
+                bin_bytes, sweep_min):
+        return None
+    if g.inputs[0] is not r or g.inputs[1] is not s or r.coords_ready is not None \
+            or s.coords_ready is not None or r.ids_ready is not None \
+            or g.ptrs != tuple(t.data_ptr() for t in r.columns() + s.columns()):
+        return None
+    g.graph.replay()
+    torch.cuda.current_stream(device).synchronize()
+    w = g.hdr_words.tolist()
+    v = [w[i] for i in _MISS_IX]
+    c = g.cap_list  # (_CAPS: list_r, list_s, nested, other, pairs, nested_r, nested_s)
+    if (w[-1] & 0xffffffff) or v[0] > c[0] or v[1] > c[1] or v[2] > c[2] or v[3] + v[4] > c[3] \
+            or v[5] > c[4] or v[6] > c[5] or v[7] > c[6]:
+        with _state_lock:
+            _fast.pop((str(device), _raw_stream(device)), None)
+        return None  # (the general path replays, reads the same header and handles it)
+    count = v[5]
+    if g.view[0] != count:
+        g.view = (count, g.pairs[:count])
+    h = dict(zip(_HDR_NAMES, w))
+    h["error"] = 0
+    h["n_units"] = v[2] + v[3] + v[4]
+    return DeviceJoinResult(count, g.view[1], header=h)
 
 
 def _emit_split(lib, wsp, grid, rl, list_r, sl, list_s, split_bufs, r, s, late, plan, bounds,
