@@ -358,24 +358,45 @@ __device__ __forceinline__ u32 large_pass(LargeSmem& S, int n, bool have, const 
   if (!have) return 0;
   const double mxl = key_x(me.xl_key);
   const bool mxin = !(me.xl_key & kXOut), myin = !(me.xl_key & kYOut);
-  for (int k = 0; k < n; ++k) {
+  // Branch-free test on both 16-byte halves of the record, four entries per
+  // step: with early-outs every iteration was its own load -> compare ->
+  // branch chain (shared-memory latency per test); here the eight loads and
+  // the compares of four entries are in flight together and the rare hits
+  // are handled after them.
+  auto test = [&](const Rec& o) -> bool {
+    const ulonglong2 ox = *reinterpret_cast<const ulonglong2*>(&o.xl_key);
+    const double2 oy = *reinterpret_cast<const double2*>(&o.yl);
+    const u64 ok = ox.x;
+    const double oxl = key_x(ok), oxu = __longlong_as_double((long long)ox.y);
+    return (mxl <= oxu) & (oxl <= me.xu) & (me.yl <= oy.y) & (oy.x <= me.yu) &
+           (mxin | !(ok & kXOut)) & (myin | !(ok & kYOut));
+  };
+  auto record = [&](int k) {
     const Rec& o = S.other[k];
-    const u64 ok = o.xl_key;
-    const double oxl = key_x(ok);
-    if (mxl <= o.xu && oxl <= me.xu && me.yl <= o.yu && o.yl <= me.yu &&
-        (mxin || !(ok & kXOut)) && (myin || !(ok & kYOut)) &&
-        (!eps || within_eps(mpt, rec_point(o), eps_sq))) {
-      if (EMIT) {
-        *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
-            lead_r ? make_longlong2(my_id, o.id) : make_longlong2(o.id, my_id);
-      }
-      if (LIST) {
-        const u32 h = atomicAdd_block(&S.nhit, 1u);
-        if (h < (u32)kLargeHitCap) S.hit[h] = threadIdx.x | ((k0 + (u32)k) << 8);
-      }
-      ++c;
+    if (eps && !within_eps(mpt, rec_point(o), eps_sq)) return;
+    if (EMIT) {
+      *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
+          lead_r ? make_longlong2(my_id, o.id) : make_longlong2(o.id, my_id);
+    }
+    if (LIST) {
+      const u32 h = atomicAdd_block(&S.nhit, 1u);
+      if (h < (u32)kLargeHitCap) S.hit[h] = threadIdx.x | ((k0 + (u32)k) << 8);
+    }
+    ++c;
+  };
+  int k = 0;
+  for (; k + 4 <= n; k += 4) {
+    bool h[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) h[u] = test(S.other[k + u]);
+    if (h[0] | h[1] | h[2] | h[3]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (h[u]) record(k + u);
     }
   }
+  for (; k < n; ++k)
+    if (test(S.other[k])) record(k);
   return c;
 }
 
@@ -1180,8 +1201,10 @@ __global__ void __launch_bounds__(kNT, pipe_ctas(MODE)) k_join_nested_pipe(JoinA
   }
 }
 
+// 4 CTAs per SM (64 registers; 3 fit at the uncapped 67): cfg3's large work
+// items 1.33 -> 1.00 ms (8.31 -> 8.08 ms per join), cfg2 neutral (r03e)
 #ifndef PBSM_JOIN_MINB
-#define PBSM_JOIN_MINB 2
+#define PBSM_JOIN_MINB 4
 #endif
 template <bool EMIT>
 __device__ __forceinline__ void k_join_body(JoinArgs& A);

@@ -36,8 +36,8 @@ tmp = Path(tempfile.mkdtemp())
 subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
 cubins = list(tmp.glob("*.cubin"))
 dis = subprocess.run(["nvdisasm", "-g", "-c", str(cubins[0])], capture_output=True, text=True).stdout
-bools = re.findall(r"\(bool\)([01])", kname)
-want = ("I" + "".join(f"Lb{b}E" for b in bools) + "E") if bools else ""
+targs = re.findall(r"\((bool|int)\)(\d+)", kname)
+want = ("I" + "".join(f"L{'b' if t == 'bool' else 'i'}{v}E" for t, v in targs) + "E") if targs else ""
 short = kname.split("(")[0].split("::")[-1].split("<")[0]
 line_of = {}
 cur_fn = None
