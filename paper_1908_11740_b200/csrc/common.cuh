@@ -44,7 +44,7 @@ constexpr int kNT = PBSM_NESTED_THREADS;  // threads of a nested-join CTA
 #define PBSM_NESTED_ROWS 1  // 1: lane per lead entry; 0: pair-flattened lanes
 #endif
 constexpr int kMaxTilesN = kCapN / 2;
-static_assert(kCapN <= 512 && kLmax <= 128, "nested row descriptors: 9-bit positions, 7-bit counts");
+static_assert(kCapN <= 512 && kLmax <= 256, "nested row descriptors: 9-bit positions, 8-bit counts");
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
 #ifndef PBSM_LARGE_OTHER
 #define PBSM_LARGE_OTHER 2048

@@ -631,9 +631,9 @@ struct NestedBuf {               // one staged chunk
 
 struct NestedSmem {
   NestedBuf buf;
-  // row form: per lead entry pos | o0 << 9 | |other| << 18 | R-leads << 25
-  // (positions < kCapN = 512; |other| <= 64: the smaller side of a tile of
-  // <= kLmax = 128 entries)
+  // row form: per lead entry pos | o0 << 9 | |other| << 18 | R-leads << 26
+  // (positions < kCapN = 512; |other| <= kLmax / 2 <= 128: the smaller side
+  // of a tile of <= kLmax entries)
   u32 lead[PBSM_NESTED_ROWS ? kCapN : 1];
   // flat form: tile table, pair-prefix boundaries (tb[nt] = pair total) and
   // 32 sentinels (no bounds check per warp-step)
@@ -838,8 +838,8 @@ __device__ __forceinline__ void nested_rows(const Smem& S, const View& B, double
     const u32 ei = g + lane;
     const bool valid = ei < e_end;
     const u32 d = valid ? S.lead[ei] : 0u;
-    const u32 pos = d & 511u, o0 = (d >> 9) & 511u, nO = valid ? (d >> 18) & 127u : 0u;
-    const bool lr = (d >> 25) & 1u;
+    const u32 pos = d & 511u, o0 = (d >> 9) & 511u, nO = valid ? (d >> 18) & 255u : 0u;
+    const bool lr = (d >> 26) & 1u;
     const ulonglong2 mx = B.ax(pos);
     const double2 my = B.ay(pos);
     const double mxu = __longlong_as_double((long long)mx.y);
@@ -936,7 +936,7 @@ __device__ __forceinline__ void nested_chunk(Smem& S, const View& B, const JoinA
       const bool lr = tr[h].z >= tr[h].w;
       const u32 nL = lr ? tr[h].z : tr[h].w, nO = lr ? tr[h].w : tr[h].z;
       const u32 l0 = lr ? r0 : s0, o0 = lr ? s0 : r0;
-      const u32 d = (o0 << 9) | (nO << 18) | ((u32)lr << 25);
+      const u32 d = (o0 << 9) | (nO << 18) | ((u32)lr << 26);
       for (u32 i = 0; i < nL; ++i) S.lead[pre + i] = (l0 + i) | d;
       pre += nL;
     } else {

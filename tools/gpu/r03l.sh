@@ -1,0 +1,11 @@
+# tile-size thresholds: Lmax 256 (mid tiles leave the large work items), nested_max
+for name in "" _lm256 _lm256n _nm4k _lm192; do
+  for c in 2 3; do
+    PBSM_LIB_NAME=libpbsm$name.so python tools/timeline.py $c 2>/dev/null | python -c "
+import sys,json
+rows=[json.loads(l) for l in sys.stdin]
+print('lib$name cfg$c span', rows[-1]['span_us'], 'durs', [r['dur_us'] for r in rows[:-1]][-4:], 'last starts', [r['start_us'] for r in rows[-4:-1]])"
+  done
+  for c in 2 3 5 4; do PBSM_LIB_NAME=libpbsm$name.so timeout 600 python bench.py --config $c --no-e2e --no-cpu-baseline --sub-configs none --steps 50 2>/dev/null | python -c "
+import sys,json; d=json.loads(sys.stdin.read()); print('lib$name cfg$c bench', round(d['ms_per_step'],4), d['parity']['match'])"; done
+done 2>&1 | tee gpurun_out/r03l_lmax_ab.txt
