@@ -495,6 +495,9 @@ def main():
 
     hbm, peak_kind = peaks()
     B_alg = 40 * (n_r + n_s) + 80 * (A_R + A_S) + 16 * P
+    once = self_join and dev.SELF_ONCE  # one array, partitioned once: its bytes move once
+    if once:
+        B_alg = 40 * n_r + 80 * A_R + 16 * P
     step_gbs = B_alg / step_s / 1e9
     # dominant kernel: the longest device phase
     dev_phases = {k_: v for k_, v in phases.items()
@@ -504,6 +507,8 @@ def main():
     # algorithmic bytes of each phase, per SURVEY §8(d)'s per-unit figures
     n_in = len(rr[0]) + len(ss[0])   # both inputs are partitioned (engine.py:231-232)
     lists = h["list_r"] + h["list_s"]
+    if once:  # ... unless they are one array: one count, one scatter, one list
+        n_in, lists = len(rr[0]), h["list_r"]
     dom_bytes = {
         "count": 32 * n_in,                           # every MBR read once
         "scatter": 40 * n_in + 40 * lists,            # MBR+id read, entry written
@@ -514,7 +519,7 @@ def main():
     }[dom]
     # the dominant phase runs one launch per input (count, scatter) or the
     # nested + sorted/large join launches; report per launch of its kernel
-    n_launch = {"count": 2, "scatter": 2, "bin": 2}.get(dom, 1)
+    n_launch = 1 if once else {"count": 2, "scatter": 2, "bin": 2}.get(dom, 1)
     dom_bytes //= n_launch
     dom_time = dev_phases[dom] / n_launch
     dom_gbs = dom_bytes / dom_time / 1e9
@@ -694,10 +699,16 @@ def time_sub_config(cfg: int, steps: int, device, hbm: float, no_parity: bool) -
     dt = e0.elapsed_time(e1) / 1e3 / steps
     h = res.header
     b_alg = 40 * n + 80 * (h["a_r"] + h["a_s"]) + 16 * res.count
+    once = s is r and dev.SELF_ONCE
+    if once:  # a self-join partitions its one array once: those bytes move once
+        b_alg = 40 * len(r[0]) + 80 * h["a_r"] + 16 * res.count
     out = {"ms_per_step": dt * 1e3, "value": n / dt, "unit": UNIT, "pairs": res.count,
            "a_r": h["a_r"], "a_s": h["a_s"], "steps": steps, "cold_first_join_ms": cold,
            "step_roofline": {"alg_bytes": b_alg, "achieved": b_alg / dt / 1e9, "peak": hbm,
                              "frac": b_alg / dt / 1e9 / hbm, "unit": "GB/s"}}
+    if once:
+        out["self_join"] = ("partitioned once (R is S): B_alg = 40 n_R + 80 A_R + 16 P; the "
+                            "reference partitions the array twice (engine.py:231-232)")
     if not no_parity:
         out["parity"] = parity_record(cfg, res.count, h["a_r"], h["a_s"],
                                       sorted_sha256_device(res.pairs))

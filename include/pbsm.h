@@ -269,6 +269,15 @@ int pbsm_join_emit_eps(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t
                        const pbsm_header* plan, void* scratch, int64_t* pairs,
                        int64_t capacity, int32_t ordered, double eps_sq, void* stream);
 
+/* Self-joins (both inputs the same array) may be partitioned once: count side
+ * 0 only, copy its per-tile counters over side 1's (both live in the
+ * workspace; the shipped host code copies them with a device-to-device copy)
+ * before pbsm_plan, scatter side 0 only, and pass the SAME list (and the same
+ * compact-entry buffer) for both inputs to the join entry points — the two
+ * partitions of the reference (engine.py:231-232) are identical, so the result
+ * is too.  The join entry points recognise r_list == s_list and check the
+ * write guard against side 0's cursors for both sides. */
+
 /* pbsm_join_emit without the host copy of the plan: the kernels read the
  * unit counts from the device header and the grids are the caller's upper
  * bounds (e.g. the previous join's counts), so the pipeline needs no host

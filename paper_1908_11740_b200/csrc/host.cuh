@@ -155,10 +155,17 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
                                   pipe_ctas(split ? (split->few_pairs ? 3 : 2) : eps ? 1 : 0))
           : cn;
   const bool fused_guard = cn > 0 && (i64)L.tiles <= nested_ctas * (i64)kNT * 32;
+  // One list passed for both inputs: a self-join partitioned once (the caller
+  // copied R's counts to S's before the plan and ran one scatter, so S's
+  // cursors never moved): the S side of the write guard reads R's cursors.
+  const bool one_list = (const void*)r_list == (const void*)s_list &&
+                        (!split || split->r32 == split->s32);
+  const u32* g_cur_s = one_list ? w.cur_r : w.cur_s;
+  const u32* g_end_s = one_list ? w.cnt_r : w.cnt_s;
   if (!fused_guard) {
     const unsigned gb = (unsigned)std::max<i64>(1, std::min<i64>((i64)((L.tiles + 255) / 256),
                                                                   (i64)num_sms() * 8));
-    k_guard<<<gb, 256, 0, s>>>(w.cur_r, w.cnt_r, w.cur_s, w.cnt_s, L.tiles, w.hdr);
+    k_guard<<<gb, 256, 0, s>>>(w.cur_r, w.cnt_r, g_cur_s, g_end_s, L.tiles, w.hdr);
   }
   // (a bounded emit is the one join pass behind its plan, whose last CTA left
   // hdr->pairs at zero: no memset node between the scatter and the join —
@@ -190,8 +197,8 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   A.list_cap_s = cap_s;
   A.g_cur_r = w.cur_r;
   A.g_end_r = w.cnt_r;
-  A.g_cur_s = w.cur_s;
-  A.g_end_s = w.cnt_s;
+  A.g_cur_s = g_cur_s;
+  A.g_end_s = g_end_s;
   A.g_tiles = fused_guard ? L.tiles : 0;
   A.eps = eps;
   A.eps_sq = eps_sq;

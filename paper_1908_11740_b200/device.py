@@ -371,6 +371,12 @@ def _banded(lib, b: DeviceRects, side: int, wsp: int, grid, stream, ids_p) -> to
 # size and a miss re-runs the join synchronously.
 _plan_cache: dict = {}
 DUAL = os.environ.get("PBSM_DUAL", "1") != "0"
+# A self-join (s is r) is partitioned ONCE: side 0 is counted and scattered,
+# its counters are copied over side 1's before the plan and the join reads the
+# one list for both inputs — the reference partitions the array twice
+# (engine.py:231-232) into two identical datasets (PBSM_SELF_ONCE=0: as the
+# reference)
+SELF_ONCE = os.environ.get("PBSM_SELF_ONCE", "1") != "0"
 _side_streams: dict = {}
 
 
@@ -726,12 +732,17 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
     if DUAL:
         main_st = torch.cuda.current_stream(device)
         side_st = _side_stream(device, stream)
-    dual = DUAL and cur is None
+    same = SELF_ONCE and s is r and half is None and cur is None and r.ids_ready is None
+    dual = DUAL and cur is None and not same
     if dual:
         fork = torch.cuda.Event()
         fork.record(main_st)
         side_st.wait_event(fork)
     for side, b in ((0, r), (1, s)):
+        if same and side == 1:  # S's counters are R's
+            cnt_r_v, cnt_s_v = _tile_count_views(ws, kx, ky, kx * (row_hi - row_lo))
+            cnt_s_v.copy_(cnt_r_v, non_blocking=True)
+            continue
         _wait(b.coords_ready, cur)
         st_ = side_st.cuda_stream if (dual and side == 1) else stream
         if half is not None:
@@ -769,13 +780,19 @@ def _run_join_impl(r: DeviceRects, s: DeviceRects, kx: int, ky: int, *, collect:
                       guess["count"] if guess is not None else None, late)
     binned = _binned_pair(list_r, list_s, len(r), len(s), bin_bytes, split)
     split = split and not binned
-    dual_sc = DUAL and not binned
+    dual_sc = DUAL and not binned and not same
     split_bufs = []
     if dual_sc:
         fork = torch.cuda.Event()
         fork.record(main_st)
         side_st.wait_event(fork)
     for side, b, total in ((0, r, list_r), (1, s, list_s)):
+        if same and side == 1:  # one scatter: the join reads R's list for both inputs
+            lists.append(lists[0])
+            if split:
+                split_bufs.append(split_bufs[0])
+            mark("scatter")
+            continue
         ent = _buffer(device, f"list{side}", (max(total, 1), 8), torch.int64,
                       stream)  # 64 B records
         ids_p = None if late else _ptr(b.ids)
@@ -1036,8 +1053,10 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
     ws = torch.empty(int(lib.pbsm_workspace_bytes(*grid)), dtype=torch.uint8, device=device)
     wsp = ws.data_ptr()
     list_r, list_s = guess["list_r"], guess["list_s"]
-    lists = [torch.empty((max(list_r, 1), 8), dtype=torch.int64, device=device),
-             torch.empty((max(list_s, 1), 8), dtype=torch.int64, device=device)]
+    same = SELF_ONCE and s is r  # a self-join: one count, one scatter, one list
+    lists = [torch.empty((max(list_r, 1), 8), dtype=torch.int64, device=device)]
+    lists.append(lists[0] if same else
+                 torch.empty((max(list_s, 1), 8), dtype=torch.int64, device=device))
     cap, cn, rest = guess["pairs"], guess["nested"], guess["other"]
     lcap, mtile = guess["large"], guess["max_huge"]
     scratch = torch.empty(int(lib.pbsm_join_scratch_bytes(cn + rest, lcap)), dtype=torch.uint8,
@@ -1050,7 +1069,9 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
     split_bufs = []
     if split:
         split_bufs = [(torch.empty((max(nest[q], 1), 4), dtype=torch.int64, device=device),
-                       max(nest[q], 1)) for q in range(2)]
+                       max(nest[q], 1)) for q in range(1 if same else 2)]
+        if same:
+            split_bufs.append(split_bufs[0])
         g.keep.append(split_bufs)
 
     def fork():
@@ -1064,15 +1085,22 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
         main_st.wait_event(e)
 
     _native.check(lib.pbsm_init(wsp, *grid, stream), "pbsm_init")
-    fork()
-    for side, b in ((0, r), (1, s)):
-        _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
-                                     side, wsp, *grid,
-                                     side_st.cuda_stream if side else stream), "pbsm_count")
-    join()
+    if same:
+        _native.check(lib.pbsm_count(_ptr(r.xl), _ptr(r.xu), _ptr(r.yl), _ptr(r.yu), len(r), 0,
+                                     wsp, *grid, stream), "pbsm_count")
+        cnt_r_v, cnt_s_v = _tile_count_views(ws, kx, ky, kx * (row_hi - row_lo))
+        cnt_s_v.copy_(cnt_r_v, non_blocking=True)
+    else:
+        fork()
+        for side, b in ((0, r), (1, s)):
+            _native.check(lib.pbsm_count(_ptr(b.xl), _ptr(b.xu), _ptr(b.yl), _ptr(b.yu), len(b),
+                                         side, wsp, *grid,
+                                         side_st.cuda_stream if side else stream), "pbsm_count")
+        join()
     _native.check(lib.pbsm_plan(wsp, *grid, nested_max, sweep_min, stream), "pbsm_plan")
-    fork()
-    for side, b, total in ((0, r, list_r), (1, s, list_s)):
+    if not same:
+        fork()
+    for side, b, total in (((0, r, list_r),) if same else ((0, r, list_r), (1, s, list_s))):
         st_ = side_st.cuda_stream if side else stream
         if split:
             rec32, n32 = split_bufs[side]
@@ -1084,7 +1112,8 @@ def _graph_enqueue(lib, g: _Graphed, r: DeviceRects, s: DeviceRects, grid, guess
             _native.check(lib.pbsm_scatter(_ptr(b.ids), _ptr(b.xl), _ptr(b.xu), _ptr(b.yl),
                                            _ptr(b.yu), len(b), side, wsp, *grid,
                                            lists[side].data_ptr(), total, st_), "pbsm_scatter")
-    join()
+    if not same:
+        join()
     if split:
         _emit_split(lib, wsp, grid, lists[0], list_r, lists[1], list_s, split_bufs, r, s, False,
                     None, (cn, rest, lcap, mtile), scratch, g.pairs, cap, stream, guess["count"])

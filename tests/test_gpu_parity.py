@@ -289,6 +289,34 @@ def test_self_join_identity_pairs():
     assert len(diag) == len(r[0])  # every rectangle intersects itself
 
 
+def test_self_join_partitioned_once():
+    """A device-resident self-join (s is r) counts and scatters its array
+    once and joins the one list with itself; the same array passed as two
+    inputs takes the reference's two-partition route (engine.py:231-232).
+    Both give the reference pair list — eager, speculative and graphed."""
+    from paper_1908_11740_b200 import device as dev
+
+    r, _, k = make_config(5, 0.02)
+    want = oracle.sorted_pairs(oracle.join(r, r, "2d", k)["pairs"])
+    Rd, Rd2 = dev.to_device(r, "cuda"), dev.to_device(r, "cuda")
+    two = dev.run_join(Rd, Rd2, k, k)
+    assert np.array_equal(oracle.sorted_pairs(two.pairs.cpu().numpy()), want)
+    for i in range(4):  # exact plan, speculative sizes, graph capture, graph replay
+        one = dev.run_join(Rd, Rd, k, k, graph=i >= 2)
+        assert one.count == two.count
+        assert one.header["a_r"] == one.header["a_s"] == two.header["a_r"]
+        assert np.array_equal(oracle.sorted_pairs(one.pairs.cpu().numpy()), want)
+    # strips, ordered emit and a forced large-tile plan through the same route
+    half = dev.run_join(Rd, Rd, k, k, row_lo=0, row_hi=k // 2)
+    rest = dev.run_join(Rd, Rd, k, k, row_lo=k // 2, row_hi=k)
+    both = np.concatenate([half.pairs.cpu().numpy(), rest.pairs.cpu().numpy()])
+    assert np.array_equal(oracle.sorted_pairs(both), want)
+    coarse = dev.run_join(Rd, Rd, 8, 8, ordered=True)
+    ref8 = oracle.sorted_pairs(oracle.join(r, r, "2d", 8)["pairs"])
+    assert np.array_equal(oracle.sorted_pairs(coarse.pairs.cpu().numpy()), ref8)
+    dev.release_buffers()
+
+
 def test_repeat_runs_identical_sets():
     r, s, k = make_config(4, 0.005)
     R, S = pb.RectBatch(*r), pb.RectBatch(*s)
