@@ -126,7 +126,7 @@ struct __align__(32) Half {  // the MBR half of a record: one sector
 // ---------------------------------------------------------------- workspace
 struct WsLayout {
   size_t hdr, bx, by, cnt_r, cnt_s, cur_r, cur_s, jrec[2], cdesc[2], lrec, lpre, lwin,
-      partials, bc[2], bo, bscan, total;
+      partials, bc[2], bo, bscan, litem, total;
   u64 tiles;
   u64 nblocks;
 };
@@ -159,6 +159,8 @@ inline WsLayout ws_layout(int kx, int ky, int row_lo, int row_hi) {
   }
   L.bo = o; o = align_up(o + 8 * ((size_t)kBinSlots * kMaxPartBlocks + 1), 256);
   L.bscan = o; o = align_up(o + 8 * (((size_t)kBinSlots * kMaxPartBlocks) / 4096 + 2), 256);
+  // large work item → its tile (the first `tiles` items; later ones search lpre)
+  L.litem = o; o = align_up(o + 4 * T, 256);
   L.total = o;
   return L;
 }
@@ -167,7 +169,7 @@ struct Ws {
   pbsm_header* hdr;
   double* bx;
   double* by;
-  u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *lpre, *lwin;
+  u32 *cnt_r, *cnt_s, *cur_r, *cur_s, *lpre, *lwin, *litem;
   uint4* cdesc[2];  // chunk c: {first tile j0, r_start, s_start, -}; [n_chunks] = ends
   uint4* jrec[2];   // {r_start, s_start, nR, nS}
   uint4* lrec;
@@ -199,6 +201,7 @@ inline Ws ws_bind(void* base, const WsLayout& L) {
   for (int q = 0; q < 2; ++q) w.bc[q] = (u32*)(b + L.bc[q]);
   w.bo = (u64*)(b + L.bo);
   w.bscan = (u64*)(b + L.bscan);
+  w.litem = (u32*)(b + L.litem);
   w.tiles = L.tiles;
   w.nblocks = L.nblocks;
   return w;

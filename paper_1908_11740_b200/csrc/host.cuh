@@ -180,6 +180,8 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
   }
   A.lrec = w.lrec;
   A.lpre = w.lpre;
+  A.litem = w.litem;
+  A.litem_n = L.tiles;
   A.ls = large_sort_bind((char*)scratch + join_status_bytes(n_units), lcap);
   A.ls.passes = sort_passes(mtile);
   A.rl = reinterpret_cast<const Rec*>(r_list);

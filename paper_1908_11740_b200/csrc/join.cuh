@@ -9,6 +9,8 @@ struct JoinArgs {
   const uint4* cdesc[2];
   const uint4* lrec;
   const u32* lpre;
+  const u32* litem;  // large work item → tile (items < litem_n; the plan's table)
+  u64 litem_n;
   LargeSort ls;            // huge tiles: sort buffers and the sorted copies (sweep.cuh)
   const Rec* rl;
   const Rec* sl;
@@ -1246,6 +1248,12 @@ __device__ __forceinline__ void k_join_body(JoinArgs& A) {
     const i64 smin = A.hdr->sweep_min;  // (in flight during the search)
     int lo = 0, hi = (int)A.hdr->n_large;  // lpre[0] = 0 <= item
     const int lane = threadIdx.x & 31;
+    // (the plan's item → tile table answers in one load what the search
+    // finds in log32(n_large) dependent ones; items past the table search)
+    if ((u64)item < A.litem_n) {
+      lo = (int)__ldg(A.litem + item);
+      hi = lo + 1;
+    }
     while (hi - lo > 1) {
       const int step = (hi - lo + 31) >> 5;
       const int m = lo + lane * step;

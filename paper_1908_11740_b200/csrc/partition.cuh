@@ -774,6 +774,7 @@ struct PlanOut {
   uint4* lrec;
   u32* lpre;
   u32* lwin;
+  u32* litem;  // [tiles]: large work item → index of its tile in lrec (k_join skips its search)
 };
 
 // the lanes k_plan_apply scans: every lane but the two totals (L_A, L_B)
@@ -872,13 +873,16 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
     } else if (kind == kLarge) {
       r0 = (u32)(rl_base + g(L_LA));
       s0 = (u32)(sl_base + g(L_LB));
-      if (t < T) {
-        P.lrec[g(L_LF)] = make_uint4(r0, s0, a[i], b[i]);
-        P.lpre[g(L_LF)] = (u32)g(L_LI);
-        P.lwin[g(L_LF)] = (u32)g(L_LW);
-      }
       u32 v[kNV];
       tile_vals(a[i], b[i], nm, v, sm);
+      if (t < T) {
+        const u64 lf = g(L_LF), it0 = g(L_LI);
+        P.lrec[lf] = make_uint4(r0, s0, a[i], b[i]);
+        P.lpre[lf] = (u32)it0;
+        P.lwin[lf] = (u32)g(L_LW);
+        // item → tile, for the items the table holds (T of them)
+        for (u64 it = it0; it < it0 + v[L_LI] && it < T; ++it) P.litem[it] = (u32)lf;
+      }
       pre[L_LF - 2] += 1u;
       pre[L_LI - 2] += v[L_LI];
       pre[L_LA - 2] += a[i];

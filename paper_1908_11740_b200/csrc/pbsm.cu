@@ -160,6 +160,7 @@ int pbsm_plan(void* ws, int32_t kx, int32_t ky, int32_t row_lo, int32_t row_hi,
   P.lrec = w.lrec;
   P.lpre = w.lpre;
   P.lwin = w.lwin;
+  P.litem = w.litem;
   k_plan_apply<<<(unsigned)w.nblocks, kPlanThreads, 0, s>>>(w.cnt_r, w.cnt_s, w.tiles,
                                                              w.nblocks, nm, sm, w.partials, P);
   return launch_status();
