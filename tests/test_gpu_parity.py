@@ -586,6 +586,46 @@ def test_speculative_plan_reuse(golden):
     assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
 
 
+def test_fast_replay_follows_the_inputs(golden):
+    """The fast replay of a repeated graphed join (device._fast_replay) is
+    keyed by the input objects and their column addresses: new VALUES in the
+    same tensors are joined afresh (the graph reads the tensors; a size miss
+    falls back to the exact path), other input objects, a replaced column or
+    other options take the general path — always the oracle's pair list."""
+    g = golden["configs"]
+    r, s, k = make_config(2, float(g["cfg2_scale"]))
+    R, S = dev.to_device(r), dev.to_device(s)
+    want = g["cfg2_pairs"]
+    for _ in range(4):  # exact, speculative, graph capture, fast replay
+        res = dev.run_join(R, S, k, k, graph=True)
+        assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+    assert dev._fast
+    # new values in place (denser S: longer lists than the graph was sized for)
+    s2 = tuple(a.copy() for a in s)
+    s2[1][:] = s2[1] * 0.5
+    s2[2][:] = s2[2] * 0.5 + 0.01
+    for col, a in zip(S.columns(), s2):
+        col.copy_(torch.from_numpy(a))
+    ref = oracle.join(r, s2, "2d", k)
+    for _ in range(3):
+        got = dev.run_join(R, S, k, k, graph=True)
+        assert got.count == ref["count"]
+        assert np.array_equal(oracle.sorted_pairs(got.pairs.cpu().numpy()),
+                              oracle.sorted_pairs(ref["pairs"]))
+    # the original values again, in NEW tensors behind the same DeviceRects
+    S.xl, S.xu, S.yl, S.yu = (torch.from_numpy(a).cuda() for a in s[1:])
+    for _ in range(3):
+        res = dev.run_join(R, S, k, k, graph=True)
+        assert np.array_equal(oracle.sorted_pairs(res.pairs.cpu().numpy()), want)
+    # another strip / other options never hit the entry
+    half = dev.run_join(R, S, k, k, graph=True, row_lo=0, row_hi=k // 2)
+    rest = dev.run_join(R, S, k, k, graph=True, row_lo=k // 2, row_hi=k)
+    both = np.concatenate([half.pairs.cpu().numpy(), rest.pairs.cpu().numpy()])
+    assert np.array_equal(oracle.sorted_pairs(both), want)
+    dev.release_buffers()
+    assert not dev._fast
+
+
 @pytest.mark.slow
 def test_speculative_plan_reuse_full_size_overrun():
     """Full-size version of the mismatch: a cfg2-shaped join
