@@ -593,6 +593,35 @@ __device__ __forceinline__ void tile_vals(u32 a, u32 b, i64 nm, u32 v[kNV], i64 
   }
 }
 
+// The plan kernels give thread j of CTA c the kPlanPer = 8 CONSECUTIVE tiles
+// from c * kPlanTile + 8 j: two 16-byte loads per counter array put all of a
+// thread's counts in flight at once (with one 4-byte load per tile and step
+// both kernels sat on their first loads: 59% / 24% of their stall samples),
+// and k_plan_apply writes its four outputs back the same way, with no
+// shared-memory staging.  Tiles past T read as empty.
+static_assert(kPlanPer == 8, "plan kernels: two uint4 per thread and array");
+__device__ __forceinline__ void plan_load8(const u32* __restrict__ c, u64 t0, u64 T, u32 v[8]) {
+  if (t0 + 8 <= T && (t0 & 3) == 0) {
+    const uint4 x = *reinterpret_cast<const uint4*>(c + t0);
+    const uint4 y = *reinterpret_cast<const uint4*>(c + t0 + 4);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = t0 + i < T ? c[t0 + i] : 0u;
+  }
+}
+__device__ __forceinline__ void plan_store8(u32* __restrict__ c, u64 t0, u64 T, const u32 v[8]) {
+  if (t0 + 8 <= T && (t0 & 3) == 0) {
+    *reinterpret_cast<uint4*>(c + t0) = make_uint4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<uint4*>(c + t0 + 4) = make_uint4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (t0 + i < T) c[t0 + i] = v[i];
+  }
+}
+
 __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restrict__ cr,
                                                               const u32* __restrict__ cs,
                                                               u64 T, i64 nm, i64 sm,
@@ -607,11 +636,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan_reduce(const u32* __restr
   for (int q = 0; q < kNV; ++q) acc[q] = 0;
   u32 mx = 0, mh = 0;
   u64 bound = 0;
-  const u64 base = (u64)blockIdx.x * kPlanTile;
+  const u64 t0 = (u64)blockIdx.x * kPlanTile + (u64)threadIdx.x * kPlanPer;
+  u32 av[kPlanPer], bv[kPlanPer];
+  plan_load8(cr, t0, T, av);
+  plan_load8(cs, t0, T, bv);
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
-    const u64 t = base + (u64)i * kPlanThreads + threadIdx.x;
-    const u32 a = t < T ? cr[t] : 0u, b = t < T ? cs[t] : 0u;
+    const u32 a = av[i], b = bv[i];
     u32 v[kNV];
     tile_vals(a, b, nm, v, sm);
 #pragma unroll
@@ -784,10 +815,6 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
                                                              i64 nm, i64 sm,
                                                              const u64* __restrict__ partials,
                                                              PlanOut P) {
-  __shared__ u32 sa[kPlanTile];   // counts, then the tiles' list starts
-  __shared__ u32 sb[kPlanTile];
-  __shared__ u32 ca[kPlanTile];   // counts (for the expected cursor ends)
-  __shared__ u32 cb[kPlanTile];
   __shared__ u32 shs[kPlanThreads / 32][kNA];
   __shared__ u64 shp[2][kNV];  // this CTA's global prefixes, the totals
   const u64 base = (u64)blockIdx.x * kPlanTile;
@@ -797,23 +824,16 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
     const int q = threadIdx.x % kNV;
     shp[threadIdx.x / kNV][q] = partials[(u64)q * (nb + 1) + (threadIdx.x < kNV ? blockIdx.x : nb)];
   }
-  for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
-    const u64 t = base + i;
-    const u32 x = t < T ? cr[t] : 0u, y = t < T ? cs[t] : 0u;
-    sa[i] = x;
-    sb[i] = y;
-    ca[i] = x;
-    cb[i] = y;
-  }
-  __syncthreads();
+  // this thread's 8 consecutive tiles (plan_load8)
+  const u64 t0 = base + (u64)threadIdx.x * kPlanPer;
   u32 a[kPlanPer], b[kPlanPer];
+  plan_load8(cr, t0, T, a);
+  plan_load8(cs, t0, T, b);
   u32 pre[kNA];  // in-CTA exclusive prefixes of lanes 2..11 (u32: a CTA's sums fit)
 #pragma unroll
   for (int q = 0; q < kNA; ++q) pre[q] = 0;
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
-    a[i] = sa[threadIdx.x * kPlanPer + i];
-    b[i] = sb[threadIdx.x * kPlanPer + i];
     u32 v[kNV];
     tile_vals(a[i], b[i], nm, v, sm);
 #pragma unroll
@@ -829,11 +849,10 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
   auto g = [&](int q) -> u64 { return shp[0][q] + pre[q - 2]; };
   const u64 rs_base = shp[1][L_NA], ss_base = shp[1][L_NB];
   const u64 rl_base = shp[1][L_NA] + shp[1][L_SA], sl_base = shp[1][L_NB] + shp[1][L_SB];
-  // (the scan ended with a barrier, so sa/sb may be overwritten now: they
-  // receive the list starts)
+  u32 r0v[kPlanPer], s0v[kPlanPer];  // the tiles' list starts
 #pragma unroll
   for (int i = 0; i < kPlanPer; ++i) {
-    const u64 t = base + (u64)threadIdx.x * kPlanPer + i;
+    const u64 t = t0 + i;
     const int kind = tile_kind(a[i], b[i], nm);
     u32 r0 = kSkip, s0 = kSkip;
     // chunks: consecutive tiles of one strategy whose LAST entry falls in the
@@ -889,20 +908,20 @@ __global__ void __launch_bounds__(kPlanThreads, PBSM_PLAN_MINB) k_plan_apply(u32
       pre[L_LB - 2] += b[i];
       pre[L_LW - 2] += v[L_LW];
     }
-    sa[threadIdx.x * kPlanPer + i] = r0;
-    sb[threadIdx.x * kPlanPer + i] = s0;
+    r0v[i] = r0;
+    s0v[i] = s0;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kPlanTile; i += kPlanThreads) {
-    const u64 t = base + i;
-    if (t < T) {
-      const u32 r0 = sa[i], s0 = sb[i];
-      cr[t] = r0 + ca[i];   // expected end of tile t's R cursor (for k_guard)
-      cs[t] = s0 + cb[i];
-      P.cur_r[t] = r0;
-      P.cur_s[t] = s0;
-    }
+  // cursors start at the list starts; the counters become the expected cursor
+  // ends (for k_guard)
+  plan_store8(P.cur_r, t0, T, r0v);
+  plan_store8(P.cur_s, t0, T, s0v);
+#pragma unroll
+  for (int i = 0; i < kPlanPer; ++i) {
+    r0v[i] += a[i];
+    s0v[i] += b[i];
   }
+  plan_store8(cr, t0, T, r0v);
+  plan_store8(cs, t0, T, s0v);
 }
 
 
