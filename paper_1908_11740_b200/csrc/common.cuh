@@ -47,7 +47,7 @@ constexpr int kMaxTilesN = kCapN / 2;
 static_assert(kCapN <= 512 && kLmax <= 256, "nested row descriptors: 9-bit positions, 8-bit counts");
 constexpr int kLargeLead = kJoinThreads;  // lead-side entries per large work item
 #ifndef PBSM_LARGE_OTHER
-#define PBSM_LARGE_OTHER 2048
+#define PBSM_LARGE_OTHER 1024  // (a bitmap row of 32 words per lead thread; 256-2048 time alike, r03f)
 #endif
 constexpr int kLargeOther = PBSM_LARGE_OTHER;  // other-side entries per large work item
 constexpr int kSweepLeaders = 256;    // leaders per sweep work item (sweep.cuh)

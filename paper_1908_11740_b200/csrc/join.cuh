@@ -77,18 +77,20 @@ struct ChunkSmem {
   int unit, nt, NR, NS;
 };
 
-#ifndef PBSM_LARGE_HITS
-#define PBSM_LARGE_HITS 4096
-#endif
-constexpr int kLargeHitCap = PBSM_LARGE_HITS;  // hits of a large work item kept for the emit
+// Large work items keep their hits as one bitmap row per lead thread (bit k
+// of word w = other entry 32 w + k of the item), word-major so a warp's rows
+// never share a bank: the count pass sets bits without atomics and the emit
+// walks them — every pair is tested exactly once, however many hits an item
+// has (a 4096-entry hit list made every denser item test all its pairs twice;
+// on cfg3 that was most of them).
+constexpr int kLargePiece = 256;  // other-side entries staged per step
+static_assert(kLargeOther % 32 == 0 && kLargePiece % 32 == 0, "bitmap words");
 struct LargeSmem {
-  Rec other[kCap];
-  u32 hit[kLargeHitCap];        // lead thread | other index (in the item) << 8
-  i64 lead_id[kJoinThreads];
+  Rec other[kLargePiece];
+  u32 bits[kLargeOther / 32][kJoinThreads];
   u64 bar;
   u64 scan[kJoinThreads / 32 + 1];
   u64 base;
-  u32 nhit;
   int unit;
 };
 
@@ -347,58 +349,44 @@ __device__ void join_sorted(ChunkSmem& S, const JoinArgs& A, i64 unit, int c) {
 
 // Large join tiles (|R_T|+|S_T| > kLmax): work items of kLargeLead entries of
 // the larger side (one per thread) × kLargeOther entries of the other side,
-// which stream through shared memory.  Every (lead, other) pair is tested with the full
-// closed-interval predicate (intersects, geometry.py:59-61) and the class rule
-// (>= 1 x-in and >= 1 y-in ⇔ Eq. 1 owner tile).
-// LIST: also record each hit (lead thread, other index k0 + k) in the block's
-// hit list while it has room
-template <bool EMIT, bool LIST>
+// which stream through shared memory in pieces.  Every (lead, other) pair is
+// tested once with the full closed-interval predicate (intersects,
+// geometry.py:59-61) and the class rule (>= 1 x-in and >= 1 y-in ⇔ Eq. 1
+// owner tile); a hit sets its bit in the lead thread's bitmap row.
+// One piece of n (<= kLargePiece, staged in S.other) entries, the item's
+// entries [k0, k0 + n): returns the lead's hits among them.
 __device__ __forceinline__ u32 large_pass(LargeSmem& S, int n, bool have, const Half& me,
-                                          bool lead_r, i64 my_id, i64* out, u32 k0,
-                                          double2 mpt, int eps, double eps_sq) {
-  u32 c = 0;
+                                          u32 k0, double2 mpt, int eps, double eps_sq) {
   if (!have) return 0;
+  u32 c = 0;
   const double mxl = key_x(me.xl_key);
   const bool mxin = !(me.xl_key & kXOut), myin = !(me.xl_key & kYOut);
-  // Branch-free test on both 16-byte halves of the record, four entries per
-  // step: with early-outs every iteration was its own load -> compare ->
-  // branch chain (shared-memory latency per test); here the eight loads and
-  // the compares of four entries are in flight together and the rare hits
-  // are handled after them.
+  // Branch-free test on both 16-byte halves of the record: no early-outs, so
+  // the loads and compares of consecutive entries are in flight together
   auto test = [&](const Rec& o) -> bool {
     const ulonglong2 ox = *reinterpret_cast<const ulonglong2*>(&o.xl_key);
     const double2 oy = *reinterpret_cast<const double2*>(&o.yl);
     const u64 ok = ox.x;
     const double oxl = key_x(ok), oxu = __longlong_as_double((long long)ox.y);
-    return (mxl <= oxu) & (oxl <= me.xu) & (me.yl <= oy.y) & (oy.x <= me.yu) &
-           (mxin | !(ok & kXOut)) & (myin | !(ok & kYOut));
+    bool hit = (mxl <= oxu) & (oxl <= me.xu) & (me.yl <= oy.y) & (oy.x <= me.yu) &
+               (mxin | !(ok & kXOut)) & (myin | !(ok & kYOut));
+    if (eps) hit = hit && within_eps(mpt, rec_point(o), eps_sq);
+    return hit;
   };
-  auto record = [&](int k) {
-    const Rec& o = S.other[k];
-    if (eps && !within_eps(mpt, rec_point(o), eps_sq)) return;
-    if (EMIT) {
-      *reinterpret_cast<longlong2*>(out + 2 * (i64)c) =
-          lead_r ? make_longlong2(my_id, o.id) : make_longlong2(o.id, my_id);
-    }
-    if (LIST) {
-      const u32 h = atomicAdd_block(&S.nhit, 1u);
-      if (h < (u32)kLargeHitCap) S.hit[h] = threadIdx.x | ((k0 + (u32)k) << 8);
-    }
-    ++c;
-  };
-  int k = 0;
-  for (; k + 4 <= n; k += 4) {
-    bool h[4];
+  for (int w0 = 0; w0 < n; w0 += 32) {  // (k0 and the piece size are multiples of 32)
+    const int m = min(32, n - w0);
+    u32 word = 0;
+    int k = 0;
+    for (; k + 4 <= m; k += 4) {
+      u32 h = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) h[u] = test(S.other[k + u]);
-    if (h[0] | h[1] | h[2] | h[3]) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (h[u]) record(k + u);
+      for (int u = 0; u < 4; ++u) h |= (u32)test(S.other[w0 + k + u]) << u;
+      word |= h << k;
     }
+    for (; k < m; ++k) word |= (u32)test(S.other[w0 + k]) << k;
+    S.bits[(k0 + (u32)w0) >> 5][threadIdx.x] = word;
+    c += __popc(word);
   }
-  for (; k < n; ++k)
-    if (test(S.other[k])) record(k);
   return c;
 }
 
@@ -427,65 +415,47 @@ __device__ void join_large(LargeSmem& S, const JoinArgs& A, i64 unit, i64 item, 
     my_id = L[a].id;
     if (A.eps) mpt = rec_point(L[a]);
   }
-  if (tid == 0) {
-    mbar_init(&S.bar, 1);
-    S.nhit = 0;
-  }
-  S.lead_id[tid] = my_id;
+  if (tid == 0) mbar_init(&S.bar, 1);
   __syncthreads();
   u32 phase = 0;
   u32 cnt = 0;
-  const int passes = EMIT ? 2 : 1;
-  i64* out = nullptr;
-  bool ok = true;
-  for (int pass = 0; pass < passes; ++pass) {
-    for (u32 ob = o_beg; ob < o_end; ob += kCap) {
-      const int n = (int)min((u32)kCap, o_end - ob);
-      __syncthreads();  // previous piece fully consumed
-      if (tid == 0) {
-        mbar_expect_tx(&S.bar, (u32)n * (u32)sizeof(Rec));
-        bulk_g2s(&S.other[0], O + ob, (u32)n * (u32)sizeof(Rec), &S.bar);
-      }
-      mbar_wait(&S.bar, phase);
-      phase ^= 1u;
-      if (pass == 0) {
-        cnt += large_pass<false, EMIT>(S, n, have, me, lead_r, my_id, nullptr, ob - o_beg, mpt,
-                                       A.eps, A.eps_sq);
-      } else if (ok) {
-        out += 2 * (i64)large_pass<true, false>(S, n, have, me, lead_r, my_id, out, 0, mpt,
-                                                A.eps, A.eps_sq);
-      }
+  for (u32 ob = o_beg; ob < o_end; ob += kLargePiece) {
+    const int n = (int)min((u32)kLargePiece, o_end - ob);
+    if (ob != o_beg) __syncthreads();  // previous piece fully consumed
+    if (tid == 0) {
+      mbar_expect_tx(&S.bar, (u32)n * (u32)sizeof(Rec));
+      bulk_g2s(&S.other[0], O + ob, (u32)n * (u32)sizeof(Rec), &S.bar);
     }
-    if (pass == 0) {
-      u64 total;
-      const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
-      if (!EMIT) {
-        if (tid == 0 && total) atomicAdd(A.total, total);
-        return;
-      }
-      if (tid == 0) S.base = reserve(A, unit, total);
-      __syncthreads();
-      if (total <= (u64)kLargeHitCap) {
-        // every hit is in the list: emit from it (no second pass over the
-        // other side), one coalesced 16-byte store per hit
-        if ((i64)(S.base + total) > A.capacity) {
-          if (tid == 0 && total) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
-          return;
-        }
-        i64* o = A.pairs + 2 * (i64)S.base;
-        for (u32 h = tid; h < (u32)total; h += kJoinThreads) {
-          const u32 v = S.hit[h];
-          const i64 lid = S.lead_id[v & 0xffu];
-          const i64 oid = O[o_beg + (v >> 8)].id;
-          *reinterpret_cast<longlong2*>(o + 2 * (i64)h) =
-              lead_r ? make_longlong2(lid, oid) : make_longlong2(oid, lid);
-        }
-        return;
-      }
-      const i64 start = (i64)(S.base + excl);
-      ok = start + (i64)cnt <= A.capacity;
-      if (!ok && cnt) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
-      out = A.pairs + 2 * start;
+    mbar_wait(&S.bar, phase);
+    phase ^= 1u;
+    cnt += large_pass(S, n, have, me, ob - o_beg, mpt, A.eps, A.eps_sq);
+  }
+  u64 total;
+  const u64 excl = block_excl_scan<kJoinThreads>((u64)cnt, &total, S.scan);
+  if (!EMIT) {
+    if (tid == 0 && total) atomicAdd(A.total, total);
+    return;
+  }
+  if (tid == 0) S.base = reserve(A, unit, total);
+  __syncthreads();
+  if ((i64)(S.base + total) > A.capacity) {
+    if (tid == 0 && total) atomicOr(&A.hdr->error, PBSM_ERR_PAIR_OVERFLOW);
+    return;
+  }
+  if (!cnt) return;
+  // emit: the thread's bitmap row, in other-entry order (its own bits only:
+  // no barrier needed between the passes)
+  i64* out = A.pairs + 2 * (i64)(S.base + excl);
+  const u32 nw = (o_end - o_beg + 31u) >> 5;
+  for (u32 w = 0; w < nw; ++w) {
+    u32 word = S.bits[w][tid];
+    while (word) {
+      const u32 k = (u32)__ffs((int)word) - 1u;
+      word &= word - 1u;
+      const i64 oid = O[o_beg + 32u * w + k].id;
+      *reinterpret_cast<longlong2*>(out) =
+          lead_r ? make_longlong2(my_id, oid) : make_longlong2(oid, my_id);
+      out += 2;
     }
   }
 }

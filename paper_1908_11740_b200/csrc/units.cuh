@@ -34,6 +34,10 @@
 //                   entries over all SMs (persistent CTAs, item ticket)
 #pragma once
 
+// other-side entries per deferred large work item of the unit pipeline (its own
+// constant: the tile-list pipeline's kLargeOther follows its bitmap rows)
+constexpr int kULargeOther = 2048;
+
 constexpr int kUnitMaxW = 4096;        // widest unit, in tile columns
 constexpr int kUnitMaxCells = 32768;   // cells of the P1 histogram (128 KB of shared memory)
 constexpr int kUnitMaxG = 64;          // column groups per tile row
@@ -697,7 +701,7 @@ __device__ __forceinline__ URec ld_urec(const URec* p) {
 
 __device__ __forceinline__ u32 large_items(u32 a, u32 b) {
   const u32 lead = a >= b ? a : b, other = a >= b ? b : a;
-  return ((lead + kLargeLead - 1) / kLargeLead) * ((other + kLargeOther - 1) / kLargeOther);
+  return ((lead + kLargeLead - 1) / kLargeLead) * ((other + kULargeOther - 1) / kULargeOther);
 }
 
 __device__ __forceinline__ i64 map_id(const i64* ids, u32 row) { return ids ? __ldg(ids + row) : (i64)row; }
@@ -1083,7 +1087,7 @@ __global__ void __launch_bounds__(kUJoinThreads, 6) k_uchunks(UJoinArgs A) {
 
 // ---------------------------------------------------------------- P4 deferred tiles
 // Tiles of more than LMAX entries, queued by the units: work items of
-// kLargeLead lead entries (one per thread) × kLargeOther entries of the other
+// kLargeLead lead entries (one per thread) × kULargeOther entries of the other
 // side (streamed through shared memory), every pair tested with the closed
 // predicate and the class rule, count → reserve → emit (hits kept in a list;
 // a second pass re-tests if the list overflows).  Persistent CTAs take items
@@ -1164,10 +1168,10 @@ __global__ void __launch_bounds__(kJoinThreads, 2) k_ularge(UJoinArgs A) {
     const bool lead_r = nR >= nS;
     const u32 no = lead_r ? nS : nR, nl = lead_r ? nR : nS;
     const u32 L = lead_r ? rec.x : rec.y, O = lead_r ? rec.y : rec.x;
-    const u32 nob = (no + kLargeOther - 1) / kLargeOther;
+    const u32 nob = (no + kULargeOther - 1) / kULargeOther;
     const u32 li = (u32)(item - (i64)A.sc.ditem[lo]);
     const u32 a = (li / nob) * kLargeLead + tid;
-    const u32 o_beg = (li % nob) * kLargeOther, o_end = min(no, o_beg + kLargeOther);
+    const u32 o_beg = (li % nob) * kULargeOther, o_end = min(no, o_beg + kULargeOther);
     const bool have = a < nl;
     URec me;
     u32 my_idx = 0;
