@@ -154,7 +154,10 @@ int launch_join(bool emit, bool ordered, void* ws, int kx, int ky, int row_lo, i
           ? std::min<i64>(cn, (i64)num_sms() *
                                   pipe_ctas(split ? (split->few_pairs ? 3 : 2) : eps ? 1 : 0))
           : cn;
-  const bool fused_guard = cn > 0 && (i64)L.tiles <= nested_ctas * (i64)kNT * 32;
+#ifndef PBSM_GUARD_PER
+#define PBSM_GUARD_PER 32  // tiles a nested-join thread may check
+#endif
+  const bool fused_guard = cn > 0 && (i64)L.tiles <= nested_ctas * (i64)kNT * PBSM_GUARD_PER;
   // One list passed for both inputs: a self-join partitioned once (the caller
   // copied R's counts to S's before the plan and ran one scatter, so S's
   // cursors never moved): the S side of the write guard reads R's cursors.

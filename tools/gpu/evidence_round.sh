@@ -1,6 +1,6 @@
 # Final evidence round at HEAD: GPU tests, smoke, both bench arms, launch list + full captures, all-kernel
 # captures, strip emulation, fixed cost, timelines.
-tag=r03zz
+tag=r04
 bash tools/round_cmd.sh $tag 2>&1 | tail -30
 bash tools/gpu/ncu_all.sh $tag 2>&1 | tail -8
 bash tools/gpu/ncu_misc2.sh $tag 2>&1 | tail -3
