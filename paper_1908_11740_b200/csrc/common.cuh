@@ -55,7 +55,7 @@ constexpr int kSweepLeaders = 256;    // leaders per sweep work item (sweep.cuh)
 #define PBSM_SWEEP_MIN (1ll << 26)
 #endif
 // A large tile whose |R_T|*|S_T| exceeds this is sorted + swept (sweep.cuh);
-// smaller ones are brute-forced in work items of 256 x 2048 entries, which
+// smaller ones are brute-forced in work items of 256 x 1024 entries, which
 // on a GPU beats the sort + scan (bounded cost, no divergence) below ~10^8
 // pair tests per tile
 constexpr long long kSweepMin = PBSM_SWEEP_MIN;

@@ -24,7 +24,7 @@
 //                      reserves the chunk's output range, then it emits
 //       k_join         medium tiles: TMA-staged chunk, per-(tile, side) rank
 //                      sort by x-lower + the forward scan (Alg. 1); large
-//                      tiles: work items of 256 lead x 2048 other entries
+//                      tiles: work items of 256 lead x 1024 other entries
 //  The output range is reserved with one atomic per unit (the reference's pair
 //  list is unordered) or, in ordered mode, by a decoupled look-back.
 //
