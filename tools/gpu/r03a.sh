@@ -1,3 +1,4 @@
+# (record of a reverted experiment: the PBSM_CHAIN / PBSM_CHAIN_PDL switches existed only in that build; see profiles/r03a_join_chain_pdl_ab.txt)
 # join chain (one stream, fused R+S count / scatter launches, PDL at every boundary) vs the two-stream graph
 timeout 1400 python -m pytest tests -m gpu -x -q > gpurun_out/r03a_pytest.log 2>&1; echo pytest rc=$?; tail -2 gpurun_out/r03a_pytest.log
 for mode in "0 0" "1 0" "1 1"; do
