@@ -87,8 +87,9 @@ int32_t pbsm_abi_version(void) { return PBSM_ABI_VERSION; }
 #define PBSM_STR(x) PBSM_STR2(x)
 const char* pbsm_build_info(void) {
   return "pbsm sm_100a abi" PBSM_STR(PBSM_ABI_VERSION) ": count+validate / plan / scatter "
-         "(64B records, join tiles only) / guard / mini-joins: nested (cp.async-staged) | "
-         "sort+forward-scan, large (TMA-staged), count->emit; pair groups; B=" PBSM_STR(PBSM_CHUNK_B) " Bn=" PBSM_STR(PBSM_CHUNK_BN) " Lmax=" PBSM_STR(
+         "(join tiles only; 64B records, compact 32B nested entries) / guard / mini-joins: "
+         "nested (persistent, TMA-staged) | sort+forward-scan | large (TMA-staged, hit bitmaps) "
+         "| huge (sort+sweep), count->emit; pair groups; B=" PBSM_STR(PBSM_CHUNK_B) " Bn=" PBSM_STR(PBSM_CHUNK_BN) " Lmax=" PBSM_STR(
              PBSM_LMAX) " nested<=" PBSM_STR(PBSM_NESTED_MAX);
 }
 
